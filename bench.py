@@ -1,0 +1,338 @@
+"""Benchmark of the full-amplitude hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Metric: amplitude-gate updates/s = G * 2^n / time, G = gate instructions of
+the expanded program.  Workload at N=1: BASELINE config 2 -
+the 30-qubit 5x6 grid RQC, 24 cycles, eight cycled CZ patterns, seed 0
+(16 GiB complex128 state, fused schedule).  A step = reset to |0..0> and run
+the whole circuit.  Inputs (the 16 GiB state) are far larger than the 126 MB
+L2, so no explicit flush is needed between steps.
+
+`value` is device-timed with the state resident in HBM (CUDA events on the
+engine's stream, barrier + synchronize around the K timed steps, max over
+ranks).  `e2e` is the same metric through the public API `run_full(program)`
+with the gate records uploaded and the full 2^n amplitude vector downloaded
+to pinned host memory inside the timed region.
+
+N > 1 (torchrun): the path is sharded by global qubits (n = 30 + log2 N, weak
+scaling); see paper_2008_07140_b200/distributed.py.
+
+`--impl reference` times the reference CPU algorithm (the oracle port,
+oracle/qsv_oracle.c, a restatement of qcsim/statevector.py) on the host
+cores over a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "amplitude-gate updates/s"
+UNIT = "amp-gate/s"
+N_BASE = 30
+C2 = (5, 6, 24)
+SEED = 0
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d.get("hbm_gbs", 6650.0), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/qsv_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self) -> dict:
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(n: int):
+    from paper_2008_07140_b200 import workloads
+    from paper_2008_07140_b200.program import parse_program
+
+    if n == N_BASE:
+        text = workloads.rqc_text(*C2, seed=SEED)
+    else:
+        text = workloads.rqc_for_qubits(n, C2[2], SEED)
+    return text, parse_program(text)
+
+
+# --------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference algorithm; test infrastructure)
+# --------------------------------------------------------------------------
+
+
+def cpu_reference_sample(prog, budget_s: float, threads: int | None = None) -> dict:
+    from oracle import oracle as O
+
+    threads = threads or O.cpu_threads()
+    n = prog.qubit_count
+    st = O.init_state(n, workers=threads, max_qubits=n)
+    st.amplitudes[:] = 0  # first touch outside the timed region
+    st.amplitudes[0] = 1
+    insts = [i for i in prog.instructions if i.is_gate]
+    done = 0
+    t0 = time.perf_counter()
+    for inst in insts:
+        O.apply_instruction(st, inst, workers=threads)
+        done += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done * float(1 << n) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {done} of {len(insts)} gates of the n={n} config-2 RQC "
+                      f"({dt:.1f} s, oracle/qsv_oracle.c restating qcsim/statevector.py:73-247, "
+                      f"{threads} threads = WorkerPool({threads}))",
+            "seconds": dt, "gates": done}
+
+
+def run_reference(args) -> None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    n = N_BASE
+    _, prog = workload(n)
+    threads = O.cpu_threads()
+    per_step = args.ref_step_seconds
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_sample(prog, per_step, threads)
+        if i >= args.warmup:
+            vals.append(r)
+    value = statistics.median(v["value"] for v in vals)
+    ms = statistics.median(v["seconds"] for v in vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": f"C2: RQC 5x6 grid, 24 cycles, n={n}, seed {SEED} (bounded CPU sample)",
+                   "n_qubits": n, "gates": len(prog.gate_instructions())},
+        "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+
+def run_gpu(args) -> None:
+    rank, world, local = dist_env()
+    if world > 1:
+        from paper_2008_07140_b200 import distributed
+
+        distributed.bench_main(args)
+        return
+
+    import torch
+
+    from paper_2008_07140_b200 import _native as N
+    from paper_2008_07140_b200 import statevector as SV
+
+    torch.cuda.set_device(local)
+    n = args.qubits or N_BASE
+    text, prog = workload(n)
+    gates_list = prog.gate_instructions()
+    G = len(gates_list)
+    rec = SV.compile_gates(gates_list)
+    L = N.lib()
+    opts = N.options(fuse=not args.unfused, tile_qubits=args.tile, reg_qubits=args.regs,
+                     low_qubits=args.low, profile=True)
+
+    stream = torch.cuda.Stream(device=local)
+    state = SV.init_state(n, max_qubits=n, device=local, stream=stream.cuda_stream)
+    plan = C.c_void_p()
+    N.check(L.qsv_plan_create(rec.ctypes.data, len(rec), n, C.byref(opts), C.byref(plan)))
+    info = N.qsv_plan_info()
+    N.check(L.qsv_plan_summary(plan, C.byref(info)))
+
+    def step(stats):
+        state.set_basis(0)
+        if args.unfused:
+            N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(stats)))
+        else:
+            N.check(L.qsv_plan_execute(state.handle, plan, C.byref(opts), C.byref(stats)))
+
+    for _ in range(args.warmup):
+        step(N.qsv_run_stats())
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    stats = N.qsv_run_stats()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(stats)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    ms_step = total_ms / args.steps
+    value = G * float(1 << n) / (ms_step / 1e3)
+
+    # roofline of the dominant kernel (fused pass kernel): algorithmic bytes per
+    # launch = 2 * 16 * 2^n (read + write every amplitude once)
+    launches = stats.launches
+    avg_launch_ms = stats.kernel_ms / max(1, launches)
+    pk = peaks()
+    bytes_per_launch = 32.0 * float(1 << n)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": args.traffic,
+                "peak_src": pk["src"], "kernel": "pass_kernel<4>" if not args.unfused else "gate_kernel",
+                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
+                "kernel_share_of_step": stats.kernel_ms / total_ms}
+
+    # end to end through the public API: program in, amplitudes out (pinned host)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(1 << n, dtype=torch.complex128, pin_memory=True)
+        hv = host.numpy()
+        e2e_ms = []
+        h2d = int(rec.nbytes)
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            res = SV.run_full(prog, state=state, max_qubits=n, tile_qubits=args.tile, reg_qubits=args.regs,
+                              low_qubits=args.low, fuse=not args.unfused)
+            res.state.download(hv)
+            t1.record(stream)
+            torch.cuda.synchronize()
+            if i:  # first call is warm-up
+                e2e_ms.append(t0.elapsed_time(t1))
+        e2e_t = statistics.median(e2e_ms)
+        e2e = {"value": G * float(1 << n) / (e2e_t / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": (1 << n) * 16, "ms_per_step": e2e_t,
+               "api": "paper_2008_07140_b200.run_full(program) + RunResult.state download"}
+        del host
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_reference_sample(prog, args.cpu_seconds)
+        cpu.pop("seconds", None)
+        cpu.pop("gates", None)
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": {"workload": f"C2: RQC {C2[0]}x{C2[1]} grid, {C2[2]} cycles, 8 CZ patterns, seed {SEED}"
+                               if n == N_BASE else f"RQC n={n}",
+                   "n_qubits": n, "gates": G, "fused": not args.unfused, "passes": int(info.passes),
+                   "stages": int(info.stages), "tile_qubits": int(info.tile_qubits),
+                   "reg_qubits": int(info.reg_qubits), "low_qubits": int(info.low_qubits),
+                   "l2": "state (16 GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": int(launches + args.steps),  # pass kernels + set_basis per step
+        "clocks": clocks,
+    }
+    L.qsv_plan_destroy(plan)
+    state.close()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--qubits", type=int, default=0)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--regs", type=int, default=0)
+    ap.add_argument("--low", type=int, default=0)
+    ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=12.0)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per pass_kernel launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/*
+ * qsv.h - C ABI of libqsv.so, the B200-native full-amplitude state-vector engine.
+ *
+ * The reference (qcsim 0.1.0, pure Python + numba) has no plugin registry; its
+ * seam is function level.  Each entry point below replaces one
+ * reference function; the Python host package paper_2008_07140_b200 binds them
+ * with ctypes (see INTEGRATION.md for the binding a maintainer would add).
+ *
+ *   qsv_create / qsv_set_basis  <- statevector.init_state          statevector.py:52-65
+ *                                  (+ run_full initial_index)      statevector.py:421-423
+ *   qsv_upload / qsv_download   <- StateVector(n, amps, ...)       statevector.py:32-36
+ *                                  / StateVector.amplitudes reads
+ *   qsv_apply_gate              <- _apply_gate (apply_single_qubit,
+ *                                  apply_controlled, apply_two_qubit,
+ *                                  apply_projector)                statevector.py:217-289
+ *   qsv_run / qsv_plan_*        <- the run_full gate loop          statevector.py:425-426
+ *                                  (fused + scheduled; no reference
+ *                                  counterpart: SPEC.md:115 has no fusion)
+ *   qsv_norm_sq                 <- StateVector.norm_sq             statevector.py:42-43
+ *   qsv_prob_bit0               <- probability_bit0                statevector.py:292-295
+ *   qsv_collapse                <- the collapse half of measure    statevector.py:305-307
+ *   qsv_pmeasure                <- pmeasure                        statevector.py:311-328
+ *   qsv_scale                   <- noise renormalisation           noise.py:219-221
+ *   qsv_reduced_density         <- branch_probabilities            noise.py:145-185
+ *
+ * Conventions: amplitudes are complex128 (interleaved
+ * re, im float64), index bit k <-> qubit k (little-endian).  Gate matrices are
+ * row-major with the FIRST target as the matrix MSB (gates.py:3-4); controls
+ * are a bit mask and act on the all-ones block only (gates.py:162-168).
+ *
+ * Every call returns 0 on success or a negative status whose class mirrors
+ * qcsim/errors.py (see QSV_E_*); qsv_last_error() gives the message.  Calls are
+ * asynchronous on the state's stream except readouts, which synchronise.
+ * There is no CPU execution path: without a CUDA device, state calls fail
+ * with QSV_E_DEVICE.  The planning calls (qsv_plan_*) are pure host code.
+ */
+#ifndef QSV_H
+#define QSV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSV_OK 0
+#define QSV_E_PARSE (-2)           /* ParseError             (exit code 2) */
+#define QSV_E_TOO_MANY_QUBITS (-3) /* TooManyQubits          (exit code 3) */
+#define QSV_E_NUMERIC (-4)         /* NumericError           (exit code 4) */
+#define QSV_E_DEVICE (-5)          /* CUDA / NCCL failure, no reference analogue */
+#define QSV_E_UNSUPPORTED (-6)     /* UnsupportedGate        (exit code 2) */
+#define QSV_E_DEGENERATE (-7)      /* DegenerateState        (exit code 4) */
+
+#define QSV_MAX_QUBITS 63
+
+typedef struct qsv_state qsv_state;
+typedef struct qsv_plan qsv_plan;
+
+/* One gate in controlled form: the record of gates.controlled_form (gates.py:150-159). */
+typedef struct qsv_gate {
+    int32_t n_targets;     /* 1 or 2 */
+    int32_t targets[2];    /* targets[0] is the matrix MSB */
+    uint64_t control_mask; /* bit q set <=> control on qubit q; must not overlap targets */
+    double u[32];          /* row-major complex (re,im): 2x2 uses u[0..7], 4x4 u[0..31] */
+} qsv_gate;
+
+/* Scheduling knobs.  Zero means "library default". */
+typedef struct qsv_options {
+    int32_t fuse;        /* 0: one kernel per gate (reference-shaped, unfused)  1: fused passes */
+    int32_t tile_qubits; /* m: qubits resident in one CTA tile (2^m amplitudes in shared memory) */
+    int32_t reg_qubits;  /* r: qubits held in registers per stage (2^r amplitudes per thread) */
+    int32_t low_qubits;  /* L: lowest qubits always in the tile (coalescing) */
+    int32_t profile;     /* 1: time every launch with CUDA events (qsv_run_stats) */
+    int32_t n_global;    /* sharded layout: top n_global qubits are global (not resident) */
+    int32_t reserved[2];
+} qsv_options;
+
+typedef struct qsv_run_stats {
+    int64_t gates;         /* gate records consumed */
+    int64_t passes;        /* HBM passes executed (fused passes or unfused gate kernels) */
+    int64_t stages;        /* register stages (shared-memory round trips) inside passes */
+    int64_t launches;      /* kernels launched by this call */
+    double kernel_ms;      /* sum of event-timed launch durations (profile=1 only) */
+    double max_launch_ms;  /* longest single launch (profile=1 only) */
+    double algorithmic_bytes; /* passes * 2 * 16 * 2^n_local */
+} qsv_run_stats;
+
+typedef struct qsv_plan_info {
+    int32_t n_qubits, tile_qubits, reg_qubits, low_qubits;
+    int64_t gates, passes, stages, ops;
+} qsv_plan_info;
+
+/* One fused pass: a tile of 2^m amplitudes over the qubits in tile_mask. */
+typedef struct qsv_pass_info {
+    uint64_t tile_mask;
+    int32_t m;
+    int32_t n_stages;
+    int64_t n_ops;
+} qsv_pass_info;
+
+#define QSV_OP_MAT1 1  /* 2x2 on register position a               */
+#define QSV_OP_MAT2 2  /* 4x4 on register positions a (MSB), b     */
+#define QSV_OP_DIAG1 3 /* diag(d0,d1) on qubit qa                  */
+#define QSV_OP_DIAG2 4 /* diag(d00,d01,d10,d11) on qubits qa (MSB), qb */
+
+/* One operation of a pass, exported for inspection/validation (tests emulate it). */
+typedef struct qsv_op_info {
+    int32_t stage;         /* stage index inside the pass */
+    int32_t kind;          /* QSV_OP_* */
+    int32_t qa, qb;        /* global qubits acted on (qb = -1 when unused) */
+    uint64_t control_mask; /* global control qubits */
+    uint64_t stage_regs;   /* global qubits held in registers during this stage */
+    double m[32];          /* MAT1: 2x2, MAT2: 4x4, DIAG1: d0,d1, DIAG2: d00..d11 (complex) */
+} qsv_op_info;
+
+const char *qsv_version(void);
+const char *qsv_last_error(void);
+int qsv_device_count(int *out);
+
+/* ---- state lifetime and data movement ---- */
+int qsv_create(int n_qubits, int device, void *stream, qsv_state **out);
+int qsv_create_on(int n_qubits, int device, void *stream, void *device_amplitudes, qsv_state **out);
+int qsv_destroy(qsv_state *st);
+int qsv_device_ptr(qsv_state *st, void **out);
+int qsv_set_basis(qsv_state *st, uint64_t index);
+int qsv_upload(qsv_state *st, const void *host_c128, uint64_t offset, uint64_t count);
+int qsv_download(qsv_state *st, void *host_c128, uint64_t offset, uint64_t count);
+int qsv_synchronize(qsv_state *st);
+
+/* ---- gate application ---- */
+int qsv_apply_gate(qsv_state *st, const qsv_gate *gate);
+int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
+            qsv_run_stats *stats);
+
+/* ---- planning (host only; usable without a GPU) ---- */
+int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const qsv_options *opt,
+                    qsv_plan **out);
+int qsv_plan_destroy(qsv_plan *plan);
+int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out);
+int qsv_plan_pass(const qsv_plan *plan, int64_t pass, qsv_pass_info *out);
+int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out);
+int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats);
+
+/* ---- readout (synchronous) ---- */
+int qsv_norm_sq(qsv_state *st, double *out);
+int qsv_prob_bit0(qsv_state *st, int k, double *out);
+int qsv_collapse(qsv_state *st, int k, int outcome, double scale);
+int qsv_scale(qsv_state *st, double scale);
+int qsv_pmeasure(qsv_state *st, const int32_t *qubits_msb_first, int m, double *table);
+int qsv_inner(qsv_state *st, const void *other_device_c128, double *re, double *im);
+int qsv_max_abs_diff(qsv_state *st, const void *other_device_c128, double *out);
+/* reduced density matrix of 1 or 2 qubits (first listed = MSB), row-major complex
+ * 2^nq x 2^nq; branch weights ||K psi||^2 = tr(K rho K^dag) (noise.py:173-185) */
+int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits_msb_first, double *out_c128);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSV_H */

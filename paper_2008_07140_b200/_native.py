@@ -1,0 +1,138 @@
+"""ctypes binding of libqsv.so (include/qsv.h).
+
+Loading is strict: if the library is missing or a CUDA call fails, the
+caller gets an exception - there is no eager/CPU substitute anywhere in the
+package.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+from .errors import NativeLibraryMissing, raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "libqsv.so"
+
+QSV_OP_MAT1, QSV_OP_MAT2, QSV_OP_DIAG1, QSV_OP_DIAG2 = 1, 2, 3, 4
+
+# numpy mirror of `qsv_gate` (C layout: int32 n_targets, int32 targets[2],
+# uint64 control_mask, double u[32]) - built in bulk from a Program
+GATE_DTYPE = np.dtype([("n_targets", "<i4"), ("targets", "<i4", (2,)),
+                       ("control_mask", "<u8"), ("u", "<f8", (32,))], align=True)
+
+
+class qsv_options(C.Structure):
+    _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
+                ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
+
+
+class qsv_run_stats(C.Structure):
+    _fields_ = [("gates", C.c_int64), ("passes", C.c_int64), ("stages", C.c_int64),
+                ("launches", C.c_int64), ("kernel_ms", C.c_double), ("max_launch_ms", C.c_double),
+                ("algorithmic_bytes", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class qsv_plan_info(C.Structure):
+    _fields_ = [("n_qubits", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
+                ("low_qubits", C.c_int32), ("gates", C.c_int64), ("passes", C.c_int64),
+                ("stages", C.c_int64), ("ops", C.c_int64)]
+
+
+class qsv_pass_info(C.Structure):
+    _fields_ = [("tile_mask", C.c_uint64), ("m", C.c_int32), ("n_stages", C.c_int32),
+                ("n_ops", C.c_int64)]
+
+
+class qsv_op_info(C.Structure):
+    _fields_ = [("stage", C.c_int32), ("kind", C.c_int32), ("qa", C.c_int32), ("qb", C.c_int32),
+                ("control_mask", C.c_uint64), ("stage_regs", C.c_uint64), ("m", C.c_double * 32)]
+
+
+_P = C.c_void_p
+_SIGNATURES = {
+    "qsv_version": ([], C.c_char_p),
+    "qsv_last_error": ([], C.c_char_p),
+    "qsv_device_count": ([C.POINTER(C.c_int)], C.c_int),
+    "qsv_create": ([C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),
+    "qsv_create_on": ([C.c_int, C.c_int, _P, _P, C.POINTER(_P)], C.c_int),
+    "qsv_destroy": ([_P], C.c_int),
+    "qsv_device_ptr": ([_P, C.POINTER(_P)], C.c_int),
+    "qsv_set_basis": ([_P, C.c_uint64], C.c_int),
+    "qsv_upload": ([_P, _P, C.c_uint64, C.c_uint64], C.c_int),
+    "qsv_download": ([_P, _P, C.c_uint64, C.c_uint64], C.c_int),
+    "qsv_synchronize": ([_P], C.c_int),
+    "qsv_apply_gate": ([_P, _P], C.c_int),
+    "qsv_run": ([_P, _P, C.c_int64, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),
+    "qsv_plan_create": ([_P, C.c_int64, C.c_int, C.POINTER(qsv_options), C.POINTER(_P)], C.c_int),
+    "qsv_plan_destroy": ([_P], C.c_int),
+    "qsv_plan_summary": ([_P, C.POINTER(qsv_plan_info)], C.c_int),
+    "qsv_plan_pass": ([_P, C.c_int64, C.POINTER(qsv_pass_info)], C.c_int),
+    "qsv_plan_op": ([_P, C.c_int64, C.c_int64, C.POINTER(qsv_op_info)], C.c_int),
+    "qsv_plan_execute": ([_P, _P, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),
+    "qsv_norm_sq": ([_P, C.POINTER(C.c_double)], C.c_int),
+    "qsv_prob_bit0": ([_P, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "qsv_collapse": ([_P, C.c_int, C.c_int, C.c_double], C.c_int),
+    "qsv_scale": ([_P, C.c_double], C.c_int),
+    "qsv_pmeasure": ([_P, _P, C.c_int, _P], C.c_int),
+    "qsv_inner": ([_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+    "qsv_max_abs_diff": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
+    "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def lib():
+    """The loaded library (raises NativeLibraryMissing when it is not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is not built; run `python -m paper_2008_07140_b200.build_native` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise_for_status(rc, lib().qsv_last_error().decode(errors="replace"))
+
+
+def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0) -> qsv_options:
+    o = qsv_options()
+    o.fuse, o.tile_qubits, o.reg_qubits = int(bool(fuse)), int(tile_qubits), int(reg_qubits)
+    o.low_qubits, o.profile, o.n_global = int(low_qubits), int(bool(profile)), int(n_global)
+    return o
+
+
+def gate_records(items) -> np.ndarray:
+    """Pack (base matrix, targets, controls) triples into a qsv_gate array."""
+    items = list(items)
+    rec = np.zeros(len(items), dtype=GATE_DTYPE)
+    for i, (u, targets, controls) in enumerate(items):
+        u = np.asarray(u, dtype=np.complex128)
+        nt = len(targets)
+        rec["n_targets"][i] = nt
+        rec["targets"][i, :nt] = targets
+        mask = 0
+        for c in controls:
+            mask |= 1 << int(c)
+        rec["control_mask"][i] = mask
+        flat = u.reshape(-1)
+        rec["u"][i, : 2 * flat.size] = flat.view(np.float64)
+    return rec

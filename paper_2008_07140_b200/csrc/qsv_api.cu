@@ -1,0 +1,617 @@
+// C ABI of libqsv.so (declared in include/qsv.h).  Launch logic for the
+// kernels in qsv_kernels.cuh and the schedule built by qsv_plan.cpp.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/qsv.h"
+#include "qsv_kernels.cuh"
+#include "qsv_plan.h"
+
+using namespace qsv;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string &msg) {
+    g_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                           \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            return fail(QSV_E_DEVICE, std::string(#expr) + ": " + cudaGetErrorString(_e));       \
+    } while (0)
+
+constexpr int kReduceBlocks = 148 * 8;  // fixed grid: deterministic reduction order
+constexpr int kReduceThreads = 256;
+constexpr int kPmeasureSmallBits = 12;
+
+}  // namespace
+
+struct qsv_state {
+    int n = 0;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    double2 *amps = nullptr;
+    bool own_mem = false;
+    double *work = nullptr;  // reduction partials / pmeasure partials
+    size_t work_bytes = 0;
+    double *result = nullptr;  // 2 doubles
+    void *plan_buf = nullptr;  // scratch for one-shot plans
+    size_t plan_buf_bytes = 0;
+    int sm_count = 148;
+    uint64_t size() const { return 1ull << n; }
+};
+
+struct qsv_plan {
+    Plan p;
+};
+
+namespace {
+
+int grid_for(uint64_t items, int threads, int sm_count) {
+    const uint64_t want = (items + threads - 1) / threads;
+    const uint64_t cap = (uint64_t)sm_count * 32;
+    return (int)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+int ensure_work(qsv_state *st, size_t bytes) {
+    if (st->work_bytes >= bytes) return QSV_OK;
+    if (st->work) cudaFree(st->work);
+    st->work = nullptr;
+    st->work_bytes = 0;
+    CUDA_TRY(cudaMalloc(&st->work, bytes));
+    st->work_bytes = bytes;
+    return QSV_OK;
+}
+
+int set_device(int dev) {
+    CUDA_TRY(cudaSetDevice(dev));
+    return QSV_OK;
+}
+
+// Timer for profile=1: one event pair per launch.
+struct LaunchTimer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    void begin() {
+        if (!on) return;
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        ev.push_back({a, b});
+    }
+    void end() {
+        if (on) cudaEventRecord(ev.back().second, s);
+    }
+    void collect(qsv_run_stats *stats) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        double tot = 0, mx = 0;
+        for (auto &p : ev) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, p.first, p.second);
+            tot += ms;
+            mx = std::max(mx, (double)ms);
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        ev.clear();
+        if (stats) {
+            stats->kernel_ms += tot;
+            stats->max_launch_ms = std::max(stats->max_launch_ms, mx);
+        }
+    }
+};
+
+size_t pass_smem_bytes(int m) { return ((size_t)16 << m) + sizeof(uint64_t) * ((1 << kLoTabBits) + (1 << kHiTabBits)); }
+
+template <int R>
+int configure_pass_kernel() {
+    static bool done = false;
+    if (!done) {
+        CUDA_TRY(cudaFuncSetAttribute(pass_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)pass_smem_bytes(kMaxTileQubits)));
+        done = true;
+    }
+    return QSV_OK;
+}
+
+int launch_pass(qsv_state *st, const Plan &P, int pass_idx, const DevPass *d_pass, const DevStage *d_st,
+                const DevOp *d_ops) {
+    const int m = P.m, r = P.r;
+    const uint64_t n_tiles = 1ull << (st->n - m);
+    const int threads = 1 << (m - r);
+    const uint64_t grid = std::min<uint64_t>(n_tiles, 0x7fffffffull);
+    const size_t smem = pass_smem_bytes(m);
+    const DevPass *pp = d_pass + pass_idx;
+    int rc = QSV_OK;
+    switch (r) {
+        case 1: rc = configure_pass_kernel<1>(); if (!rc) pass_kernel<1><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
+        case 2: rc = configure_pass_kernel<2>(); if (!rc) pass_kernel<2><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
+        case 3: rc = configure_pass_kernel<3>(); if (!rc) pass_kernel<3><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
+        case 4: rc = configure_pass_kernel<4>(); if (!rc) pass_kernel<4><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
+        default: return fail(QSV_E_UNSUPPORTED, "register qubits must be 1..4");
+    }
+    if (rc) return rc;
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+// Uploads plan tables into `buf` (device) laid out as [passes | stages | ops].
+int upload_plan(qsv_state *st, const Plan &P, void *buf, DevPass **dp, DevStage **ds, DevOp **dop) {
+    const size_t bp = P.passes.size() * sizeof(DevPass), bs = P.stages.size() * sizeof(DevStage),
+                 bo = std::max<size_t>(1, P.ops.size()) * sizeof(DevOp);
+    char *b = (char *)buf;
+    *dp = (DevPass *)b;
+    *ds = (DevStage *)(b + bp);
+    *dop = (DevOp *)(b + bp + bs);
+    if (bp) CUDA_TRY(cudaMemcpyAsync(*dp, P.passes.data(), bp, cudaMemcpyHostToDevice, st->stream));
+    if (bs) CUDA_TRY(cudaMemcpyAsync(*ds, P.stages.data(), bs, cudaMemcpyHostToDevice, st->stream));
+    if (!P.ops.empty()) CUDA_TRY(cudaMemcpyAsync(*dop, P.ops.data(), P.ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, st->stream));
+    (void)bo;
+    return QSV_OK;
+}
+
+size_t plan_bytes(const Plan &P) {
+    return P.passes.size() * sizeof(DevPass) + P.stages.size() * sizeof(DevStage) +
+           std::max<size_t>(1, P.ops.size()) * sizeof(DevOp);
+}
+
+int execute_plan(qsv_state *st, const Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, bool profile,
+                 qsv_run_stats *stats) {
+    LaunchTimer tm;
+    tm.on = profile;
+    tm.s = st->stream;
+    for (size_t i = 0; i < P.passes.size(); ++i) {
+        tm.begin();
+        int rc = launch_pass(st, P, (int)i, dp, ds, dop);
+        tm.end();
+        if (rc) return rc;
+    }
+    tm.collect(stats);
+    if (stats) {
+        stats->gates += P.gates;
+        stats->passes += (int64_t)P.passes.size();
+        stats->stages += (int64_t)P.stages.size();
+        stats->launches += (int64_t)P.passes.size();
+        stats->algorithmic_bytes += (double)P.passes.size() * 32.0 * (double)st->size();
+    }
+    return QSV_OK;
+}
+
+int launch_gate(qsv_state *st, const GateRec &g) {
+    GateArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.nt = g.nt;
+    a.t0 = g.t[0];
+    a.t1 = g.nt == 2 ? g.t[1] : 0;
+    a.cmask = g.cmask;
+    const int d = 1 << g.nt;
+    for (int k = 0; k < d * d; ++k) a.u[k] = make_double2(g.u[k].real(), g.u[k].imag());
+    std::vector<int> ins;
+    for (int q = 0; q < st->n; ++q)
+        if ((g.cmask >> q) & 1) ins.push_back(q);
+    if (g.diag) {
+        // diagonal: visit every amplitude whose controls are set; d[] = diagonal entries
+        for (int k = 0; k < d; ++k) a.u[k] = make_double2(g.u[k * d + k].real(), g.u[k * d + k].imag());
+        a.n_ins = (int)ins.size();
+        std::copy(ins.begin(), ins.end(), a.ins);
+        const uint64_t n_idx = st->size() >> ins.size();
+        diag_kernel<<<grid_for(n_idx, 256, st->sm_count), 256, 0, st->stream>>>(st->amps, a, n_idx);
+    } else {
+        for (int k = 0; k < g.nt; ++k) ins.push_back(g.t[k]);
+        std::sort(ins.begin(), ins.end());
+        a.n_ins = (int)ins.size();
+        std::copy(ins.begin(), ins.end(), a.ins);
+        const uint64_t n_groups = st->size() >> ins.size();
+        gate_kernel<<<grid_for(n_groups, 256, st->sm_count), 256, 0, st->stream>>>(st->amps, a, n_groups);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+int reduce(qsv_state *st, int mode, int k, const void *other, double *out2) {
+    int rc = ensure_work(st, sizeof(double) * 2 * kReduceBlocks);
+    if (rc) return rc;
+    reduce_kernel<<<kReduceBlocks, kReduceThreads, 0, st->stream>>>(st->amps, (const double2 *)other, st->size(),
+                                                                    mode, k, st->work);
+    finish_kernel<<<1, 1024, 0, st->stream>>>(st->work, kReduceBlocks, mode, st->result);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out2, st->result, 2 * sizeof(double), cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *qsv_version(void) { return "qsv 0.1.0 (sm_100a)"; }
+
+const char *qsv_last_error(void) { return g_error.c_str(); }
+
+int qsv_device_count(int *out) {
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *out = 0;
+        return fail(QSV_E_DEVICE, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return QSV_OK;
+}
+
+static int create_impl(int n, int device, void *stream, void *mem, qsv_state **out) {
+    *out = nullptr;
+    if (n < 1 || n > QSV_MAX_QUBITS) return fail(QSV_E_TOO_MANY_QUBITS, "qubit count " + std::to_string(n) + " outside [1, 63]");
+    int rc = set_device(device);
+    if (rc) return rc;
+    auto st = std::make_unique<qsv_state>();
+    st->n = n;
+    st->device = device;
+    cudaDeviceGetAttribute(&st->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (stream == (void *)-1) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+        st->own_stream = true;
+    } else {
+        st->stream = (cudaStream_t)stream;
+    }
+    if (mem) {
+        st->amps = (double2 *)mem;
+    } else {
+        const size_t bytes = (size_t)16 << n;
+        cudaError_t e = cudaMalloc(&st->amps, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            if (st->own_stream) cudaStreamDestroy(st->stream);
+            return fail(QSV_E_TOO_MANY_QUBITS, "cannot allocate " + std::to_string(bytes) + " bytes for " +
+                                                   std::to_string(n) + " qubits: " + cudaGetErrorString(e));
+        }
+        st->own_mem = true;
+    }
+    CUDA_TRY(cudaMalloc(&st->result, 32 * sizeof(double)));
+    *out = st.release();
+    return qsv_set_basis(*out, 0);
+}
+
+int qsv_create(int n_qubits, int device, void *stream, qsv_state **out) {
+    return create_impl(n_qubits, device, stream, nullptr, out);
+}
+
+int qsv_create_on(int n_qubits, int device, void *stream, void *device_amplitudes, qsv_state **out) {
+    if (!device_amplitudes) return fail(QSV_E_PARSE, "null device buffer");
+    return create_impl(n_qubits, device, stream, device_amplitudes, out);
+}
+
+int qsv_destroy(qsv_state *st) {
+    if (!st) return QSV_OK;
+    cudaSetDevice(st->device);
+    cudaStreamSynchronize(st->stream);
+    if (st->own_mem) cudaFree(st->amps);
+    if (st->work) cudaFree(st->work);
+    if (st->result) cudaFree(st->result);
+    if (st->plan_buf) cudaFree(st->plan_buf);
+    if (st->own_stream) cudaStreamDestroy(st->stream);
+    delete st;
+    return QSV_OK;
+}
+
+int qsv_device_ptr(qsv_state *st, void **out) {
+    *out = st->amps;
+    return QSV_OK;
+}
+
+int qsv_set_basis(qsv_state *st, uint64_t index) {
+    if (index >= st->size()) return fail(QSV_E_PARSE, "basis index out of range");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    set_basis_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), index);
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+int qsv_upload(qsv_state *st, const void *host, uint64_t offset, uint64_t count) {
+    if (offset + count > st->size()) return fail(QSV_E_PARSE, "upload range out of bounds");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(st->amps + offset, host, count * 16, cudaMemcpyHostToDevice, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
+    if (offset + count > st->size()) return fail(QSV_E_PARSE, "download range out of bounds");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(host, st->amps + offset, count * 16, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_synchronize(qsv_state *st) {
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_apply_gate(qsv_state *st, const qsv_gate *gate) {
+    std::vector<GateRec> recs;
+    std::string msg;
+    int rc = to_records(gate, 1, st->n, recs, msg);
+    if (rc) return fail(rc, msg);
+    rc = set_device(st->device);
+    if (rc) return rc;
+    return launch_gate(st, recs[0]);
+}
+
+int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const qsv_options *opt, qsv_plan **out) {
+    *out = nullptr;
+    if (n_qubits < 1 || n_qubits > QSV_MAX_QUBITS) return fail(QSV_E_TOO_MANY_QUBITS, "qubit count out of range");
+    std::vector<GateRec> recs;
+    std::string msg;
+    int rc = to_records(gates, n_gates, n_qubits, recs, msg);
+    if (rc) return fail(rc, msg);
+    int m, r, L;
+    resolve_options(opt, n_qubits, m, r, L);
+    auto p = std::make_unique<qsv_plan>();
+    p->p = build_plan(recs, n_qubits, m, r, L);
+    *out = p.release();
+    return QSV_OK;
+}
+
+int qsv_plan_destroy(qsv_plan *plan) {
+    if (!plan) return QSV_OK;
+    if (plan->p.d_passes) {
+        cudaSetDevice(plan->p.device);
+        cudaFree(plan->p.d_passes);
+    }
+    delete plan;
+    return QSV_OK;
+}
+
+int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out) {
+    const Plan &P = plan->p;
+    out->n_qubits = P.n;
+    out->tile_qubits = P.m;
+    out->reg_qubits = P.r;
+    out->low_qubits = P.L;
+    out->gates = P.gates;
+    out->passes = (int64_t)P.passes.size();
+    out->stages = (int64_t)P.stages.size();
+    out->ops = (int64_t)P.ops.size();
+    return QSV_OK;
+}
+
+int qsv_plan_pass(const qsv_plan *plan, int64_t pass, qsv_pass_info *out) {
+    const Plan &P = plan->p;
+    if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
+    const DevPass &d = P.passes[pass];
+    out->tile_mask = d.tile_mask;
+    out->m = d.m;
+    out->n_stages = d.stage_end - d.stage_begin;
+    out->n_ops = P.pass_op_begin[pass + 1] - P.pass_op_begin[pass];
+    return QSV_OK;
+}
+
+int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out) {
+    const Plan &P = plan->p;
+    if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
+    const int64_t g = P.pass_op_begin[pass] + op;
+    if (op < 0 || g >= P.pass_op_begin[pass + 1]) return fail(QSV_E_PARSE, "op index out of range");
+    const DevOp &d = P.ops[g];
+    const DevPass &dp = P.passes[pass];
+    std::memset(out, 0, sizeof(*out));
+    out->stage = P.op_stage[g];
+    out->kind = d.kind;
+    out->qa = d.qa;
+    out->qb = d.qb;
+    uint64_t cm = d.cmask_ext;
+    for (int j = 0; j < dp.m; ++j)
+        if ((d.cmask_local >> j) & 1) cm |= 1ull << dp.tq[j];
+    out->control_mask = cm;
+    out->stage_regs = P.stage_regs[dp.stage_begin + out->stage];
+    std::memcpy(out->m, d.m, sizeof(d.m));
+    return QSV_OK;
+}
+
+int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats) {
+    Plan &P = plan->p;
+    if (P.n != st->n) return fail(QSV_E_PARSE, "plan built for a different qubit count");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    if (!P.d_passes || P.device != st->device) {
+        if (P.d_passes) {
+            cudaSetDevice(P.device);
+            cudaFree(P.d_passes);
+            cudaSetDevice(st->device);
+        }
+        CUDA_TRY(cudaMalloc(&P.d_passes, plan_bytes(P)));
+        P.device = st->device;
+        DevPass *dp;
+        DevStage *ds;
+        DevOp *dop;
+        rc = upload_plan(st, P, P.d_passes, &dp, &ds, &dop);
+        if (rc) return rc;
+        P.d_stages = ds;
+        P.d_ops = dop;
+    }
+    return execute_plan(st, P, (DevPass *)P.d_passes, (DevStage *)P.d_stages, (DevOp *)P.d_ops,
+                        opt && opt->profile, stats);
+}
+
+int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt, qsv_run_stats *stats) {
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    std::vector<GateRec> recs;
+    std::string msg;
+    rc = to_records(gates, n_gates, st->n, recs, msg);
+    if (rc) return fail(rc, msg);
+    const bool fuse = !opt || opt->fuse;
+    if (!fuse) {
+        LaunchTimer tm;
+        tm.on = opt && opt->profile;
+        tm.s = st->stream;
+        for (const GateRec &g : recs) {
+            tm.begin();
+            rc = launch_gate(st, g);
+            tm.end();
+            if (rc) return rc;
+        }
+        tm.collect(stats);
+        if (stats) {
+            stats->gates += (int64_t)recs.size();
+            stats->passes += (int64_t)recs.size();
+            stats->launches += (int64_t)recs.size();
+            stats->algorithmic_bytes += (double)recs.size() * 32.0 * (double)st->size();
+        }
+        return QSV_OK;
+    }
+    if (recs.empty()) return QSV_OK;
+    int m, r, L;
+    resolve_options(opt, st->n, m, r, L);
+    Plan P = build_plan(recs, st->n, m, r, L);
+    const size_t bytes = plan_bytes(P);
+    if (st->plan_buf_bytes < bytes) {
+        if (st->plan_buf) {
+            CUDA_TRY(cudaStreamSynchronize(st->stream));
+            cudaFree(st->plan_buf);
+        }
+        st->plan_buf = nullptr;
+        st->plan_buf_bytes = 0;
+        CUDA_TRY(cudaMalloc(&st->plan_buf, bytes));
+        st->plan_buf_bytes = bytes;
+    }
+    DevPass *dp;
+    DevStage *ds;
+    DevOp *dop;
+    rc = upload_plan(st, P, st->plan_buf, &dp, &ds, &dop);
+    if (rc) return rc;
+    return execute_plan(st, P, dp, ds, dop, opt && opt->profile, stats);
+}
+
+int qsv_norm_sq(qsv_state *st, double *out) {
+    double r[2];
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = reduce(st, 0, 0, nullptr, r);
+    *out = r[0];
+    return rc;
+}
+
+int qsv_prob_bit0(qsv_state *st, int k, double *out) {
+    if (k < 0 || k >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
+    double r[2];
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = reduce(st, 1, k, nullptr, r);
+    *out = r[0];
+    return rc;
+}
+
+int qsv_inner(qsv_state *st, const void *other, double *re, double *im) {
+    double r[2];
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = reduce(st, 2, 0, other, r);
+    *re = r[0];
+    *im = r[1];
+    return rc;
+}
+
+int qsv_max_abs_diff(qsv_state *st, const void *other, double *out) {
+    double r[2];
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = reduce(st, 3, 0, other, r);
+    *out = r[0];
+    return rc;
+}
+
+int qsv_collapse(qsv_state *st, int k, int outcome, double scale) {
+    if (k < 0 || k >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    collapse_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), k,
+                                                                                    outcome, scale);
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+int qsv_scale(qsv_state *st, double scale) {
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    collapse_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), -1, 0,
+                                                                                    scale);
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
+    if (m < 1 || m > st->n) return fail(QSV_E_PARSE, "pmeasure qubit count out of range");
+    for (int p = 0; p < m; ++p)
+        if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "pmeasure qubit out of range");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    const size_t bins = (size_t)1 << m;
+    int *d_q = nullptr;
+    double *d_table = nullptr;
+    CUDA_TRY(cudaMallocAsync(&d_q, sizeof(int) * m, st->stream));
+    CUDA_TRY(cudaMemcpyAsync(d_q, qubits, sizeof(int) * m, cudaMemcpyHostToDevice, st->stream));
+    CUDA_TRY(cudaMallocAsync(&d_table, sizeof(double) * bins, st->stream));
+    if (m <= kPmeasureSmallBits) {
+        const int blocks = 148 * 2;
+        rc = ensure_work(st, sizeof(double) * bins * blocks);
+        if (rc) return rc;
+        pmeasure_kernel<<<blocks, 256, sizeof(double) * bins, st->stream>>>(st->amps, st->size(), m, d_q, st->work);
+        pmeasure_finish<<<(unsigned)((bins + 255) / 256), 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
+    } else {
+        CUDA_TRY(cudaMemsetAsync(d_table, 0, sizeof(double) * bins, st->stream));
+        pmeasure_global_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(),
+                                                                                               m, d_q, d_table);
+    }
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(table, d_table, sizeof(double) * bins, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaFreeAsync(d_q, st->stream));
+    CUDA_TRY(cudaFreeAsync(d_table, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *out) {
+    if (nq < 1 || nq > 2) return fail(QSV_E_UNSUPPORTED, "reduced density of 1 or 2 qubits only");
+    for (int p = 0; p < nq; ++p)
+        if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
+    if (nq == 2 && qubits[0] == qubits[1]) return fail(QSV_E_PARSE, "repeated qubit");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    const int D = 1 << nq, vals = 2 * D * D;
+    const int blocks = kReduceBlocks;
+    rc = ensure_work(st, sizeof(double) * vals * blocks);
+    if (rc) return rc;
+    const int lo = nq == 2 ? std::min(qubits[0], qubits[1]) : qubits[0];
+    const int hi = nq == 2 ? std::max(qubits[0], qubits[1]) : qubits[0];
+    const uint64_t groups = st->size() >> nq;
+    if (nq == 1)
+        rdm_kernel<2><<<blocks, 256, 0, st->stream>>>(st->amps, groups, qubits[0], 0, lo, 0, st->work);
+    else
+        rdm_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, groups, qubits[0], qubits[1], lo, hi, st->work);
+    rdm_finish<<<1, 32, 0, st->stream>>>(st->work, blocks, vals, st->result);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(out, st->result, sizeof(double) * vals, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+}  // extern "C"

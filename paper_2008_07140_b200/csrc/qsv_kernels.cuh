@@ -1,0 +1,503 @@
+// sm_100a kernels of libqsv.  Included once, by qsv_api.cu.
+//
+// Layout in HBM: one contiguous complex128 array (double2, 16 B, 16-B aligned),
+// index bit k <-> qubit k.  Every kernel moves amplitudes as 128-bit
+// double2 loads/stores; consecutive threads touch consecutive amplitudes
+// wherever the schedule allows (the planner forces the lowest qubits into
+// every tile so a warp streams >= 512 contiguous bytes).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qsv_plan.h"
+
+namespace qsv {
+
+// ---------------------------------------------------------------------------
+// complex helpers (FP64 on the CUDA cores; B200 has no FP64 tcgen05 kind)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+// u0*x0 + u1*x1
+__device__ __forceinline__ double2 cdot2(double2 u0, double2 x0, double2 u1, double2 x1) {
+    double re = u0.x * x0.x;
+    re = fma(-u0.y, x0.y, re);
+    re = fma(u1.x, x1.x, re);
+    re = fma(-u1.y, x1.y, re);
+    double im = u0.x * x0.y;
+    im = fma(u0.y, x0.x, im);
+    im = fma(u1.x, x1.y, im);
+    im = fma(u1.y, x1.x, im);
+    return make_double2(re, im);
+}
+
+__device__ __forceinline__ double2 ldm(const double *m, int k) {
+    return make_double2(__ldg(m + 2 * k), __ldg(m + 2 * k + 1));
+}
+
+// shared-memory swizzle: XOR the 16-B slot inside each 128-B row with a fold
+// of the higher index bits, so lanes whose local indices differ only in high
+// bits still spread over all bank groups (a bijection: bits >= 3 unchanged).
+__device__ __forceinline__ uint32_t swz(uint32_t i) {
+    uint32_t h = i >> 3;
+    h ^= h >> 3;
+    h ^= h >> 6;
+    return i ^ (h & 7u);
+}
+
+__device__ __forceinline__ uint32_t deposit32(uint32_t v, uint32_t mask) {
+    uint32_t out = 0;
+    while (mask) {
+        const uint32_t low = mask & (0u - mask);
+        if (v & 1u) out |= low;
+        v >>= 1;
+        mask ^= low;
+    }
+    return out;
+}
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t v, int q) {
+    const uint64_t lowm = (1ull << q) - 1;
+    return ((v & ~lowm) << 1) | (v & lowm);
+}
+
+// ---------------------------------------------------------------------------
+// fused pass kernel
+// ---------------------------------------------------------------------------
+
+template <int R>
+__device__ __forceinline__ uint32_t reg_offset(int rho, const uint32_t (&rm)[R]) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < R; ++k)
+        if ((rho >> k) & 1) s |= rm[k];
+    return s;
+}
+
+template <int R, int A>
+__device__ __forceinline__ void op_mat1(double2 (&v)[1 << R], const double *m, uint32_t tpart,
+                                        const uint32_t (&rm)[R], uint32_t cm) {
+    const double2 u0 = ldm(m, 0), u1 = ldm(m, 1), u2 = ldm(m, 2), u3 = ldm(m, 3);
+#pragma unroll
+    for (int rho = 0; rho < (1 << R); ++rho) {
+        if (rho & (1 << A)) continue;
+        if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
+        const double2 x0 = v[rho], x1 = v[rho | (1 << A)];
+        v[rho] = cdot2(u0, x0, u1, x1);
+        v[rho | (1 << A)] = cdot2(u2, x0, u3, x1);
+    }
+}
+
+template <int R, int A, int B>
+__device__ __forceinline__ void op_mat2(double2 (&v)[1 << R], const double *m, uint32_t tpart,
+                                        const uint32_t (&rm)[R], uint32_t cm) {
+#pragma unroll
+    for (int rho = 0; rho < (1 << R); ++rho) {
+        if (rho & ((1 << A) | (1 << B))) continue;
+        if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
+        const int i1 = rho | (1 << B), i2 = rho | (1 << A), i3 = rho | (1 << A) | (1 << B);
+        const double2 x0 = v[rho], x1 = v[i1], x2 = v[i2], x3 = v[i3];
+        double2 y[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double2 p = cdot2(ldm(m, 4 * r), x0, ldm(m, 4 * r + 1), x1);
+            const double2 q = cdot2(ldm(m, 4 * r + 2), x2, ldm(m, 4 * r + 3), x3);
+            y[r] = make_double2(p.x + q.x, p.y + q.y);
+        }
+        v[rho] = y[0];
+        v[i1] = y[1];
+        v[i2] = y[2];
+        v[i3] = y[3];
+    }
+}
+
+template <int R, int A>
+__device__ __forceinline__ void dispatch_mat1(int a, double2 (&v)[1 << R], const double *m, uint32_t tpart,
+                                              const uint32_t (&rm)[R], uint32_t cm) {
+    if constexpr (A < R) {
+        if (a == A) op_mat1<R, A>(v, m, tpart, rm, cm);
+        else dispatch_mat1<R, A + 1>(a, v, m, tpart, rm, cm);
+    }
+}
+
+template <int R, int A, int B>
+__device__ __forceinline__ void dispatch_mat2(int a, int b, double2 (&v)[1 << R], const double *m,
+                                              uint32_t tpart, const uint32_t (&rm)[R], uint32_t cm) {
+    if constexpr (A < R) {
+        if constexpr (B < R) {
+            if constexpr (A != B) {
+                if (a == A && b == B) {
+                    op_mat2<R, A, B>(v, m, tpart, rm, cm);
+                    return;
+                }
+            }
+            dispatch_mat2<R, A, B + 1>(a, b, v, m, tpart, rm, cm);
+        } else {
+            dispatch_mat2<R, A + 1, 0>(a, b, v, m, tpart, rm, cm);
+        }
+    }
+}
+
+// One CTA = one tile of 2^m amplitudes (tile qubits = pass->tile_mask).  The
+// tile is streamed HBM -> shared memory (coalesced 128-bit loads), then each
+// stage gathers 2^R amplitudes per thread over the stage's register qubits,
+// applies the stage's ops in registers and scatters them back; the last
+// stage's result streams back to HBM.  Tiles are independent (disjoint index
+// sets), so there is no inter-CTA communication and no atomics.
+template <int R>
+__global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, const DevPass *__restrict__ pass,
+                                                   const DevStage *__restrict__ stages,
+                                                   const DevOp *__restrict__ ops, uint64_t n_tiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int m = pass->m;
+    const uint32_t nloc = 1u << m;
+    double2 *tile = reinterpret_cast<double2 *>(smem_raw);
+    uint64_t *lo_tab = reinterpret_cast<uint64_t *>(smem_raw + ((size_t)16 << m));
+    uint64_t *hi_tab = lo_tab + (1 << kLoTabBits);
+    const uint32_t T = blockDim.x;
+
+    for (uint32_t e = threadIdx.x; e < (1u << kLoTabBits); e += T) lo_tab[e] = pass->lo_tab[e];
+    for (uint32_t e = threadIdx.x; e < (1u << kHiTabBits); e += T) hi_tab[e] = pass->hi_tab[e];
+    const int sb = pass->stage_begin, se = pass->stage_end;
+
+    for (uint64_t tile_id = blockIdx.x; tile_id < n_tiles; tile_id += gridDim.x) {
+        uint64_t base = tile_id;
+        for (int j = 0; j < m; ++j) base = insert_zero(base, pass->tq[j]);
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nloc; i += T)
+            tile[swz(i)] = __ldcs(psi + base + (lo_tab[i & ((1u << kLoTabBits) - 1)] | hi_tab[i >> kLoTabBits]));
+        __syncthreads();
+
+        for (int s = sb; s < se; ++s) {
+            const DevStage *st = stages + s;
+            const uint32_t rmask = st->reg_local_mask;
+            uint32_t rm[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) rm[k] = 1u << st->rb[k];
+            const uint32_t tpart = deposit32(threadIdx.x, (nloc - 1) & ~rmask);
+            double2 v[1 << R];
+#pragma unroll
+            for (int rho = 0; rho < (1 << R); ++rho) v[rho] = tile[swz(tpart | reg_offset<R>(rho, rm))];
+
+            const int ob = st->op_begin, oe = st->op_end;
+            for (int o = ob; o < oe; ++o) {
+                const DevOp *op = ops + o;
+                const uint64_t ce = op->cmask_ext;
+                if ((base & ce) != ce) continue;  // uniform: an outside control is 0 for this tile
+                const int kind = op->kind;
+                const uint32_t cm = op->cmask_local;
+                const double *mm = op->m;
+                if (kind == QSV_OP_MAT1) {
+                    dispatch_mat1<R, 0>(op->a, v, mm, tpart, rm, cm);
+                } else if (kind == QSV_OP_MAT2) {
+                    dispatch_mat2<R, 0, 0>(op->a, op->b, v, mm, tpart, rm, cm);
+                } else if (kind == QSV_OP_DIAG1) {
+                    const int la = op->a;
+                    const double2 d0 = ldm(mm, 0), d1 = ldm(mm, 1);
+                    if (la < 0) {
+                        const double2 d = ((base >> op->qa) & 1) ? d1 : d0;
+#pragma unroll
+                        for (int rho = 0; rho < (1 << R); ++rho) {
+                            if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
+                            v[rho] = cmul(v[rho], d);
+                        }
+                    } else {
+#pragma unroll
+                        for (int rho = 0; rho < (1 << R); ++rho) {
+                            const uint32_t loc = tpart | reg_offset<R>(rho, rm);
+                            if (cm && (loc & cm) != cm) continue;
+                            v[rho] = cmul(v[rho], ((loc >> la) & 1) ? d1 : d0);
+                        }
+                    }
+                } else {  // QSV_OP_DIAG2
+                    const int la = op->a, lb = op->b;
+                    const uint32_t ea = la < 0 ? (uint32_t)((base >> op->qa) & 1) : 0u;
+                    const uint32_t eb = lb < 0 ? (uint32_t)((base >> op->qb) & 1) : 0u;
+#pragma unroll
+                    for (int rho = 0; rho < (1 << R); ++rho) {
+                        const uint32_t loc = tpart | reg_offset<R>(rho, rm);
+                        if (cm && (loc & cm) != cm) continue;
+                        const uint32_t ba = la < 0 ? ea : ((loc >> la) & 1);
+                        const uint32_t bb = lb < 0 ? eb : ((loc >> lb) & 1);
+                        v[rho] = cmul(v[rho], ldm(mm, 2 * ba + bb));
+                    }
+                }
+            }
+#pragma unroll
+            for (int rho = 0; rho < (1 << R); ++rho) tile[swz(tpart | reg_offset<R>(rho, rm))] = v[rho];
+            __syncthreads();
+        }
+
+        for (uint32_t i = threadIdx.x; i < nloc; i += T)
+            __stcs(psi + base + (lo_tab[i & ((1u << kLoTabBits) - 1)] | hi_tab[i >> kLoTabBits]), tile[swz(i)]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// unfused single-gate kernel (one HBM sweep over the touched amplitudes per gate)
+// ---------------------------------------------------------------------------
+
+struct GateArgs {
+    int nt, t0, t1, n_ins;
+    uint64_t cmask;
+    int ins[64];     // sorted qubits (targets + controls) to insert as zero bits
+    double2 u[16];   // row-major
+};
+
+__global__ void __launch_bounds__(256) gate_kernel(double2 *__restrict__ psi, const GateArgs g, uint64_t n_groups) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_groups; k += stride) {
+        uint64_t i = k;
+        for (int j = 0; j < g.n_ins; ++j) i = insert_zero(i, g.ins[j]);
+        i |= g.cmask;
+        if (g.nt == 1) {
+            const uint64_t j1 = i | (1ull << g.t0);
+            const double2 x0 = psi[i], x1 = psi[j1];
+            psi[i] = cdot2(g.u[0], x0, g.u[1], x1);
+            psi[j1] = cdot2(g.u[2], x0, g.u[3], x1);
+        } else {
+            const uint64_t a = 1ull << g.t0, b = 1ull << g.t1;
+            const uint64_t idx[4] = {i, i | b, i | a, i | a | b};
+            double2 x[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) x[c] = psi[idx[c]];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double2 p = cdot2(g.u[4 * r], x[0], g.u[4 * r + 1], x[1]);
+                const double2 q = cdot2(g.u[4 * r + 2], x[2], g.u[4 * r + 3], x[3]);
+                psi[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
+            }
+        }
+    }
+}
+
+// diagonal gate: every amplitude whose controls are set gets d[target bits]
+__global__ void __launch_bounds__(256) diag_kernel(double2 *__restrict__ psi, const GateArgs g, uint64_t n_idx) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n_idx; k += stride) {
+        uint64_t i = k;
+        for (int j = 0; j < g.n_ins; ++j) i = insert_zero(i, g.ins[j]);  // controls only
+        i |= g.cmask;
+        const int sel = g.nt == 1 ? (int)((i >> g.t0) & 1) : (int)(2 * ((i >> g.t0) & 1) + ((i >> g.t1) & 1));
+        psi[i] = cmul(psi[i], g.u[sel]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// state initialisation and readout
+// ---------------------------------------------------------------------------
+
+__global__ void set_basis_kernel(double2 *psi, uint64_t size, uint64_t index) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride)
+        psi[i] = make_double2(i == index ? 1.0 : 0.0, 0.0);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// block-level reduction of up to 2 values; thread 0 writes partial[blockIdx.x*2 + {0,1}]
+template <bool MAX>
+__device__ __forceinline__ void block_reduce2(double a, double b, double *partial) {
+    __shared__ double sa[32], sb[32];
+    a = MAX ? warp_max(a) : warp_sum(a);
+    b = MAX ? warp_max(b) : warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sa[w] = a;
+        sb[w] = b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        a = l < nw ? sa[l] : 0.0;
+        b = l < nw ? sb[l] : 0.0;
+        a = MAX ? warp_max(a) : warp_sum(a);
+        b = MAX ? warp_max(b) : warp_sum(b);
+        if (l == 0) {
+            partial[2 * blockIdx.x] = a;
+            partial[2 * blockIdx.x + 1] = b;
+        }
+    }
+}
+
+// mode 0: sum |a|^2; mode 1: sum |a|^2 over bit k == 0; mode 2: <psi|other>; mode 3: max |psi-other|
+__global__ void __launch_bounds__(256) reduce_kernel(const double2 *__restrict__ psi, const double2 *__restrict__ other,
+                                                     uint64_t size, int mode, int k, double *partial) {
+    double a = 0.0, b = 0.0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t count = mode == 1 ? size >> 1 : size;
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride) {
+        if (mode == 0) {
+            const double2 x = psi[j];
+            a = fma(x.x, x.x, a);
+            a = fma(x.y, x.y, a);
+        } else if (mode == 1) {
+            const double2 x = psi[insert_zero(j, k)];
+            a = fma(x.x, x.x, a);
+            a = fma(x.y, x.y, a);
+        } else if (mode == 2) {
+            const double2 x = psi[j], y = other[j];
+            a = fma(x.x, y.x, a);  // Re(conj(x) y)
+            a = fma(x.y, y.y, a);
+            b = fma(x.x, y.y, b);  // Im(conj(x) y)
+            b = fma(-x.y, y.x, b);
+        } else {
+            const double2 x = psi[j], y = other[j];
+            a = fmax(a, hypot(x.x - y.x, x.y - y.y));
+        }
+    }
+    if (mode == 3) block_reduce2<true>(a, b, partial);
+    else block_reduce2<false>(a, b, partial);
+}
+
+// deterministic second stage: one block sums (or maxes) the per-block partials in order
+__global__ void finish_kernel(const double *partial, int n_blocks, int mode, double *out) {
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n_blocks; i += blockDim.x) {
+        if (mode == 3) {
+            a = fmax(a, partial[2 * i]);
+        } else {
+            a += partial[2 * i];
+            b += partial[2 * i + 1];
+        }
+    }
+    __shared__ double sa[32], sb[32];
+    a = mode == 3 ? warp_max(a) : warp_sum(a);
+    b = warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        sa[w] = a;
+        sb[w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double ra = sa[0], rb = sb[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            ra = mode == 3 ? fmax(ra, sa[i]) : ra + sa[i];
+            rb += sb[i];
+        }
+        out[0] = ra;
+        out[1] = rb;
+    }
+}
+
+// zero amplitudes whose bit k != outcome, scale the rest (measure collapse, statevector.py:305-307)
+__global__ void collapse_kernel(double2 *psi, uint64_t size, int k, int outcome, double scale) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        const double2 x = psi[i];
+        if (k >= 0 && (int)((i >> k) & 1) != outcome) psi[i] = make_double2(0.0, 0.0);
+        else psi[i] = make_double2(x.x * scale, x.y * scale);
+    }
+}
+
+// probability histogram over m qubits (first listed = MSB); small tables in shared memory
+__global__ void __launch_bounds__(256) pmeasure_kernel(const double2 *__restrict__ psi, uint64_t size, int m,
+                                                       const int *__restrict__ qubits, double *partial) {
+    extern __shared__ double hist[];
+    const int bins = 1 << m;
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) hist[b] = 0.0;
+    __syncthreads();
+    int q[16];
+    for (int p = 0; p < m; ++p) q[p] = qubits[p];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        const double2 x = psi[i];
+        uint32_t key = 0;
+        for (int p = 0; p < m; ++p) key |= (uint32_t)((i >> q[p]) & 1) << (m - 1 - p);
+        atomicAdd(&hist[key], fma(x.x, x.x, x.y * x.y));
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < bins; b += blockDim.x) partial[(size_t)blockIdx.x * bins + b] = hist[b];
+}
+
+__global__ void pmeasure_finish(const double *partial, int n_blocks, int bins, double *table) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= bins) return;
+    double s = 0.0;
+    for (int i = 0; i < n_blocks; ++i) s += partial[(size_t)i * bins + b];
+    table[b] = s;
+}
+
+// large tables (m > 12): scatter with global atomics
+__global__ void pmeasure_global_kernel(const double2 *__restrict__ psi, uint64_t size, int m,
+                                       const int *__restrict__ qubits, double *table) {
+    int q[64];
+    for (int p = 0; p < m; ++p) q[p] = qubits[p];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        const double2 x = psi[i];
+        uint64_t key = 0;
+        for (int p = 0; p < m; ++p) key |= ((i >> q[p]) & 1) << (m - 1 - p);
+        atomicAdd(&table[key], fma(x.x, x.x, x.y * x.y));
+    }
+}
+
+// reduced density matrix of nq in {1,2} qubits: rho[r][c] = sum_groups x_r conj(x_c)
+template <int D>
+__global__ void __launch_bounds__(256) rdm_kernel(const double2 *__restrict__ psi, uint64_t n_groups, int qa, int qb,
+                                                  int ins0, int ins1, double *partial) {
+    double acc[2 * D * D];
+#pragma unroll
+    for (int k = 0; k < 2 * D * D; ++k) acc[k] = 0.0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_groups; g += stride) {
+        uint64_t i = insert_zero(g, ins0);
+        if (D == 4) i = insert_zero(i, ins1);
+        double2 x[D];
+        if (D == 2) {
+            x[0] = psi[i];
+            x[1] = psi[i | (1ull << qa)];
+        } else {
+            const uint64_t a = 1ull << qa, b = 1ull << qb;
+            x[0] = psi[i];
+            x[1] = psi[i | b];
+            x[2] = psi[i | a];
+            x[3] = psi[i | a | b];
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                // x_r * conj(x_c)
+                acc[2 * (r * D + c)] = fma(x[r].x, x[c].x, fma(x[r].y, x[c].y, acc[2 * (r * D + c)]));
+                acc[2 * (r * D + c) + 1] = fma(x[r].y, x[c].x, fma(-x[r].x, x[c].y, acc[2 * (r * D + c) + 1]));
+            }
+    }
+    __shared__ double red[32][2 * D * D];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 2 * D * D; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (l == 0) red[w][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * D * D) {
+        double s = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
+        partial[(size_t)blockIdx.x * 2 * D * D + threadIdx.x] = s;
+    }
+}
+
+__global__ void rdm_finish(const double *partial, int n_blocks, int vals, double *out) {
+    const int k = threadIdx.x;
+    if (k >= vals) return;
+    double s = 0.0;
+    for (int i = 0; i < n_blocks; ++i) s += partial[(size_t)i * vals + k];
+    out[k] = s;
+}
+
+}  // namespace qsv

@@ -1,0 +1,334 @@
+"""Full-amplitude engine: the reference API, executed by libqsv on a B200.
+
+Drop-in mirror of `qcsim/statevector.py` (statevector.py:27-430): the same
+names, arguments and error classes, with the amplitudes resident in HBM.
+
+* `StateVector` owns a device buffer of 2^n complex128 amplitudes.
+  `.amplitudes` downloads a host copy (numpy) and assigning to it uploads;
+  `chunk_log2` is kept for signature compatibility (the GPU layout does not
+  use chunks).
+* `apply_single_qubit / apply_controlled / apply_two_qubit / apply_projector`
+  launch one unfused gate kernel each (the reference kernel API,
+  statevector.py:255-289).
+* `run_full` hands maximal runs of gates to the native scheduler, which fuses
+  them into a few HBM passes (`qsv_run`); MEASURE, PMEASURE and noisy gates
+  are executed between runs with the reference's RNG semantics.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import gates
+from .errors import DegenerateBranch, DegenerateState, TooManyQubits, UnsupportedGate
+from .program import Instruction, Program
+
+DEFAULT_MAX_QUBITS = 30
+
+
+def default_chunk_log2(n: int, workers: int = 1) -> int:
+    """Reference chunk sizing (statevector.py:46-49); informational on the GPU."""
+    want = max(4, 4 * max(1, workers))
+    return max(0, n - (max(1, want - 1).bit_length()))
+
+
+class StateVector:
+    """2^n complex128 amplitudes in device memory (reference statevector.py:32-43)."""
+
+    def __init__(self, qubit_count: int, amplitudes=None, chunk_log2: int | None = None, *,
+                 device: int = 0, stream=None, _handle=None):
+        self.qubit_count = int(qubit_count)
+        self.chunk_log2 = default_chunk_log2(self.qubit_count) if chunk_log2 is None else chunk_log2
+        self.device = device
+        L = N.lib()
+        if _handle is None:
+            h = C.c_void_p()
+            N.check(L.qsv_create(self.qubit_count, device,
+                                 C.c_void_p(-1 if stream is None else stream), C.byref(h)))
+            _handle = h
+        self._h = _handle
+        if amplitudes is not None:
+            self.amplitudes = amplitudes
+
+    # -- lifetime ---------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.lib().qsv_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def device_ptr(self) -> int:
+        p = C.c_void_p()
+        N.check(N.lib().qsv_device_ptr(self._h, C.byref(p)))
+        return p.value
+
+    @property
+    def chunk_count(self) -> int:
+        return 1 << (self.qubit_count - self.chunk_log2)
+
+    # -- data movement ----------------------------------------------------
+    @property
+    def amplitudes(self) -> np.ndarray:
+        out = np.empty(1 << self.qubit_count, dtype=np.complex128)
+        self.download(out)
+        return out
+
+    @amplitudes.setter
+    def amplitudes(self, values) -> None:
+        values = np.ascontiguousarray(values, dtype=np.complex128)
+        if values.size != 1 << self.qubit_count:
+            raise ValueError(f"expected {1 << self.qubit_count} amplitudes, got {values.size}")
+        N.check(N.lib().qsv_upload(self._h, values.ctypes.data, 0, values.size))
+
+    def download(self, out: np.ndarray, offset: int = 0) -> np.ndarray:
+        assert out.dtype == np.complex128 and out.flags.c_contiguous
+        N.check(N.lib().qsv_download(self._h, out.ctypes.data, offset, out.size))
+        return out
+
+    def set_basis(self, index: int) -> None:
+        N.check(N.lib().qsv_set_basis(self._h, int(index)))
+
+    def synchronize(self) -> None:
+        N.check(N.lib().qsv_synchronize(self._h))
+
+    # -- readout ------------------------------------------------------------
+    def norm_sq(self) -> float:
+        out = C.c_double()
+        N.check(N.lib().qsv_norm_sq(self._h, C.byref(out)))
+        return out.value
+
+    def inner(self, other: "StateVector") -> complex:
+        """<self|other> computed on the device."""
+        re, im = C.c_double(), C.c_double()
+        N.check(N.lib().qsv_inner(self._h, C.c_void_p(other.device_ptr), C.byref(re), C.byref(im)))
+        return complex(re.value, im.value)
+
+    def max_abs_diff(self, other: "StateVector") -> float:
+        out = C.c_double()
+        N.check(N.lib().qsv_max_abs_diff(self._h, C.c_void_p(other.device_ptr), C.byref(out)))
+        return out.value
+
+    def reduced_density(self, qubits) -> np.ndarray:
+        qubits = tuple(int(q) for q in qubits)
+        d = 1 << len(qubits)
+        out = np.empty((d, d), dtype=np.complex128)
+        q = np.asarray(qubits, dtype=np.int32)
+        N.check(N.lib().qsv_reduced_density(self._h, len(qubits), q.ctypes.data, out.ctypes.data))
+        return out
+
+
+def init_state(n: int, *, chunk_log2: int | None = None, max_qubits: int = DEFAULT_MAX_QUBITS,
+               device: int = 0, stream=None) -> StateVector:
+    """|0...0> on n qubits (statevector.py:52-65); TooManyQubits above the ceiling."""
+    if n < 1:
+        raise TooManyQubits(f"need at least 1 qubit, got {n}")
+    if n > max_qubits:
+        raise TooManyQubits(f"{n} qubits exceed the {max_qubits}-qubit memory ceiling")
+    if chunk_log2 is None:
+        chunk_log2 = default_chunk_log2(n)
+    return StateVector(n, None, min(max(chunk_log2, 0), n), device=device, stream=stream)
+
+
+# --------------------------------------------------------------------------
+# kernel API (one gate, one launch)
+# --------------------------------------------------------------------------
+
+
+def _apply_gate(state: StateVector, u, targets, controls=()) -> None:
+    rec = N.gate_records([(np.asarray(u, dtype=np.complex128), tuple(targets), tuple(controls))])
+    N.check(N.lib().qsv_apply_gate(state.handle, rec.ctypes.data))
+
+
+def apply_single_qubit(state, u, k, pool=None) -> None:
+    """(a_i, a_{i+2^k}) <- U (a_i, a_{i+2^k}) for every index with bit k = 0."""
+    _apply_gate(state, u, (k,))
+
+
+def apply_controlled(state, u, controls, k, pool=None) -> None:
+    """Pair update on indices whose control bits are all 1; others untouched."""
+    _apply_gate(state, u, (k,), tuple(controls))
+
+
+def apply_two_qubit(state, u, q_hi, q_lo, pool=None, controls=()) -> None:
+    """4x4 update; q_hi indexes the high matrix bit, q_lo the low one."""
+    _apply_gate(state, u, (q_hi, q_lo), tuple(controls))
+
+
+def apply_projector(state, p, k, pool=None) -> None:
+    """Non-unitary diagonal update (no renormalisation)."""
+    _apply_gate(state, p, (k,))
+
+
+# --------------------------------------------------------------------------
+# readout (statevector.py:292-328)
+# --------------------------------------------------------------------------
+
+
+def probability_bit0(state: StateVector, k: int) -> float:
+    out = C.c_double()
+    N.check(N.lib().qsv_prob_bit0(state.handle, int(k), C.byref(out)))
+    return out.value
+
+
+def measure(state: StateVector, k: int, rng: np.random.Generator) -> int:
+    """Projective measurement: collapse and renormalise (statevector.py:298-308)."""
+    p0 = probability_bit0(state, k)
+    p1 = state.norm_sq() - p0
+    if p0 < 1e-12 and p1 < 1e-12:
+        raise DegenerateState(f"both outcomes of qubit {k} have ~zero probability")
+    outcome = 0 if rng.random() < p0 else 1
+    N.check(N.lib().qsv_collapse(state.handle, int(k), outcome,
+                                 1.0 / math.sqrt(p0 if outcome == 0 else p1)))
+    return outcome
+
+
+def pmeasure(state: StateVector, qubits) -> np.ndarray:
+    """Probability table over the listed qubits, first listed = MSB; state untouched."""
+    q = np.asarray(tuple(qubits), dtype=np.int32)
+    table = np.empty(1 << q.size, dtype=np.float64)
+    N.check(N.lib().qsv_pmeasure(state.handle, q.ctypes.data, int(q.size), table.ctypes.data))
+    return table
+
+
+# --------------------------------------------------------------------------
+# program execution
+# --------------------------------------------------------------------------
+
+
+@dataclass
+class RunResult:
+    cregs: list[int]
+    tables: list[tuple[tuple[int, ...], np.ndarray]] = field(default_factory=list)
+    state: StateVector | None = None
+    stats: dict = field(default_factory=dict)
+
+
+def _gate_triplet(inst):
+    base, targets, controls = gates.controlled_form(inst)
+    if len(targets) > 2:
+        raise UnsupportedGate(f"{inst.name} targets {targets}", inst.line)
+    return base, targets, controls
+
+
+def compile_gates(instructions) -> np.ndarray:
+    """Gate instructions -> packed qsv_gate records (controlled form)."""
+    return N.gate_records(_gate_triplet(i) for i in instructions)
+
+
+def _noisy(state, inst, noise, rng) -> bool:
+    """Reference trajectory step (statevector.py:343-357, noise.py:188-222).
+
+    Branch weights ||K_i psi||^2 = tr(K_i rho K_i^dag) come from ONE on-device
+    reduced-density pass over the gate's qubits; U.K_i / sqrt(p_i) is then
+    applied as a single dense gate (renormalisation folded in when the
+    reference would renormalise, i.e. |p_i - 1| > 1e-12)."""
+    if noise is None:
+        return False
+    base, targets, controls = gates.controlled_form(inst)
+    qubits = tuple(controls) + tuple(targets)
+    if len(qubits) > 2:
+        return False
+    kraus = noise.kraus_for(inst, len(qubits))
+    if kraus is None:
+        return False
+    rho = state.reduced_density(qubits)
+    probs = [float(np.real(np.trace(k @ rho @ k.conj().T))) for k in kraus]
+    total = sum(probs)
+    if total < 1e-12:
+        raise DegenerateBranch("all Kraus branches have ~zero probability")
+    r = rng.random() * total
+    acc, choice = 0.0, len(probs) - 1
+    for i, p in enumerate(probs):
+        acc += p
+        if r < acc:
+            choice = i
+            break
+    noisy = gates.embed_controls(base, len(controls)) @ kraus[choice]
+    if abs(probs[choice] - 1.0) > 1e-12:
+        noisy = noisy / math.sqrt(probs[choice])
+    _apply_gate(state, noisy, qubits)
+    return True
+
+
+def _flush(state, batch, options, stats) -> None:
+    if not batch:
+        return
+    rec = compile_gates(batch)
+    st = N.qsv_run_stats()
+    N.check(N.lib().qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(options), C.byref(st)))
+    for k, v in st.as_dict().items():
+        stats[k] = stats.get(k, 0) + v
+    batch.clear()
+
+
+def apply_instruction(state: StateVector, inst: Instruction, pool=None, rng=None, noise=None,
+                      result: RunResult | None = None) -> None:
+    """Execute one expanded instruction (statevector.py:360-394)."""
+    if inst.name == "MEASURE":
+        if rng is None:
+            raise UnsupportedGate("MEASURE needs a random stream", inst.line)
+        bit = measure(state, inst.qubits[0], rng)
+        if result is not None:
+            result.cregs[inst.creg] = bit
+        return
+    if inst.name == "PMEASURE":
+        table = pmeasure(state, inst.qubits)
+        if result is not None:
+            result.tables.append((inst.qubits, table))
+        return
+    if _noisy(state, inst, noise, rng):
+        return
+    base, targets, controls = _gate_triplet(inst)
+    _apply_gate(state, base, targets, controls)
+
+
+def run_full(program: Program, rng: np.random.Generator | None = None, noise=None, *,
+             workers: int = 1, pool=None, chunk_log2: int | None = None,
+             max_qubits: int = DEFAULT_MAX_QUBITS, initial_index: int = 0,
+             initial_state=None, fuse: bool = True, tile_qubits: int = 0, reg_qubits: int = 0,
+             low_qubits: int = 0, device: int = 0, stream=None, state: StateVector | None = None,
+             profile: bool = False) -> RunResult:
+    """Run a program on the B200 full-amplitude backend (statevector.py:397-430).
+
+    Extra keywords over the reference: `initial_state` (host amplitudes to
+    start from), `fuse`/`tile_qubits`/`reg_qubits`/`low_qubits` (scheduler
+    knobs), `device`/`stream`, `state` (reuse an existing device state) and
+    `profile` (per-launch CUDA-event timing into `RunResult.stats`).
+    `workers`, `pool` and `chunk_log2` are accepted and ignored.
+    """
+    n = program.qubit_count
+    if state is None:
+        state = init_state(n, chunk_log2=chunk_log2, max_qubits=max_qubits, device=device, stream=stream)
+    elif state.qubit_count != n:
+        raise ValueError("state has a different qubit count")
+    if initial_state is not None:
+        state.amplitudes = initial_state
+    else:
+        state.set_basis(initial_index)
+    result = RunResult(cregs=[0] * program.creg_count, state=state)
+    opts = N.options(fuse=fuse, tile_qubits=tile_qubits, reg_qubits=reg_qubits,
+                     low_qubits=low_qubits, profile=profile)
+    batch: list = []
+    for inst in program.instructions:
+        if inst.is_gate and noise is None:
+            batch.append(inst)
+            continue
+        _flush(state, batch, opts, result.stats)
+        apply_instruction(state, inst, None, rng, noise, result)
+    _flush(state, batch, opts, result.stats)
+    return result

@@ -1,0 +1,162 @@
+"""Seeded synthetic inputs for the five BASELINE.json configurations.
+
+No public dataset is involved; every input is generated
+here from a recorded seed and emitted as .qprog text in the reference
+grammar, so the oracle and the GPU engine consume the identical gate stream.
+
+* C1/C2/C3 - eight-pattern no-repeat grid RQC (`rqc.py`, patterns=8)
+* C4       - little-endian QFT (H + CR "pi/2^k" + reversal SWAPs) on an
+             i.i.d. complex Gaussian state, inverse via DAGGER
+* C5       - depolarising trajectories: Pauli errors pre-sampled on the host
+             with the reference's exact draw rule (`noise.py:188-222`) and
+             inserted as explicit X/Y/Z gates BEFORE the noisy gate (the
+             reference applies U.K_i, `noise.py:214`).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .rqc import RqcConfig, generate_rqc
+
+C2_SHAPE = (5, 6, 24)   # n=30, 24 cycles
+C1_SHAPE = (4, 5, 20)   # n=20, 20 cycles
+C5_SHAPE = (4, 6, 20)   # n=24, 20 cycles
+
+
+def grid_shape(n: int) -> tuple[int, int]:
+    """Most square rows x cols = n with rows <= cols (33 -> 3x11, 34 -> 2x17)."""
+    best = (1, n)
+    for r in range(1, int(math.isqrt(n)) + 1):
+        if n % r == 0:
+            best = (r, n // r)
+    return best
+
+
+def rqc_text(rows: int, cols: int, depth: int, seed: int = 0, pmeasure=()) -> str:
+    """BASELINE RQC: 8 cycled CZ patterns, no repeated pool gate per qubit."""
+    return generate_rqc(RqcConfig(rows, cols, depth, seed, pmeasure=tuple(pmeasure),
+                                  patterns=8, no_repeat=True))
+
+
+def rqc_for_qubits(n: int, depth: int = 24, seed: int = 0) -> str:
+    r, c = grid_shape(n)
+    return rqc_text(r, c, depth, seed)
+
+
+def qft_lines(n: int) -> list[str]:
+    """QFT body: for j = n-1..0: H j; CR i,j,"pi/2^(j-i)" for i = j-1..0; swaps."""
+    body = []
+    for j in range(n - 1, -1, -1):
+        body.append(f"H {j}")
+        for i in range(j - 1, -1, -1):
+            body.append(f'CR {i},{j},"pi/{2 ** (j - i)}"')
+    body += [f"SWAP {q},{n - 1 - q}" for q in range(n // 2)]
+    return body
+
+
+def qft_text(n: int, round_trip: bool = False) -> str:
+    body = qft_lines(n)
+    lines = [f"QINIT {n}"] + body
+    if round_trip:
+        lines += ["DAGGER"] + body + ["ENDDAGGER"]
+    return "\n".join(lines) + "\n"
+
+
+def gaussian_state(n: int, seed: int = 0, chunk: int = 1 << 24) -> np.ndarray:
+    """i.i.d. complex Gaussian amplitudes, unit norm (tests/helpers.py:50-52 recipe:
+    all real parts are drawn first, then all imaginary parts)."""
+    size = 1 << n
+    rng = np.random.default_rng(seed)
+    out = np.empty(size, dtype=np.complex128)
+    view = out.view(np.float64).reshape(size, 2)
+    for part in (0, 1):
+        for s in range(0, size, chunk):
+            e = min(size, s + chunk)
+            view[s:e, part] = rng.standard_normal(e - s)
+    # pairwise (numpy) sum of squares, then one scale
+    norm = math.sqrt(float(np.sum(view * view, dtype=np.float64)))
+    out /= norm
+    return out
+
+
+# --------------------------------------------------------------------------
+# C5: depolarising trajectories as explicit Pauli insertions
+# --------------------------------------------------------------------------
+
+_PAULI = ("I", "X", "Y", "Z")
+
+
+def _depolarizing_weights(p: float) -> list[float]:
+    """||K_i psi||^2 / ||psi||^2 for the depolarising Kraus set (noise.py:56-63)."""
+    c = [math.sqrt(1.0 - 0.75 * p)] + [0.5 * math.sqrt(p)] * 3
+    return [x * x for x in c]
+
+
+def sample_pauli_insertions(program, p: float, seed: int):
+    """Replay the reference trajectory draw rule on the host.
+
+    For each <=2-qubit gate in program order the reference draws one
+    `rng.random() * sum(probs)` and picks the first branch whose cumulative
+    weight exceeds it (`noise.py:202-213`); 2-qubit gates use the Kronecker
+    set K_a (x) M_b with index a*4+b, K_a acting on the first qubit of
+    controls+targets (`noise.py:77-79`, `statevector.py:347-356`).  MEASURE
+    consumes one draw too (`statevector.py:304`).  Returns {instruction index:
+    [(qubit, pauli), ...]} for non-identity branches.
+    """
+    from . import gates
+
+    w1 = _depolarizing_weights(p)
+    w2 = [a * b for a in w1 for b in w1]
+    rng = np.random.default_rng(seed)
+    out = {}
+    for idx, inst in enumerate(program.instructions):
+        if inst.name == "MEASURE":
+            rng.random()
+            continue
+        if not inst.is_gate:
+            continue
+        _, targets, controls = gates.controlled_form(inst)
+        qubits = tuple(controls) + tuple(targets)
+        if len(qubits) > 2:
+            continue
+        w = w1 if len(qubits) == 1 else w2
+        r = rng.random() * sum(w)
+        acc, choice = 0.0, len(w) - 1
+        for i, wi in enumerate(w):
+            acc += wi
+            if r < acc:
+                choice = i
+                break
+        if len(qubits) == 1:
+            picks = [(qubits[0], _PAULI[choice])]
+        else:
+            picks = [(qubits[0], _PAULI[choice // 4]), (qubits[1], _PAULI[choice % 4])]
+        picks = [(q, g) for q, g in picks if g != "I"]
+        if picks:
+            out[idx] = picks
+    return out
+
+
+def noisy_trajectory_program(program, p: float, seed: int):
+    """The program with the sampled Paulis inserted before their gates."""
+    from .program import Instruction, Program
+
+    ins = sample_pauli_insertions(program, p, seed)
+    insts = []
+    for idx, inst in enumerate(program.instructions):
+        insts += [Instruction(g, (q,), line=inst.line) for q, g in ins.get(idx, ())]
+        insts.append(inst)
+    return Program(program.qubit_count, program.creg_count, tuple(insts))
+
+
+def noisy_trajectory_text(program, p: float, seed: int) -> str:
+    from .program import to_script
+
+    return to_script(noisy_trajectory_program(program, p, seed))
+
+
+def trajectory_seed(base_seed: int, t: int) -> int:
+    return base_seed * 1_000_003 + t

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (libqsv through its C ABI) vs the oracle and the
+reference golden vectors.  Tolerances (north_star): max|d amplitude| <= 1e-10
+and 1 - |<psi_ref|psi>| <= 1e-12 in complex128."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import program_text
+from oracle import oracle as O
+from paper_2008_07140_b200 import errors, gates, workloads
+from paper_2008_07140_b200 import statevector as SV
+from paper_2008_07140_b200.noise import make_noise_model
+from paper_2008_07140_b200.program import parse_program
+
+pytestmark = pytest.mark.gpu
+
+ATOL = 1e-10
+FID = 1e-12
+
+
+def assert_parity(got, want):
+    got = np.asarray(got)
+    want = np.asarray(want)
+    assert np.abs(got - want).max() <= ATOL
+    ov = abs(np.vdot(want, got)) / math.sqrt(np.vdot(want, want).real * np.vdot(got, got).real)
+    assert 1.0 - ov <= FID
+
+
+CONFIGS = [dict(), dict(fuse=False), dict(tile_qubits=3, reg_qubits=2, low_qubits=1),
+           dict(tile_qubits=5, reg_qubits=3, low_qubits=2), dict(tile_qubits=8, reg_qubits=4),
+           dict(tile_qubits=6, reg_qubits=1)]
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+def test_run_full_golden_programs(golden, golden_arrays, cfg):
+    for name, rec in golden["runs"].items():
+        prog = parse_program(program_text(golden, name))
+        res = SV.run_full(prog, np.random.default_rng(rec["seed"]), **cfg)
+        assert_parity(res.state.amplitudes, golden_arrays[f"run/{name}"])
+        assert res.cregs == rec["cregs"], name
+        for t_i, _ in enumerate(rec["tables"]):
+            assert np.abs(res.tables[t_i][1] - golden_arrays[f"run/{name}/table{t_i}"]).max() <= 1e-12
+        res.state.close()
+
+
+def test_golden_table_appendix_a2(golden):
+    res = SV.run_full(parse_program(golden["programs"]["golden"]["text"]))
+    want = {0: 0.820082, 2: 0.106694, 4: 0.0549175, 6: 0.0183058}
+    table = res.tables[0][1]
+    for i in range(8):
+        assert abs(table[i] - want.get(i, 0.0)) <= 1e-4
+
+
+def test_kernel_api_streams(golden, golden_arrays):
+    """apply_single_qubit / apply_controlled / apply_two_qubit / apply_projector (unfused kernels)."""
+    for s_idx, rec in enumerate(golden["kernel_streams"]):
+        st = SV.StateVector(rec["n"], golden_arrays[f"stream{s_idx}/psi0"], rec["chunk_log2"])
+        for o_idx, op in enumerate(rec["ops"]):
+            u = golden_arrays[f"stream{s_idx}/u{o_idx}"]
+            if op["kind"] == "single":
+                SV.apply_single_qubit(st, u, op["targets"][0])
+            elif op["kind"] == "controlled":
+                SV.apply_controlled(st, u, op["controls"], op["targets"][0])
+            elif op["kind"] == "two":
+                SV.apply_two_qubit(st, u, *op["targets"], controls=tuple(op["controls"]))
+            else:
+                SV.apply_projector(st, u, op["targets"][0])
+        assert np.abs(st.amplitudes - golden_arrays[f"stream{s_idx}/final"]).max() <= ATOL
+        st.close()
+
+
+@pytest.mark.parametrize("n", [3, 6, 9])
+def test_qft_random_state_golden(golden, golden_arrays, n):
+    psi0 = golden_arrays[f"qft{n}/psi0"]
+    for tag in ("forward", "round_trip"):
+        res = SV.run_full(parse_program(golden["qft"][str(n)][tag]), initial_state=psi0)
+        assert_parity(res.state.amplitudes, golden_arrays[f"qft{n}/{tag}"])
+
+
+def test_reference_noise_semantics(golden, golden_arrays):
+    """run_full with a depolarising NoiseModel reproduces the reference trajectory."""
+    for rec in golden["noise"]:
+        res = SV.run_full(parse_program(rec["text"]), np.random.default_rng(rec["traj_seed"]),
+                          make_noise_model("depolarizing", rec["p"]))
+        assert_parity(res.state.amplitudes, golden_arrays[rec["key"]])
+
+
+def test_presampled_pauli_trajectories_match_reference(golden, golden_arrays):
+    """BASELINE C5 semantics: explicit Pauli insertion + fused noiseless run."""
+    for rec in golden["noise"]:
+        prog = parse_program(rec["text"])
+        traj = workloads.noisy_trajectory_program(prog, rec["p"], rec["traj_seed"])
+        res = SV.run_full(traj)
+        assert_parity(res.state.amplitudes, golden_arrays[rec["key"]])
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(fuse=False), dict(tile_qubits=10, reg_qubits=3, low_qubits=4),
+                                 dict(tile_qubits=13, reg_qubits=4)])
+def test_c1_twenty_qubits_vs_oracle(golden, golden_arrays, cfg):
+    prog = parse_program(golden["c1"]["text"])
+    res = SV.run_full(prog, **cfg)
+    got = res.state.amplitudes
+    idx = golden_arrays["c1/idx"]
+    assert np.abs(got[idx] - golden_arrays["c1/amps"]).max() <= ATOL
+    ref = O.run_full(prog, workers=O.cpu_threads())
+    assert_parity(got, ref.state.amplitudes)
+    assert np.abs(SV.pmeasure(res.state, (0, 7, 13, 19)) - golden_arrays["c1/pm_0_7_13_19"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n,depth,seed", [(22, 12, 1), (24, 20, 0)])
+def test_rqc_vs_oracle_larger(n, depth, seed):
+    prog = parse_program(workloads.rqc_for_qubits(n, depth, seed))
+    res = SV.run_full(prog)
+    ref = O.run_full(prog, workers=O.cpu_threads())
+    assert_parity(res.state.amplitudes, ref.state.amplitudes)
+
+
+def test_qft_round_trip_22():
+    n = 22
+    psi0 = workloads.gaussian_state(n, 11)
+    fwd = SV.run_full(parse_program(workloads.qft_text(n)), initial_state=psi0)
+    assert_parity(fwd.state.amplitudes, math.sqrt(1 << n) * np.fft.ifft(psi0))
+    fwd.state.close()
+    rt = SV.run_full(parse_program(workloads.qft_text(n, round_trip=True)), initial_state=psi0)
+    assert_parity(rt.state.amplitudes, psi0)
+
+
+def test_random_programs_all_configs(golden):
+    rng = np.random.default_rng(5)
+    for name, rec in golden["random_programs"].items():
+        prog = parse_program(rec["text"])
+        psi0 = workloads.gaussian_state(prog.qubit_count, int(rng.integers(1 << 30)))
+        ref = O.run_full(prog, initial=psi0)
+        for cfg in CONFIGS:
+            res = SV.run_full(prog, initial_state=psi0, **cfg)
+            assert_parity(res.state.amplitudes, ref.state.amplitudes)
+            res.state.close()
+
+
+def test_readouts():
+    n = 12
+    psi = workloads.gaussian_state(n, 4)
+    st = SV.StateVector(n, psi)
+    ref = O.OracleState(n, psi.copy(), 0)
+    assert st.norm_sq() == pytest.approx(ref.norm_sq(), abs=1e-14)
+    for k in (0, 5, 11):
+        assert SV.probability_bit0(st, k) == pytest.approx(O.probability_bit0(ref, k), abs=1e-14)
+    for qs in [(0,), (11, 0), (3, 7, 1), tuple(range(n - 1, -1, -1)), (2, 9, 4, 6, 0, 11, 8, 1, 5, 3, 10, 7)]:
+        assert np.abs(SV.pmeasure(st, qs) - O.pmeasure(ref, qs)).max() <= 1e-14
+    rho = st.reduced_density((3, 8))
+    t = psi.reshape((2,) * n)
+    sub = np.moveaxis(t, [n - 1 - 3, n - 1 - 8], [0, 1]).reshape(4, -1)
+    assert np.abs(rho - sub @ sub.conj().T).max() <= 1e-14
+    other = SV.StateVector(n, psi * np.exp(0.3j))
+    assert st.inner(other) == pytest.approx(np.exp(0.3j), abs=1e-13)
+    assert st.max_abs_diff(other) == pytest.approx(np.abs(psi * np.exp(0.3j) - psi).max(), abs=1e-15)
+
+
+def test_measure_collapse_and_statistics():
+    rng = np.random.default_rng(1)
+    st = SV.StateVector(2, np.array([1, 0, 0, 1], dtype=complex) / math.sqrt(2))
+    bit = SV.measure(st, 0, rng)
+    want = np.zeros(4)
+    want[3 * bit] = 1
+    assert np.abs(st.amplitudes - want).max() <= 1e-15
+    ones = 0
+    rng = np.random.default_rng(42)
+    for _ in range(2000):
+        st.amplitudes = np.array([1, 1, 0, 0], dtype=complex) / math.sqrt(2)
+        ones += SV.measure(st, 0, rng)
+    assert abs(ones - 1000) < 3 * math.sqrt(500)
+    st.amplitudes = np.zeros(4, dtype=complex)
+    with pytest.raises(errors.DegenerateState):
+        SV.measure(st, 0, rng)
+
+
+def test_errors_and_ceiling():
+    with pytest.raises(errors.TooManyQubits):
+        SV.init_state(31)
+    with pytest.raises(errors.TooManyQubits):
+        SV.init_state(0)
+    st = SV.init_state(3)
+    with pytest.raises(errors.ParseError):
+        SV.apply_single_qubit(st, gates.H, 7)
+    assert np.array_equal(SV.init_state(3).amplitudes, [1, 0, 0, 0, 0, 0, 0, 0])
