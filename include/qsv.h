@@ -72,7 +72,9 @@ typedef struct qsv_options {
     int32_t low_qubits;  /* L: lowest qubits always in the tile (coalescing) */
     int32_t profile;     /* 1: time every launch with CUDA events (qsv_run_stats) */
     int32_t n_global;    /* sharded layout: top n_global qubits are global (not resident) */
-    int32_t reserved[2];
+    int32_t jit;         /* pass kernels: 0 auto (specialise when n >= 16), 1 always, -1 never
+                            (specialised = runtime-generated CUDA compiled with NVRTC for sm_100a) */
+    int32_t reserved;
 } qsv_options;
 
 typedef struct qsv_run_stats {
@@ -140,6 +142,14 @@ int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out);
 int qsv_plan_pass(const qsv_plan *plan, int64_t pass, qsv_pass_info *out);
 int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out);
 int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats);
+
+/* source of the specialised (runtime-generated) kernel of one pass; copies at most
+ * buf_size bytes (NUL-terminated) and reports the full size in *needed; host=1 renders the
+ * same pass as plain C++ (used by the CPU tests to check the generator) */
+int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *buf, int64_t buf_size,
+                           int64_t *needed);
+/* compile CUDA source for sm_100a with NVRTC (no GPU needed); *cubin_bytes = image size */
+int qsv_jit_compile(const char *src, int64_t *cubin_bytes);
 
 /* ---- readout (synchronous) ---- */
 int qsv_norm_sq(qsv_state *st, double *out);

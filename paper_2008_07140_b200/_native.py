@@ -27,7 +27,7 @@ GATE_DTYPE = np.dtype([("n_targets", "<i4"), ("targets", "<i4", (2,)),
 class qsv_options(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
-                ("reserved", C.c_int32 * 2)]
+                ("jit", C.c_int32), ("reserved", C.c_int32)]
 
 
 class qsv_run_stats(C.Structure):
@@ -84,6 +84,8 @@ _SIGNATURES = {
     "qsv_inner": ([_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "qsv_max_abs_diff": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),
+    "qsv_plan_kernel_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_jit_compile": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -113,10 +115,13 @@ def check(rc: int) -> None:
         raise_for_status(rc, lib().qsv_last_error().decode(errors="replace"))
 
 
-def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0) -> qsv_options:
+def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0,
+            jit=0) -> qsv_options:
+    """jit: 0 auto (specialised kernels for n >= 16), 1 always, -1 never."""
     o = qsv_options()
     o.fuse, o.tile_qubits, o.reg_qubits = int(bool(fuse)), int(tile_qubits), int(reg_qubits)
     o.low_qubits, o.profile, o.n_global = int(low_qubits), int(bool(profile)), int(n_global)
+    o.jit = int(jit)
     return o
 
 

@@ -19,8 +19,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libqsv.so"
-SOURCES = [CSRC / "qsv_api.cu", CSRC / "qsv_plan.cpp"]
-DEPS = SOURCES + [CSRC / "qsv_kernels.cuh", CSRC / "qsv_plan.h", PKG.parent / "include" / "qsv.h"]
+SOURCES = [CSRC / "qsv_api.cu", CSRC / "qsv_plan.cpp", CSRC / "qsv_jit.cpp"]
+DEPS = SOURCES + [CSRC / "qsv_kernels.cuh", CSRC / "qsv_plan.h", CSRC / "qsv_jit.h", PKG.parent / "include" / "qsv.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -41,7 +41,7 @@ def host_cxx() -> str:
 def command(out: Path = LIB, extra=()) -> list[str]:
     return [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++20", "-ccbin", host_cxx(),
             "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v", "--expt-relaxed-constexpr",
-            "-shared", "-o", str(out), *map(str, SOURCES), *extra]
+            "-shared", "-o", str(out), *map(str, SOURCES), "-ldl", *extra]
 
 
 def stale() -> bool:

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/qsv.h"
+#include "qsv_jit.h"
 #include "qsv_kernels.cuh"
 #include "qsv_plan.h"
 
@@ -150,34 +151,56 @@ int launch_pass(qsv_state *st, const Plan &P, int pass_idx, const DevPass *d_pas
     return QSV_OK;
 }
 
-// Uploads plan tables into `buf` (device) laid out as [passes | stages | ops].
+// Uploads plan tables into `buf` (device) laid out as [passes | stages | ops],
+// every section 256-byte aligned (DevOp headers are read as 16-byte vectors).
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
 int upload_plan(qsv_state *st, const Plan &P, void *buf, DevPass **dp, DevStage **ds, DevOp **dop) {
-    const size_t bp = P.passes.size() * sizeof(DevPass), bs = P.stages.size() * sizeof(DevStage),
-                 bo = std::max<size_t>(1, P.ops.size()) * sizeof(DevOp);
+    const size_t bp = P.passes.size() * sizeof(DevPass), bs = P.stages.size() * sizeof(DevStage);
     char *b = (char *)buf;
     *dp = (DevPass *)b;
-    *ds = (DevStage *)(b + bp);
-    *dop = (DevOp *)(b + bp + bs);
+    *ds = (DevStage *)(b + align256(bp));
+    *dop = (DevOp *)(b + align256(bp) + align256(bs));
     if (bp) CUDA_TRY(cudaMemcpyAsync(*dp, P.passes.data(), bp, cudaMemcpyHostToDevice, st->stream));
     if (bs) CUDA_TRY(cudaMemcpyAsync(*ds, P.stages.data(), bs, cudaMemcpyHostToDevice, st->stream));
-    if (!P.ops.empty()) CUDA_TRY(cudaMemcpyAsync(*dop, P.ops.data(), P.ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, st->stream));
-    (void)bo;
+    if (!P.ops.empty())
+        CUDA_TRY(cudaMemcpyAsync(*dop, P.ops.data(), P.ops.size() * sizeof(DevOp), cudaMemcpyHostToDevice, st->stream));
     return QSV_OK;
 }
 
 size_t plan_bytes(const Plan &P) {
-    return P.passes.size() * sizeof(DevPass) + P.stages.size() * sizeof(DevStage) +
+    return align256(P.passes.size() * sizeof(DevPass)) + align256(P.stages.size() * sizeof(DevStage)) +
            std::max<size_t>(1, P.ops.size()) * sizeof(DevOp);
 }
 
-int execute_plan(qsv_state *st, const Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, bool profile,
+constexpr int kJitAutoQubits = 16;
+
+int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, const qsv_options *opt,
                  qsv_run_stats *stats) {
+    const bool profile = opt && opt->profile;
+    const int jit_mode = opt ? opt->jit : 0;
+    bool use_jit = jit_mode > 0 || (jit_mode == 0 && st->n >= kJitAutoQubits);
+    if (use_jit) {
+        std::string err;
+        const int rc = jit_prepare(P, st->device, err);
+        if (rc) {
+            if (jit_mode > 0) return fail(rc, err);
+            use_jit = false;  // auto mode: the interpreted pass kernel runs the same plan
+        }
+    }
     LaunchTimer tm;
     tm.on = profile;
     tm.s = st->stream;
     for (size_t i = 0; i < P.passes.size(); ++i) {
         tm.begin();
-        int rc = launch_pass(st, P, (int)i, dp, ds, dop);
+        int rc;
+        if (use_jit) {
+            std::string err;
+            rc = jit_launch(P, (int)i, st->amps, st->n, st->stream, err);
+            if (rc) return fail(rc, err);
+        } else {
+            rc = launch_pass(st, P, (int)i, dp, ds, dop);
+        }
         tm.end();
         if (rc) return rc;
     }
@@ -410,20 +433,22 @@ int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out
     if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
     const int64_t g = P.pass_op_begin[pass] + op;
     if (op < 0 || g >= P.pass_op_begin[pass + 1]) return fail(QSV_E_PARSE, "op index out of range");
-    const DevOp &d = P.ops[g];
+    const GlobalOp &d = P.gops[g];
     const DevPass &dp = P.passes[pass];
     std::memset(out, 0, sizeof(*out));
     out->stage = P.op_stage[g];
     out->kind = d.kind;
     out->qa = d.qa;
     out->qb = d.qb;
-    uint64_t cm = d.cmask_ext;
-    for (int j = 0; j < dp.m; ++j)
-        if ((d.cmask_local >> j) & 1) cm |= 1ull << dp.tq[j];
-    out->control_mask = cm;
+    out->control_mask = d.cmask;
     out->stage_regs = P.stage_regs[dp.stage_begin + out->stage];
-    std::memcpy(out->m, d.m, sizeof(d.m));
+    const int cnt = d.kind == QSV_OP_MAT2 ? 16 : (d.kind == QSV_OP_DIAG1 ? 2 : 4);
+    for (int i = 0; i < cnt; ++i) {
+        out->m[2 * i] = d.m[i].real();
+        out->m[2 * i + 1] = d.m[i].imag();
+    }
     return QSV_OK;
+
 }
 
 int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats) {
@@ -447,8 +472,7 @@ int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_
         P.d_stages = ds;
         P.d_ops = dop;
     }
-    return execute_plan(st, P, (DevPass *)P.d_passes, (DevStage *)P.d_stages, (DevOp *)P.d_ops,
-                        opt && opt->profile, stats);
+    return execute_plan(st, P, (DevPass *)P.d_passes, (DevStage *)P.d_stages, (DevOp *)P.d_ops, opt, stats);
 }
 
 int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt, qsv_run_stats *stats) {
@@ -498,7 +522,29 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     DevOp *dop;
     rc = upload_plan(st, P, st->plan_buf, &dp, &ds, &dop);
     if (rc) return rc;
-    return execute_plan(st, P, dp, ds, dop, opt && opt->profile, stats);
+    return execute_plan(st, P, dp, ds, dop, opt, stats);
+}
+
+int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *buf, int64_t buf_size, int64_t *needed) {
+    const Plan &P = plan->p;
+    if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
+    const std::string src = jit_source(P, (int)pass, host != 0);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (buf && buf_size > 0) {
+        const size_t k = std::min<size_t>(src.size(), (size_t)buf_size - 1);
+        std::memcpy(buf, src.data(), k);
+        buf[k] = 0;
+    }
+    return QSV_OK;
+}
+
+int qsv_jit_compile(const char *src, int64_t *cubin_bytes) {
+    std::string log;
+    const std::string cubin = jit_compile_cubin(src, log);
+    if (cubin_bytes) *cubin_bytes = (int64_t)cubin.size();
+    if (cubin.empty()) return fail(QSV_E_DEVICE, "NVRTC: " + log);
+    g_error = log;
+    return QSV_OK;
 }
 
 int qsv_norm_sq(qsv_state *st, double *out) {

@@ -39,6 +39,14 @@ __device__ __forceinline__ double2 ldm(const double *m, int k) {
     return make_double2(__ldg(m + 2 * k), __ldg(m + 2 * k + 1));
 }
 
+// matrix entry load the compiler may not hoist out of a loop (keeps register
+// pressure bounded for dense 4x4 ops; the entries stay L1-resident)
+__device__ __forceinline__ double2 ldm_v(const double *m, int k) {
+    double2 r;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(m + 2 * k));
+    return r;
+}
+
 // shared-memory swizzle: XOR the 16-B slot inside each 128-B row with a fold
 // of the higher index bits, so lanes whose local indices differ only in high
 // bits still spread over all bank groups (a bijection: bits >= 3 unchanged).
@@ -78,67 +86,219 @@ __device__ __forceinline__ uint32_t reg_offset(int rho, const uint32_t (&rm)[R])
     return s;
 }
 
-template <int R, int A>
-__device__ __forceinline__ void op_mat1(double2 (&v)[1 << R], const double *m, uint32_t tpart,
-                                        const uint32_t (&rm)[R], uint32_t cm) {
-    const double2 u0 = ldm(m, 0), u1 = ldm(m, 1), u2 = ldm(m, 2), u3 = ldm(m, 3);
+__device__ __forceinline__ double2 cneg(double2 x) {
+    return make_double2(__longlong_as_double(__double_as_longlong(x.x) ^ (long long)0x8000000000000000ull),
+                        __longlong_as_double(__double_as_longlong(x.y) ^ (long long)0x8000000000000000ull));
+}
+
+// multiply the amplitudes of one register class (rho & cls_mask) == cls_val by f;
+// mode (from the plan): 0 f == 1 (nothing), 1 f == -1 (sign flip), 2 general
+template <int R, bool CTRL>
+__device__ __forceinline__ void scale_class(double2 (&v)[1 << R], int cls_mask, int cls_val, double2 f, uint32_t mode,
+                                            uint32_t rc) {
+    if (mode == 0) return;
+    if (mode == 1) {
+#pragma unroll
+        for (int rho = 0; rho < (1 << R); ++rho)
+            if ((rho & cls_mask) == cls_val && (!CTRL || (rho & rc) == rc)) v[rho] = cneg(v[rho]);
+    } else {
+#pragma unroll
+        for (int rho = 0; rho < (1 << R); ++rho)
+            if ((rho & cls_mask) == cls_val && (!CTRL || (rho & rc) == rc)) v[rho] = cmul(v[rho], f);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void mat1_pair(double2 &x0, double2 &x1, const double *m) {
+    const double2 a = x0, b = x1;
+    if constexpr (V == V_REAL) {
+        const double u00 = __ldg(m + 0), u01 = __ldg(m + 2), u10 = __ldg(m + 4), u11 = __ldg(m + 6);
+        x0 = make_double2(fma(u01, b.x, u00 * a.x), fma(u01, b.y, u00 * a.y));
+        x1 = make_double2(fma(u11, b.x, u10 * a.x), fma(u11, b.y, u10 * a.y));
+    } else if constexpr (V == V_RXL) {
+        // [[p, i q], [i r, s]] with p, q, r, s real
+        const double p = __ldg(m + 0), q = __ldg(m + 3), r = __ldg(m + 5), t = __ldg(m + 6);
+        x0 = make_double2(fma(-q, b.y, p * a.x), fma(q, b.x, p * a.y));
+        x1 = make_double2(fma(t, b.x, -r * a.y), fma(t, b.y, r * a.x));
+    } else {
+        x0 = cdot2(ldm(m, 0), a, ldm(m, 1), b);
+        x1 = cdot2(ldm(m, 2), a, ldm(m, 3), b);
+    }
+}
+
+template <int R, int A, int V, bool CTRL>
+__device__ __forceinline__ void op_mat1(double2 (&v)[1 << R], const double *m, uint32_t rc) {
 #pragma unroll
     for (int rho = 0; rho < (1 << R); ++rho) {
         if (rho & (1 << A)) continue;
-        if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
-        const double2 x0 = v[rho], x1 = v[rho | (1 << A)];
-        v[rho] = cdot2(u0, x0, u1, x1);
-        v[rho | (1 << A)] = cdot2(u2, x0, u3, x1);
+        if (CTRL && (rho & rc) != rc) continue;
+        mat1_pair<V>(v[rho], v[rho | (1 << A)], m);
     }
 }
 
-template <int R, int A, int B>
-__device__ __forceinline__ void op_mat2(double2 (&v)[1 << R], const double *m, uint32_t tpart,
-                                        const uint32_t (&rm)[R], uint32_t cm) {
-#pragma unroll
-    for (int rho = 0; rho < (1 << R); ++rho) {
-        if (rho & ((1 << A) | (1 << B))) continue;
-        if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
-        const int i1 = rho | (1 << B), i2 = rho | (1 << A), i3 = rho | (1 << A) | (1 << B);
-        const double2 x0 = v[rho], x1 = v[i1], x2 = v[i2], x3 = v[i3];
-        double2 y[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const double2 p = cdot2(ldm(m, 4 * r), x0, ldm(m, 4 * r + 1), x1);
-            const double2 q = cdot2(ldm(m, 4 * r + 2), x2, ldm(m, 4 * r + 3), x3);
-            y[r] = make_double2(p.x + q.x, p.y + q.y);
-        }
-        v[rho] = y[0];
-        v[i1] = y[1];
-        v[i2] = y[2];
-        v[i3] = y[3];
-    }
+template <int R, int A, bool CTRL>
+__device__ __forceinline__ void mat1_var(uint32_t var, double2 (&v)[1 << R], const double *m, uint32_t rc) {
+    if (var == V_REAL) op_mat1<R, A, V_REAL, CTRL>(v, m, rc);
+    else if (var == V_RXL) op_mat1<R, A, V_RXL, CTRL>(v, m, rc);
+    else op_mat1<R, A, V_GEN, CTRL>(v, m, rc);
 }
 
 template <int R, int A>
-__device__ __forceinline__ void dispatch_mat1(int a, double2 (&v)[1 << R], const double *m, uint32_t tpart,
-                                              const uint32_t (&rm)[R], uint32_t cm) {
+__device__ __forceinline__ void dispatch_mat1(uint32_t a, uint32_t var, double2 (&v)[1 << R], const double *m,
+                                              uint32_t rc) {
     if constexpr (A < R) {
-        if (a == A) op_mat1<R, A>(v, m, tpart, rm, cm);
-        else dispatch_mat1<R, A + 1>(a, v, m, tpart, rm, cm);
+        if (a == A) {
+            if (rc) mat1_var<R, A, true>(var, v, m, rc);
+            else mat1_var<R, A, false>(var, v, m, rc);
+        } else {
+            dispatch_mat1<R, A + 1>(a, var, v, m, rc);
+        }
     }
 }
 
 template <int R, int A, int B>
-__device__ __forceinline__ void dispatch_mat2(int a, int b, double2 (&v)[1 << R], const double *m,
-                                              uint32_t tpart, const uint32_t (&rm)[R], uint32_t cm) {
+__device__ __forceinline__ void op_mat2_perm(double2 (&v)[1 << R], const double *m, uint32_t code, uint32_t rc) {
+    int src[4];
+    uint32_t mode[4];
+    double2 ph[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        src[r] = (code >> (24 + 2 * r)) & 3;
+        mode[r] = (code >> (16 + 2 * r)) & 3;
+        ph[r] = ldm(m, r);
+    }
+#pragma unroll
+    for (int rho = 0; rho < (1 << R); ++rho) {
+        if (rho & ((1 << A) | (1 << B))) continue;
+        if ((rho & rc) != rc) continue;
+        const int idx[4] = {rho, rho | (1 << B), rho | (1 << A), rho | (1 << A) | (1 << B)};
+        const double2 x[4] = {v[idx[0]], v[idx[1]], v[idx[2]], v[idx[3]]};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            // select the source with compile-time register indices
+            const double2 xs = src[r] == 0 ? x[0] : src[r] == 1 ? x[1] : src[r] == 2 ? x[2] : x[3];
+            v[idx[r]] = mode[r] == 0 ? xs : (mode[r] == 1 ? cneg(xs) : cmul(xs, ph[r]));
+        }
+    }
+}
+
+template <int R, int A, int B>
+__device__ __forceinline__ void op_mat2_gen(double2 (&v)[1 << R], const double *m, uint32_t rc) {
+#pragma unroll
+    for (int rho = 0; rho < (1 << R); ++rho) {
+        if (rho & ((1 << A) | (1 << B))) continue;
+        if ((rho & rc) != rc) continue;
+        const int idx[4] = {rho, rho | (1 << B), rho | (1 << A), rho | (1 << A) | (1 << B)};
+        const double2 x[4] = {v[idx[0]], v[idx[1]], v[idx[2]], v[idx[3]]};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const double2 p = cdot2(ldm_v(m, 4 * r), x[0], ldm_v(m, 4 * r + 1), x[1]);
+            const double2 q = cdot2(ldm_v(m, 4 * r + 2), x[2], ldm_v(m, 4 * r + 3), x[3]);
+            v[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
+        }
+    }
+}
+
+template <int R, int A, int B, bool PERM>
+__device__ __forceinline__ void dispatch_mat2(uint32_t a, uint32_t b, double2 (&v)[1 << R], const double *m,
+                                              uint32_t code, uint32_t rc) {
     if constexpr (A < R) {
         if constexpr (B < R) {
             if constexpr (A != B) {
                 if (a == A && b == B) {
-                    op_mat2<R, A, B>(v, m, tpart, rm, cm);
+                    if constexpr (PERM) op_mat2_perm<R, A, B>(v, m, code, rc);
+                    else op_mat2_gen<R, A, B>(v, m, rc);
                     return;
                 }
             }
-            dispatch_mat2<R, A, B + 1>(a, b, v, m, tpart, rm, cm);
+            dispatch_mat2<R, A, B + 1, PERM>(a, b, v, m, code, rc);
         } else {
-            dispatch_mat2<R, A + 1, 0>(a, b, v, m, tpart, rm, cm);
+            dispatch_mat2<R, A + 1, 0, PERM>(a, b, v, m, code, rc);
         }
+    }
+}
+
+// diagonal with one register qubit at position P: two classes by bit P
+template <int R, int P, bool CTRL>
+__device__ __forceinline__ void dispatch_diag1(uint32_t p, double2 (&v)[1 << R], double2 f0, uint32_t m0, double2 f1,
+                                               uint32_t m1, uint32_t rc) {
+    if constexpr (P < R) {
+        if (p == P) {
+            scale_class<R, CTRL>(v, 1 << P, 0, f0, m0, rc);
+            scale_class<R, CTRL>(v, 1 << P, 1 << P, f1, m1, rc);
+        } else {
+            dispatch_diag1<R, P + 1, CTRL>(p, v, f0, m0, f1, m1, rc);
+        }
+    }
+}
+
+// diagonal with two register qubits at positions (A, B): four classes (bitA, bitB)
+template <int R, int A, int B, bool CTRL>
+__device__ __forceinline__ void dispatch_diag2(uint32_t a, uint32_t b, double2 (&v)[1 << R], const double *m,
+                                               uint32_t modes, uint32_t rc) {
+    if constexpr (A < R) {
+        if constexpr (B < R) {
+            if constexpr (A != B) {
+                if (a == A && b == B) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const uint32_t mc = (modes >> (2 * c)) & 3;
+                        if (mc) scale_class<R, CTRL>(v, (1 << A) | (1 << B), ((c >> 1) << A) | ((c & 1) << B),
+                                                     ldm(m, c), mc, rc);
+                    }
+                    return;
+                }
+            }
+            dispatch_diag2<R, A, B + 1, CTRL>(a, b, v, m, modes, rc);
+        } else {
+            dispatch_diag2<R, A + 1, 0, CTRL>(a, b, v, m, modes, rc);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t scalar_bit(uint32_t desc, uint32_t tpart, uint64_t base) {
+    if (desc == kNoScalar) return 0;
+    if (desc < (uint32_t)kScalarExt) return (tpart >> desc) & 1u;
+    return (uint32_t)((base >> (desc - kScalarExt)) & 1ull);
+}
+
+template <int R, bool CTRL>
+__device__ __forceinline__ void apply_diag(uint32_t code, uint32_t rs, const double *m, double2 (&v)[1 << R],
+                                           uint32_t tpart, uint64_t base, uint32_t rc) {
+    const uint32_t var = (code >> 4) & 15, a = (code >> 8) & 15, b = (code >> 12) & 15, modes = (code >> 16) & 0xff;
+    if (var == D_AB) {
+        dispatch_diag2<R, 0, 0, CTRL>(a, b, v, m, modes, rc);
+        return;
+    }
+    const uint32_t sA = scalar_bit((rs >> 8) & 0xff, tpart, base), sB = scalar_bit((rs >> 16) & 0xff, tpart, base);
+    if (var == D_NONE) {
+        const uint32_t e = 2 * sA + sB;
+        scale_class<R, CTRL>(v, 0, 0, ldm(m, e), (modes >> (2 * e)) & 3, rc);
+    } else if (var == D_A) {
+        const uint32_t e0 = sB, e1 = 2 + sB;
+        dispatch_diag1<R, 0, CTRL>(a, v, ldm(m, e0), (modes >> (2 * e0)) & 3, ldm(m, e1), (modes >> (2 * e1)) & 3, rc);
+    } else {
+        const uint32_t e0 = 2 * sA, e1 = 2 * sA + 1;
+        dispatch_diag1<R, 0, CTRL>(b, v, ldm(m, e0), (modes >> (2 * e0)) & 3, ldm(m, e1), (modes >> (2 * e1)) & 3, rc);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void apply_op(const DevOp *op, double2 (&v)[1 << R], uint32_t tpart, uint64_t base) {
+    const uint4 h = __ldg(reinterpret_cast<const uint4 *>(op));
+    const uint64_t ec = __ldg(reinterpret_cast<const unsigned long long *>(op) + 2);
+    const uint32_t code = h.x, rs = h.y, tc = h.z;
+    if ((tpart & tc) != tc || (base & ec) != ec) return;  // a scalar control is 0 for this thread
+    const uint32_t kind = code & 15, rc = rs & 0xff;
+    const double *m = op->m;
+    if (kind == K_MAT1) {
+        dispatch_mat1<R, 0>((code >> 8) & 15, (code >> 4) & 15, v, m, rc);
+    } else if (kind == K_MAT2) {
+        if (((code >> 4) & 15) == V_PERM) dispatch_mat2<R, 0, 0, true>((code >> 8) & 15, (code >> 12) & 15, v, m, code, rc);
+        else dispatch_mat2<R, 0, 0, false>((code >> 8) & 15, (code >> 12) & 15, v, m, code, rc);
+    } else {
+        if (rc) apply_diag<R, true>(code, rs, m, v, tpart, base, rc);
+        else apply_diag<R, false>(code, rs, m, v, tpart, base, rc);
     }
 }
 
@@ -179,56 +339,16 @@ __global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, co
 #pragma unroll
             for (int k = 0; k < R; ++k) rm[k] = 1u << st->rb[k];
             const uint32_t tpart = deposit32(threadIdx.x, (nloc - 1) & ~rmask);
+            // swz is linear over GF(2) and tpart / register offsets have disjoint bits
+            const uint32_t tsw = swz(tpart);
             double2 v[1 << R];
 #pragma unroll
-            for (int rho = 0; rho < (1 << R); ++rho) v[rho] = tile[swz(tpart | reg_offset<R>(rho, rm))];
+            for (int rho = 0; rho < (1 << R); ++rho) v[rho] = tile[tsw ^ swz(reg_offset<R>(rho, rm))];
 
             const int ob = st->op_begin, oe = st->op_end;
-            for (int o = ob; o < oe; ++o) {
-                const DevOp *op = ops + o;
-                const uint64_t ce = op->cmask_ext;
-                if ((base & ce) != ce) continue;  // uniform: an outside control is 0 for this tile
-                const int kind = op->kind;
-                const uint32_t cm = op->cmask_local;
-                const double *mm = op->m;
-                if (kind == QSV_OP_MAT1) {
-                    dispatch_mat1<R, 0>(op->a, v, mm, tpart, rm, cm);
-                } else if (kind == QSV_OP_MAT2) {
-                    dispatch_mat2<R, 0, 0>(op->a, op->b, v, mm, tpart, rm, cm);
-                } else if (kind == QSV_OP_DIAG1) {
-                    const int la = op->a;
-                    const double2 d0 = ldm(mm, 0), d1 = ldm(mm, 1);
-                    if (la < 0) {
-                        const double2 d = ((base >> op->qa) & 1) ? d1 : d0;
+            for (int o = ob; o < oe; ++o) apply_op<R>(ops + o, v, tpart, base);
 #pragma unroll
-                        for (int rho = 0; rho < (1 << R); ++rho) {
-                            if (cm && ((tpart | reg_offset<R>(rho, rm)) & cm) != cm) continue;
-                            v[rho] = cmul(v[rho], d);
-                        }
-                    } else {
-#pragma unroll
-                        for (int rho = 0; rho < (1 << R); ++rho) {
-                            const uint32_t loc = tpart | reg_offset<R>(rho, rm);
-                            if (cm && (loc & cm) != cm) continue;
-                            v[rho] = cmul(v[rho], ((loc >> la) & 1) ? d1 : d0);
-                        }
-                    }
-                } else {  // QSV_OP_DIAG2
-                    const int la = op->a, lb = op->b;
-                    const uint32_t ea = la < 0 ? (uint32_t)((base >> op->qa) & 1) : 0u;
-                    const uint32_t eb = lb < 0 ? (uint32_t)((base >> op->qb) & 1) : 0u;
-#pragma unroll
-                    for (int rho = 0; rho < (1 << R); ++rho) {
-                        const uint32_t loc = tpart | reg_offset<R>(rho, rm);
-                        if (cm && (loc & cm) != cm) continue;
-                        const uint32_t ba = la < 0 ? ea : ((loc >> la) & 1);
-                        const uint32_t bb = lb < 0 ? eb : ((loc >> lb) & 1);
-                        v[rho] = cmul(v[rho], ldm(mm, 2 * ba + bb));
-                    }
-                }
-            }
-#pragma unroll
-            for (int rho = 0; rho < (1 << R); ++rho) tile[swz(tpart | reg_offset<R>(rho, rm))] = v[rho];
+            for (int rho = 0; rho < (1 << R); ++rho) tile[tsw ^ swz(reg_offset<R>(rho, rm))] = v[rho];
             __syncthreads();
         }
 

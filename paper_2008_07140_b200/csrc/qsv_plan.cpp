@@ -30,6 +30,7 @@ void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L) {
     L = (opt && opt->low_qubits > 0) ? opt->low_qubits : 5;
     m = std::min(std::min(m, kMaxTileQubits), n);
     r = std::max(std::min(std::min(r, kMaxRegQubits), m), std::min(2, m));
+    m = std::min(m, r + 9);  // at most 512 threads per CTA (launch bound of pass_kernel)
     // leave room for a 2-target gate outside the forced low block
     L = std::max(0, std::min(L, m - 2));
 }
@@ -119,13 +120,7 @@ inline uint64_t deposit(uint64_t v, uint64_t mask) {
     return out;
 }
 
-// Op as seen in global-qubit terms while a stage is being assembled.
-struct StageOp {
-    int kind;
-    int qa, qb;
-    uint64_t cmask;
-    cd m[16];
-};
+using StageOp = GlobalOp;
 
 inline uint64_t op_nmask(const StageOp &o) {
     if (o.kind == QSV_OP_MAT1) return 1ull << o.qa;
@@ -171,33 +166,25 @@ void mul2(const cd *b, const cd *a, cd *out) {
     for (int k = 0; k < 4; ++k) out[k] = r[k];
 }
 
-// Appends `o` to the stage, fusing it into an earlier single-qubit op on the
-// same target with the same controls when every op in between commutes with it.
+// Appends `o` to the stage, merging it into an earlier single-qubit op of the
+// same kind (MAT1 with MAT1, DIAG1 with DIAG1) on the same target with the same
+// controls when every op in between commutes with it.  A diagonal is not folded
+// into a dense 2x2: the kernel applies a phase to half the amplitudes for 2
+// FP64 ops per amplitude, while a fused complex 2x2 costs 8 against 4 for the
+// real / RX-like 2x2 it would replace.
 void append_fused(std::vector<StageOp> &ops, const StageOp &o) {
     if (o.kind == QSV_OP_MAT1 || o.kind == QSV_OP_DIAG1) {
         const uint64_t q = 1ull << o.qa;
         const bool o_diag = o.kind == QSV_OP_DIAG1;
         for (int k = (int)ops.size() - 1; k >= 0; --k) {
             StageOp &p = ops[k];
-            const bool same = (p.kind == QSV_OP_MAT1 || p.kind == QSV_OP_DIAG1) && p.qa == o.qa &&
-                              p.cmask == o.cmask;
-            if (same) {
-                cd a[4], b[4], r[4];
-                auto full = [](const StageOp &x, cd *dst) {
-                    if (x.kind == QSV_OP_DIAG1) {
-                        dst[0] = x.m[0]; dst[1] = 0; dst[2] = 0; dst[3] = x.m[1];
-                    } else {
-                        for (int i = 0; i < 4; ++i) dst[i] = x.m[i];
-                    }
-                };
-                full(p, a);
-                full(o, b);
-                mul2(b, a, r);
-                if (p.kind == QSV_OP_DIAG1 && o_diag) {
-                    p.m[0] = r[0];
-                    p.m[1] = r[3];
+            if (p.kind == o.kind && p.qa == o.qa && p.cmask == o.cmask) {
+                if (o_diag) {
+                    p.m[0] = o.m[0] * p.m[0];
+                    p.m[1] = o.m[1] * p.m[1];
                 } else {
-                    p.kind = QSV_OP_MAT1;
+                    cd r[4];
+                    mul2(o.m, p.m, r);
                     for (int i = 0; i < 4; ++i) p.m[i] = r[i];
                 }
                 return;
@@ -210,6 +197,143 @@ void append_fused(std::vector<StageOp> &ops, const StageOp &o) {
         }
     }
     ops.push_back(o);
+}
+
+inline bool is_zero(cd z) { return z.real() == 0.0 && z.imag() == 0.0; }
+
+int mat1_variant(const cd *u) {
+    bool real = true;
+    for (int i = 0; i < 4; ++i) real &= u[i].imag() == 0.0;
+    if (real) return V_REAL;
+    if (u[0].imag() == 0.0 && u[3].imag() == 0.0 && u[1].real() == 0.0 && u[2].real() == 0.0) return V_RXL;
+    return V_GEN;
+}
+
+inline int factor_mode(cd f) {
+    if (f == cd(1.0, 0.0)) return 0;
+    if (f == cd(-1.0, 0.0)) return 1;
+    return 2;
+}
+
+// Lowers one global op to the device record for a stage whose register
+// positions are given by `regpos_of_local` inside tile `tmask`.
+DevOp lower_op(const StageOp &o, int n, uint64_t tmask, const int32_t *regpos_of_local) {
+    DevOp d;
+    std::memset(&d, 0, sizeof(d));
+    // qubit class: register position (>= 0) or scalar descriptor
+    auto reg_of = [&](int q) -> int {
+        const int lb = local_bit(tmask, q);
+        return lb >= 0 ? regpos_of_local[lb] : -1;
+    };
+    auto scalar_of = [&](int q) -> uint32_t {
+        const int lb = local_bit(tmask, q);
+        return lb < 0 ? (uint32_t)(kScalarExt + q) : (uint32_t)lb;
+    };
+    uint32_t kind = 0, var = 0, a = kNoReg, b = kNoReg, modes = 0, src = 0;
+    uint32_t sa = kNoScalar, sb = kNoScalar;
+    uint64_t cmask = o.cmask;
+    cd f[4];
+    if (o.kind == QSV_OP_DIAG1 || o.kind == QSV_OP_DIAG2) {
+        kind = K_DIAG;
+        int qa = -1, qb;
+        if (o.kind == QSV_OP_DIAG1) {
+            // a controlled 1-qubit diagonal is a 2-qubit diagonal over (control, target):
+            // d = [1, 1, d0, d1]; prefer a register-resident control so the
+            // class selection is compile-time in the kernel
+            qb = o.qa;
+            f[0] = o.m[0];
+            f[1] = o.m[1];
+            f[2] = f[3] = cd(1.0, 0.0);
+            int best = -1, best_rank = 9;
+            for (int q = 0; q < n; ++q) {
+                if (!((cmask >> q) & 1)) continue;
+                const int rank = reg_of(q) >= 0 ? 0 : (local_bit(tmask, q) >= 0 ? 1 : 2);
+                if (rank < best_rank) {
+                    best_rank = rank;
+                    best = q;
+                }
+            }
+            if (best >= 0) {
+                qa = best;
+                cmask &= ~(1ull << best);
+                f[2] = o.m[0];
+                f[3] = o.m[1];
+                f[0] = f[1] = cd(1.0, 0.0);
+            }
+        } else {
+            qa = o.qa;
+            qb = o.qb;
+            for (int i = 0; i < 4; ++i) f[i] = o.m[i];
+        }
+        if (qa >= 0) {
+            const int ra = reg_of(qa);
+            if (ra >= 0) a = (uint32_t)ra;
+            else sa = scalar_of(qa);
+        }
+        const int rb = reg_of(qb);
+        if (rb >= 0) b = (uint32_t)rb;
+        else sb = scalar_of(qb);
+        var = (a != kNoReg ? D_A : 0) | (b != kNoReg ? D_B : 0);
+        for (int i = 0; i < 4; ++i) {
+            modes |= (uint32_t)factor_mode(f[i]) << (2 * i);
+            d.m[2 * i] = f[i].real();
+            d.m[2 * i + 1] = f[i].imag();
+        }
+    } else if (o.kind == QSV_OP_MAT1) {
+        kind = K_MAT1;
+        a = (uint32_t)reg_of(o.qa);
+        var = mat1_variant(o.m);
+        for (int i = 0; i < 4; ++i) {
+            d.m[2 * i] = o.m[i].real();
+            d.m[2 * i + 1] = o.m[i].imag();
+        }
+    } else {
+        kind = K_MAT2;
+        a = (uint32_t)reg_of(o.qa);
+        b = (uint32_t)reg_of(o.qb);
+        bool perm = true;
+        int srcs[4] = {0, 0, 0, 0};
+        for (int r = 0; r < 4 && perm; ++r) {
+            int nz = 0;
+            for (int c = 0; c < 4; ++c)
+                if (!is_zero(o.m[4 * r + c])) {
+                    ++nz;
+                    srcs[r] = c;
+                }
+            perm = nz == 1;
+        }
+        if (perm) {
+            var = V_PERM;
+            for (int r = 0; r < 4; ++r) {
+                src |= (uint32_t)srcs[r] << (2 * r);
+                const cd ph = o.m[4 * r + srcs[r]];
+                modes |= (uint32_t)factor_mode(ph) << (2 * r);
+                d.m[2 * r] = ph.real();
+                d.m[2 * r + 1] = ph.imag();
+            }
+        } else {
+            var = V_GEN;
+            for (int i = 0; i < 16; ++i) {
+                d.m[2 * i] = o.m[i].real();
+                d.m[2 * i + 1] = o.m[i].imag();
+            }
+        }
+    }
+    uint32_t rc = 0, tc = 0;
+    uint64_t ec = 0;
+    for (int q = 0; q < n; ++q) {
+        if (!((cmask >> q) & 1)) continue;
+        const int rq = reg_of(q);
+        const int lb = local_bit(tmask, q);
+        if (rq >= 0) rc |= 1u << rq;
+        else if (lb >= 0) tc |= 1u << lb;
+        else ec |= 1ull << q;
+    }
+    d.code = kind | var << 4 | a << 8 | b << 12 | modes << 16 | src << 24;
+    d.rs = rc | sa << 8 | sb << 16;
+    d.tc = tc;
+    d.ec = ec;
+    return d;
 }
 
 }  // namespace
@@ -272,6 +396,7 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L) {
             std::memset(&ds, 0, sizeof(ds));
             int k = 0;
             int32_t regpos_of_local[64];
+            for (int j = 0; j < 64; ++j) regpos_of_local[j] = -1;
             for (int q = 0; q < n; ++q) {
                 if ((rmask >> q) & 1) {
                     const int lb = local_bit(tmask, q);
@@ -283,33 +408,8 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L) {
             }
             ds.op_begin = (int32_t)P.ops.size();
             for (const StageOp &o : sops) {
-                DevOp d;
-                std::memset(&d, 0, sizeof(d));
-                d.kind = o.kind;
-                d.qa = o.qa;
-                d.qb = o.qb;
-                uint64_t cl = 0, ce = 0;
-                for (int q = 0; q < n; ++q) {
-                    if (!((o.cmask >> q) & 1)) continue;
-                    const int lb = local_bit(tmask, q);
-                    if (lb >= 0) cl |= 1ull << lb;
-                    else ce |= 1ull << q;
-                }
-                d.cmask_local = (uint32_t)cl;
-                d.cmask_ext = ce;
-                if (o.kind == QSV_OP_MAT1 || o.kind == QSV_OP_MAT2) {
-                    d.a = regpos_of_local[local_bit(tmask, o.qa)];
-                    d.b = o.kind == QSV_OP_MAT2 ? regpos_of_local[local_bit(tmask, o.qb)] : -1;
-                } else {
-                    d.a = local_bit(tmask, o.qa);
-                    d.b = o.kind == QSV_OP_DIAG2 ? local_bit(tmask, o.qb) : -1;
-                }
-                const int cnt = o.kind == QSV_OP_MAT2 ? 16 : (o.kind == QSV_OP_DIAG1 ? 2 : 4);
-                for (int i = 0; i < cnt; ++i) {
-                    d.m[2 * i] = o.m[i].real();
-                    d.m[2 * i + 1] = o.m[i].imag();
-                }
-                P.ops.push_back(d);
+                P.ops.push_back(lower_op(o, n, tmask, regpos_of_local));
+                P.gops.push_back(o);
                 P.op_stage.push_back(stage_in_pass);
             }
             ds.op_end = (int32_t)P.ops.size();

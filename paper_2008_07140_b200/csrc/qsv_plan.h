@@ -31,14 +31,42 @@ constexpr int kMaxRegQubits = 4;    // 16 amplitudes (64 registers) per thread
 constexpr int kLoTabBits = 6;       // local-index -> offset tables: 6 low bits ...
 constexpr int kHiTabBits = kMaxTileQubits - kLoTabBits;  // ... + 7 high bits
 
-// Device-side op record (16-byte aligned; read uniformly by every thread).
-struct DevOp {
-    int32_t kind;   // QSV_OP_*
-    int32_t a, b;   // MAT: register positions (a = MSB target); DIAG: local bits or -1
-    int32_t qa, qb; // DIAG: global qubits (used when the local bit is -1)
-    uint32_t cmask_local;  // controls on tile-local bits
-    uint64_t cmask_ext;    // controls on qubits outside the tile (per-CTA test)
-    double m[32];          // row-major complex matrix / diagonal entries
+// Device op kinds (internal; the exported qsv_op_info uses QSV_OP_* in global terms).
+enum : int32_t { K_MAT1 = 1, K_MAT2 = 2, K_DIAG = 3 };
+// MAT1 variants: structure of the 2x2 decides the FP64 work per amplitude
+enum : int32_t { V_GEN = 0, V_REAL = 1, V_RXL = 2 };  // RXL: real diagonal, imaginary off-diagonal
+enum : int32_t { V_PERM = 1 };                        // MAT2: one nonzero per row (SWAP, iSWAP, CNOT, ...)
+// DIAG variants: which of the (<=2) diagonal qubits are register-resident
+enum : int32_t { D_NONE = 0, D_A = 1, D_B = 2, D_AB = 3 };
+constexpr int32_t kScalarExt = 64;   // scalar descriptor >= 64: external global qubit (desc - 64)
+
+// Device-side op record (16-byte aligned; read uniformly by every thread).  Each
+// qubit an op touches is classified at plan time as a register position (varies
+// across a thread's 2^R amplitudes), a thread bit (a tile-local bit fixed per
+// thread in this stage) or an external bit (fixed per tile), so the kernel
+// never tests index bits per amplitude for anything but register positions.
+struct alignas(16) DevOp {
+    // code: kind | var << 4 | a << 8 | b << 12 | modes << 16 | src << 24
+    //   a, b   register positions (MAT targets, a = MSB; DIAG register qubits), 15 = none
+    //   modes  DIAG: 2 bits per entry d[e]: 0 exactly 1 (skip), 1 exactly -1 (sign flip), 2 general
+    //   src    MAT2/PERM: 2 bits per output row r = input column feeding it
+    uint32_t code;
+    uint32_t rs;    // rc (controls on register positions, 8 bits) | sa << 8 | sb << 16 (DIAG scalar qubits)
+    uint32_t tc;    // controls on thread bits (tile-local bit mask)
+    uint32_t pad0;
+    uint64_t ec;    // controls on external qubits (global mask)
+    uint64_t pad1;
+    double m[32];   // MAT1: 2x2; MAT2: 4x4 (PERM: m[2r] = phase of row r); DIAG: d[4] over (bitA, bitB)
+};
+constexpr uint32_t kNoReg = 15;
+constexpr uint32_t kNoScalar = 0xff;  // scalar descriptor: none; [0,32) tile-local bit; [64,128) external qubit - 64
+
+// Op in global-qubit terms (kept host-side for export/validation).
+struct GlobalOp {
+    int kind;  // QSV_OP_*
+    int qa, qb;
+    uint64_t cmask;
+    std::complex<double> m[16];
 };
 
 struct DevStage {
@@ -48,7 +76,7 @@ struct DevStage {
     int32_t pad;
 };
 
-struct DevPass {
+struct alignas(16) DevPass {
     uint64_t tile_mask;
     int32_t m, stage_begin, stage_end, pad;
     int32_t tq[kMaxTileQubits + 3];         // local bit j <-> global qubit tq[j]
@@ -73,11 +101,15 @@ struct Plan {
     std::vector<DevStage> stages;
     std::vector<DevOp> ops;
     std::vector<int32_t> op_stage;        // stage index (within pass) of every op
+    std::vector<GlobalOp> gops;           // every op in global-qubit terms
     std::vector<uint64_t> stage_regs;     // global register-qubit mask per stage
     std::vector<int64_t> pass_op_begin;   // first op of every pass (+ sentinel)
     // device copies (owned by the launcher, lazily uploaded)
     void *d_passes = nullptr, *d_stages = nullptr, *d_ops = nullptr;
     int device = -1;
+    // specialised kernels (qsv_jit.cpp), one CUfunction per pass
+    std::vector<void *> jit_funcs;
+    int jit_device = -1;
 };
 
 // Validates and classifies gate records; returns QSV_OK or an error status (msg set).

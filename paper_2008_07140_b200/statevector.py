@@ -301,14 +301,15 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
              workers: int = 1, pool=None, chunk_log2: int | None = None,
              max_qubits: int = DEFAULT_MAX_QUBITS, initial_index: int = 0,
              initial_state=None, fuse: bool = True, tile_qubits: int = 0, reg_qubits: int = 0,
-             low_qubits: int = 0, device: int = 0, stream=None, state: StateVector | None = None,
-             profile: bool = False) -> RunResult:
+             low_qubits: int = 0, jit: int = 0, device: int = 0, stream=None,
+             state: StateVector | None = None, profile: bool = False) -> RunResult:
     """Run a program on the B200 full-amplitude backend (statevector.py:397-430).
 
     Extra keywords over the reference: `initial_state` (host amplitudes to
     start from), `fuse`/`tile_qubits`/`reg_qubits`/`low_qubits` (scheduler
     knobs), `device`/`stream`, `state` (reuse an existing device state) and
-    `profile` (per-launch CUDA-event timing into `RunResult.stats`).
+    `profile` (per-launch CUDA-event timing into `RunResult.stats`) and `jit`
+    (0: specialised per-pass kernels from n >= 16, 1: always, -1: never).
     `workers`, `pool` and `chunk_log2` are accepted and ignored.
     """
     n = program.qubit_count
@@ -322,7 +323,7 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
         state.set_basis(initial_index)
     result = RunResult(cregs=[0] * program.creg_count, state=state)
     opts = N.options(fuse=fuse, tile_qubits=tile_qubits, reg_qubits=reg_qubits,
-                     low_qubits=low_qubits, profile=profile)
+                     low_qubits=low_qubits, profile=profile, jit=jit)
     batch: list = []
     for inst in program.instructions:
         if inst.is_gate and noise is None:

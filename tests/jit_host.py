@@ -1,0 +1,70 @@
+"""Test helper: run the specialised pass kernels' HOST rendering on the CPU.
+
+libqsv generates one CUDA kernel per fused pass (csrc/qsv_jit.cpp) and can
+render the very same op emission as plain C++ (`qsv_plan_kernel_source(...,
+host=1, ...)`).  Compiling that with gcc and running it against the oracle
+checks the generator (register classes, smem swizzle offsets, pending-phase
+merging, scalar/thread/external conditions) without a GPU.  Test
+infrastructure only.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import subprocess
+import tempfile
+from pathlib import Path
+
+import numpy as np
+
+from paper_2008_07140_b200 import _native as N
+
+_CACHE = Path(tempfile.gettempdir()) / "qsv_jit_host"
+
+
+def plan_handle(records: np.ndarray, n: int, **opts):
+    h = C.c_void_p()
+    o = N.options(**opts)
+    N.check(N.lib().qsv_plan_create(records.ctypes.data, len(records), n, C.byref(o), C.byref(h)))
+    return h
+
+
+def kernel_source(h, p: int, host: bool) -> str:
+    L = N.lib()
+    need = C.c_int64()
+    N.check(L.qsv_plan_kernel_source(h, p, int(host), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    N.check(L.qsv_plan_kernel_source(h, p, int(host), buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+def _compile(src: str):
+    _CACHE.mkdir(exist_ok=True)
+    key = hashlib.sha1(src.encode()).hexdigest()[:20]
+    so = _CACHE / f"p_{key}.so"
+    if not so.exists():
+        cpp = _CACHE / f"p_{key}.cpp"
+        cpp.write_text(src)
+        subprocess.run(["/usr/bin/g++", "-O1", "-shared", "-fPIC", "-o", str(so), str(cpp)], check=True)
+    lib = C.CDLL(str(so))
+    lib.qsv_pass_host.argtypes = [C.c_void_p, C.c_ulonglong]
+    lib.qsv_pass_host.restype = None
+    return lib
+
+
+def run_plan_host(records: np.ndarray, n: int, psi: np.ndarray, **opts) -> np.ndarray:
+    """Apply every pass of the plan through its generated host rendering."""
+    h = plan_handle(records, n, **opts)
+    try:
+        info = N.qsv_plan_info()
+        N.check(N.lib().qsv_plan_summary(h, C.byref(info)))
+        out = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        for p in range(info.passes):
+            pi = N.qsv_pass_info()
+            N.check(N.lib().qsv_plan_pass(h, p, C.byref(pi)))
+            lib = _compile(kernel_source(h, p, True))
+            lib.qsv_pass_host(out.ctypes.data, 1 << (n - pi.m))
+        return out
+    finally:
+        N.lib().qsv_plan_destroy(h)

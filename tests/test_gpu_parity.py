@@ -30,7 +30,7 @@ def assert_parity(got, want):
 
 CONFIGS = [dict(), dict(fuse=False), dict(tile_qubits=3, reg_qubits=2, low_qubits=1),
            dict(tile_qubits=5, reg_qubits=3, low_qubits=2), dict(tile_qubits=8, reg_qubits=4),
-           dict(tile_qubits=6, reg_qubits=1)]
+           dict(tile_qubits=6, reg_qubits=1), dict(jit=1), dict(jit=1, tile_qubits=5, reg_qubits=3, low_qubits=2)]
 
 
 @pytest.mark.parametrize("cfg", CONFIGS)
@@ -97,7 +97,7 @@ def test_presampled_pauli_trajectories_match_reference(golden, golden_arrays):
 
 
 @pytest.mark.parametrize("cfg", [dict(), dict(fuse=False), dict(tile_qubits=10, reg_qubits=3, low_qubits=4),
-                                 dict(tile_qubits=13, reg_qubits=4)])
+                                 dict(tile_qubits=13, reg_qubits=4), dict(jit=-1)])
 def test_c1_twenty_qubits_vs_oracle(golden, golden_arrays, cfg):
     prog = parse_program(golden["c1"]["text"])
     res = SV.run_full(prog, **cfg)
@@ -112,9 +112,11 @@ def test_c1_twenty_qubits_vs_oracle(golden, golden_arrays, cfg):
 @pytest.mark.parametrize("n,depth,seed", [(22, 12, 1), (24, 20, 0)])
 def test_rqc_vs_oracle_larger(n, depth, seed):
     prog = parse_program(workloads.rqc_for_qubits(n, depth, seed))
-    res = SV.run_full(prog)
     ref = O.run_full(prog, workers=O.cpu_threads())
-    assert_parity(res.state.amplitudes, ref.state.amplitudes)
+    for jit in (1, -1):
+        res = SV.run_full(prog, jit=jit)
+        assert_parity(res.state.amplitudes, ref.state.amplitudes)
+        res.state.close()
 
 
 def test_qft_round_trip_22():
