@@ -117,11 +117,13 @@ def dist_env():
     return rank, world, local
 
 
-def workload(n: int):
+def workload(n: int, kind: str = "rqc"):
     from paper_2008_07140_b200 import workloads
     from paper_2008_07140_b200.program import parse_program
 
-    if n == N_BASE:
+    if kind == "qft":  # BASELINE config 4: QFT then DAGGER-QFT on a random state
+        text = workloads.qft_text(n, round_trip=True)
+    elif n == N_BASE:
         text = workloads.rqc_text(*C2, seed=SEED)
     else:
         text = workloads.rqc_for_qubits(n, C2[2], SEED)
@@ -206,13 +208,13 @@ def run_gpu(args) -> None:
 
     torch.cuda.set_device(local)
     n = args.qubits or N_BASE
-    text, prog = workload(n)
+    text, prog = workload(n, args.workload)
     gates_list = prog.gate_instructions()
     G = len(gates_list)
     rec = SV.compile_gates(gates_list)
     L = N.lib()
     opts = N.options(fuse=not args.unfused, tile_qubits=args.tile, reg_qubits=args.regs,
-                     low_qubits=args.low, profile=True)
+                     low_qubits=args.low, profile=True, super_qubits=args.super)
 
     stream = torch.cuda.Stream(device=local)
     state = SV.init_state(n, max_qubits=n, device=local, stream=stream.cuda_stream)
@@ -221,8 +223,16 @@ def run_gpu(args) -> None:
     info = N.qsv_plan_info()
     N.check(L.qsv_plan_summary(plan, C.byref(info)))
 
+    psi0 = None
+    if args.workload == "qft":
+        from paper_2008_07140_b200 import workloads
+
+        psi0 = workloads.gaussian_state(n, SEED)
+        state.amplitudes = psi0
+
     def step(stats):
-        state.set_basis(0)
+        if psi0 is None:
+            state.set_basis(0)  # RQC starts from |0..0>; the QFT round trip maps psi0 back to psi0
         if args.unfused:
             N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(stats)))
         else:
@@ -264,14 +274,14 @@ def run_gpu(args) -> None:
         host = torch.empty(1 << n, dtype=torch.complex128, pin_memory=True)
         hv = host.numpy()
         e2e_ms = []
-        h2d = int(rec.nbytes)
+        h2d = int(rec.nbytes) + (0 if psi0 is None else psi0.nbytes)
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             t0.record(stream)
             res = SV.run_full(prog, state=state, max_qubits=n, tile_qubits=args.tile, reg_qubits=args.regs,
-                              low_qubits=args.low, fuse=not args.unfused)
+                              low_qubits=args.low, fuse=not args.unfused, initial_state=psi0)
             res.state.download(hv)
             t1.record(stream)
             torch.cuda.synchronize()
@@ -294,10 +304,13 @@ def run_gpu(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
-        "config": {"workload": f"C2: RQC {C2[0]}x{C2[1]} grid, {C2[2]} cycles, 8 CZ patterns, seed {SEED}"
-                               if n == N_BASE else f"RQC n={n}",
+        "config": {"workload": (f"C4: QFT + DAGGER-QFT round trip, n={n}, Gaussian state seed {SEED}"
+                                if args.workload == "qft" else
+                                f"C2: RQC {C2[0]}x{C2[1]} grid, {C2[2]} cycles, 8 CZ patterns, seed {SEED}"
+                                if n == N_BASE else f"RQC n={n}"),
                    "n_qubits": n, "gates": G, "fused": not args.unfused, "passes": int(info.passes),
                    "stages": int(info.stages), "tile_qubits": int(info.tile_qubits),
+                   "super_passes": int(info.super_passes), "super_qubits": int(info.super_qubits),
                    "reg_qubits": int(info.reg_qubits), "low_qubits": int(info.low_qubits),
                    "l2": "state (16 GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
@@ -316,9 +329,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--qubits", type=int, default=0)
+    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft"))
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--regs", type=int, default=0)
     ap.add_argument("--low", type=int, default=0)
+    ap.add_argument("--super", type=int, default=0, help="L2 super-tile qubits (0 = default)")
     ap.add_argument("--unfused", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)

@@ -74,13 +74,14 @@ typedef struct qsv_options {
     int32_t n_global;    /* sharded layout: top n_global qubits are global (not resident) */
     int32_t jit;         /* pass kernels: 0 auto (specialise when n >= 16), 1 always, -1 never
                             (specialised = runtime-generated CUDA compiled with NVRTC for sm_100a) */
-    int32_t reserved;
+    int32_t super_qubits; /* s: qubits of an L2-resident super-tile (2^s amplitudes; default 21) */
 } qsv_options;
 
 typedef struct qsv_run_stats {
     int64_t gates;         /* gate records consumed */
-    int64_t passes;        /* HBM passes executed (fused passes or unfused gate kernels) */
+    int64_t passes;        /* HBM passes executed (super-passes, or unfused gate kernels) */
     int64_t stages;        /* register stages (shared-memory round trips) inside passes */
+    int64_t inner_passes;  /* tile passes (L2-resident inside a super-pass) */
     int64_t launches;      /* kernels launched by this call */
     double kernel_ms;      /* sum of event-timed launch durations (profile=1 only) */
     double max_launch_ms;  /* longest single launch (profile=1 only) */
@@ -90,6 +91,9 @@ typedef struct qsv_run_stats {
 typedef struct qsv_plan_info {
     int32_t n_qubits, tile_qubits, reg_qubits, low_qubits;
     int64_t gates, passes, stages, ops;
+    int32_t super_qubits;
+    int32_t reserved;
+    int64_t super_passes; /* HBM passes: each streams the state once through L2 */
 } qsv_plan_info;
 
 /* One fused pass: a tile of 2^m amplitudes over the qubits in tile_mask. */
@@ -98,6 +102,8 @@ typedef struct qsv_pass_info {
     int32_t m;
     int32_t n_stages;
     int64_t n_ops;
+    uint64_t super_mask;   /* qubits of the super-tile this pass runs inside */
+    int64_t super_index;   /* which super-pass it belongs to */
 } qsv_pass_info;
 
 #define QSV_OP_MAT1 1  /* 2x2 on register position a               */
@@ -148,6 +154,12 @@ int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_
  * same pass as plain C++ (used by the CPU tests to check the generator) */
 int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *buf, int64_t buf_size,
                            int64_t *needed);
+/* source of the persistent kernel of one super-pass (all its inner passes on L2-resident
+ * super-tiles, grid barrier in between); host=1 renders it as plain C++ */
+int qsv_plan_super_source(const qsv_plan *plan, int64_t super_pass, int host, char *buf, int64_t buf_size,
+                          int64_t *needed);
+/* FP64 instructions per amplitude the specialised kernel of one pass executes (cost model) */
+int qsv_plan_pass_cost(const qsv_plan *plan, int64_t pass, double *fp64_per_amp);
 /* compile CUDA source for sm_100a with NVRTC (no GPU needed); *cubin_bytes = image size */
 int qsv_jit_compile(const char *src, int64_t *cubin_bytes);
 

@@ -27,12 +27,12 @@ GATE_DTYPE = np.dtype([("n_targets", "<i4"), ("targets", "<i4", (2,)),
 class qsv_options(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
-                ("jit", C.c_int32), ("reserved", C.c_int32)]
+                ("jit", C.c_int32), ("super_qubits", C.c_int32)]
 
 
 class qsv_run_stats(C.Structure):
     _fields_ = [("gates", C.c_int64), ("passes", C.c_int64), ("stages", C.c_int64),
-                ("launches", C.c_int64), ("kernel_ms", C.c_double), ("max_launch_ms", C.c_double),
+                ("inner_passes", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double), ("max_launch_ms", C.c_double),
                 ("algorithmic_bytes", C.c_double)]
 
     def as_dict(self) -> dict:
@@ -42,12 +42,13 @@ class qsv_run_stats(C.Structure):
 class qsv_plan_info(C.Structure):
     _fields_ = [("n_qubits", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("gates", C.c_int64), ("passes", C.c_int64),
-                ("stages", C.c_int64), ("ops", C.c_int64)]
+                ("stages", C.c_int64), ("ops", C.c_int64), ("super_qubits", C.c_int32),
+                ("reserved", C.c_int32), ("super_passes", C.c_int64)]
 
 
 class qsv_pass_info(C.Structure):
     _fields_ = [("tile_mask", C.c_uint64), ("m", C.c_int32), ("n_stages", C.c_int32),
-                ("n_ops", C.c_int64)]
+                ("n_ops", C.c_int64), ("super_mask", C.c_uint64), ("super_index", C.c_int64)]
 
 
 class qsv_op_info(C.Structure):
@@ -85,6 +86,8 @@ _SIGNATURES = {
     "qsv_max_abs_diff": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),
     "qsv_plan_kernel_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_plan_super_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_plan_pass_cost": ([_P, C.c_int64, C.POINTER(C.c_double)], C.c_int),
     "qsv_jit_compile": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int),
 }
 
@@ -116,12 +119,14 @@ def check(rc: int) -> None:
 
 
 def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0,
-            jit=0) -> qsv_options:
-    """jit: 0 auto (specialised kernels for n >= 16), 1 always, -1 never."""
+            jit=0, super_qubits=0) -> qsv_options:
+    """jit: 0 auto (specialised kernels for n >= 16), 1 always, -1 never;
+    super_qubits: L2 super-tile size s (0 = default 21; s <= tile_qubits disables)."""
     o = qsv_options()
     o.fuse, o.tile_qubits, o.reg_qubits = int(bool(fuse)), int(tile_qubits), int(reg_qubits)
     o.low_qubits, o.profile, o.n_global = int(low_qubits), int(bool(profile)), int(n_global)
     o.jit = int(jit)
+    o.super_qubits = int(super_qubits)
     return o
 
 

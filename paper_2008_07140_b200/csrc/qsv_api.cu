@@ -47,7 +47,8 @@ struct qsv_state {
     bool own_mem = false;
     double *work = nullptr;  // reduction partials / pmeasure partials
     size_t work_bytes = 0;
-    double *result = nullptr;  // 2 doubles
+    double *result = nullptr;  // 32 doubles
+    unsigned *barrier = nullptr;  // grid-barrier counter of super-pass kernels
     void *plan_buf = nullptr;  // scratch for one-shot plans
     size_t plan_buf_bytes = 0;
     int sm_count = 148;
@@ -73,6 +74,11 @@ int ensure_work(qsv_state *st, size_t bytes) {
     st->work_bytes = 0;
     CUDA_TRY(cudaMalloc(&st->work, bytes));
     st->work_bytes = bytes;
+    return QSV_OK;
+}
+
+int ensure_barrier(qsv_state *st) {
+    if (!st->barrier) CUDA_TRY(cudaMalloc(&st->barrier, 64));
     return QSV_OK;
 }
 
@@ -175,6 +181,8 @@ size_t plan_bytes(const Plan &P) {
 
 constexpr int kJitAutoQubits = 16;
 
+int ensure_barrier(qsv_state *st);
+
 int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, const qsv_options *opt,
                  qsv_run_stats *stats) {
     const bool profile = opt && opt->profile;
@@ -191,26 +199,46 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
     LaunchTimer tm;
     tm.on = profile;
     tm.s = st->stream;
-    for (size_t i = 0; i < P.passes.size(); ++i) {
-        tm.begin();
-        int rc;
-        if (use_jit) {
+    int64_t hbm_passes = 0, launches = 0;
+    for (size_t si = 0; si < P.supers.size(); ++si) {
+        const SuperPass &sp = P.supers[si];
+        if (use_jit && use_supers(P) && P.jit_super_funcs[si]) {
+            // all inner passes on L2-resident super-tiles: one HBM pass
+            int rc = ensure_barrier(st);
+            if (rc) return rc;
             std::string err;
-            rc = jit_launch(P, (int)i, st->amps, st->n, st->stream, err);
+            tm.begin();
+            rc = jit_launch_super(P, (int)si, st->amps, st->barrier, st->stream, err);
+            tm.end();
             if (rc) return fail(rc, err);
-        } else {
-            rc = launch_pass(st, P, (int)i, dp, ds, dop);
+            ++hbm_passes;
+            ++launches;
+            continue;
         }
-        tm.end();
-        if (rc) return rc;
+        for (int i = sp.pass_begin; i < sp.pass_end; ++i) {
+            tm.begin();
+            int rc;
+            if (use_jit) {
+                std::string err;
+                rc = jit_launch(P, i, st->amps, st->n, st->stream, err);
+                if (rc) return fail(rc, err);
+            } else {
+                rc = launch_pass(st, P, i, dp, ds, dop);
+            }
+            tm.end();
+            if (rc) return rc;
+            ++hbm_passes;
+            ++launches;
+        }
     }
     tm.collect(stats);
     if (stats) {
         stats->gates += P.gates;
-        stats->passes += (int64_t)P.passes.size();
+        stats->passes += hbm_passes;
+        stats->inner_passes += (int64_t)P.passes.size();
         stats->stages += (int64_t)P.stages.size();
-        stats->launches += (int64_t)P.passes.size();
-        stats->algorithmic_bytes += (double)P.passes.size() * 32.0 * (double)st->size();
+        stats->launches += launches;
+        stats->algorithmic_bytes += (double)hbm_passes * 32.0 * (double)st->size();
     }
     return QSV_OK;
 }
@@ -327,6 +355,7 @@ int qsv_destroy(qsv_state *st) {
     if (st->work) cudaFree(st->work);
     if (st->result) cudaFree(st->result);
     if (st->plan_buf) cudaFree(st->plan_buf);
+    if (st->barrier) cudaFree(st->barrier);
     if (st->own_stream) cudaStreamDestroy(st->stream);
     delete st;
     return QSV_OK;
@@ -387,9 +416,10 @@ int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const 
     int rc = to_records(gates, n_gates, n_qubits, recs, msg);
     if (rc) return fail(rc, msg);
     int m, r, L;
-    resolve_options(opt, n_qubits, m, r, L);
+    int s;
+    resolve_options(opt, n_qubits, m, r, L, s);
     auto p = std::make_unique<qsv_plan>();
-    p->p = build_plan(recs, n_qubits, m, r, L);
+    p->p = build_plan(recs, n_qubits, m, r, L, s);
     *out = p.release();
     return QSV_OK;
 }
@@ -414,6 +444,9 @@ int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out) {
     out->passes = (int64_t)P.passes.size();
     out->stages = (int64_t)P.stages.size();
     out->ops = (int64_t)P.ops.size();
+    out->super_qubits = P.s;
+    out->reserved = 0;
+    out->super_passes = (int64_t)P.supers.size();
     return QSV_OK;
 }
 
@@ -425,6 +458,11 @@ int qsv_plan_pass(const qsv_plan *plan, int64_t pass, qsv_pass_info *out) {
     out->m = d.m;
     out->n_stages = d.stage_end - d.stage_begin;
     out->n_ops = P.pass_op_begin[pass + 1] - P.pass_op_begin[pass];
+    for (size_t si = 0; si < P.supers.size(); ++si)
+        if (pass >= P.supers[si].pass_begin && pass < P.supers[si].pass_end) {
+            out->super_mask = P.supers[si].mask;
+            out->super_index = (int64_t)si;
+        }
     return QSV_OK;
 }
 
@@ -504,8 +542,9 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     }
     if (recs.empty()) return QSV_OK;
     int m, r, L;
-    resolve_options(opt, st->n, m, r, L);
-    Plan P = build_plan(recs, st->n, m, r, L);
+    int s;
+    resolve_options(opt, st->n, m, r, L, s);
+    Plan P = build_plan(recs, st->n, m, r, L, s);
     const size_t bytes = plan_bytes(P);
     if (st->plan_buf_bytes < bytes) {
         if (st->plan_buf) {
@@ -535,6 +574,26 @@ int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *b
         std::memcpy(buf, src.data(), k);
         buf[k] = 0;
     }
+    return QSV_OK;
+}
+
+int qsv_plan_super_source(const qsv_plan *plan, int64_t si, int host, char *buf, int64_t buf_size, int64_t *needed) {
+    const Plan &P = plan->p;
+    if (si < 0 || si >= (int64_t)P.supers.size()) return fail(QSV_E_PARSE, "super-pass index out of range");
+    const std::string src = jit_super_source(P, (int)si, host != 0);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (buf && buf_size > 0) {
+        const size_t k = std::min<size_t>(src.size(), (size_t)buf_size - 1);
+        std::memcpy(buf, src.data(), k);
+        buf[k] = 0;
+    }
+    return QSV_OK;
+}
+
+int qsv_plan_pass_cost(const qsv_plan *plan, int64_t pass, double *fp64_per_amp) {
+    const Plan &P = plan->p;
+    if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
+    jit_source(P, (int)pass, false, fp64_per_amp);
     return QSV_OK;
 }
 

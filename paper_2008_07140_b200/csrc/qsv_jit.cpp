@@ -10,7 +10,9 @@
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -49,6 +51,9 @@ struct Driver {
     CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              CUstream, void **, void **) = nullptr;
     CUresult (*GetErrorString)(CUresult, const char **) = nullptr;
+    CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int *, CUfunction, int, size_t) = nullptr;
+    CUresult (*LaunchCooperativeKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                        unsigned, CUstream, void **) = nullptr;
 };
 
 template <typename F>
@@ -88,7 +93,9 @@ Driver &driver() {
         }
         api.ok = sym(h, "cuModuleLoadData", api.ModuleLoadData) && sym(h, "cuModuleGetFunction", api.ModuleGetFunction) &&
                  sym(h, "cuFuncSetAttribute", api.FuncSetAttribute) && sym(h, "cuLaunchKernel", api.LaunchKernel) &&
-                 sym(h, "cuGetErrorString", api.GetErrorString);
+                 sym(h, "cuGetErrorString", api.GetErrorString) &&
+                 sym(h, "cuOccupancyMaxActiveBlocksPerMultiprocessor", api.OccupancyMaxActiveBlocksPerMultiprocessor) &&
+                 sym(h, "cuLaunchCooperativeKernel", api.LaunchCooperativeKernel);
         if (!api.ok) api.why = "libcuda lacks a required symbol";
     });
     return api;
@@ -113,6 +120,17 @@ __device__ __forceinline__ double2 ldcs2(const double2 *p) {
 }
 __device__ __forceinline__ void stcs2(double2 *p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void stwb2(double2 *p, double2 v) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void cp_async16(unsigned saddr, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 )";
 
@@ -155,6 +173,23 @@ std::string deposit_expr(const std::string &src, const std::vector<int> &pos, bo
     return e.str();
 }
 
+inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
+
+}  // namespace
+
+// tile double buffering (cp.async prefetch of the next tile into a second
+// buffer).  Off by default: one buffer with two resident CTAs per SM measured
+// faster on B200 (occupancy hides the tile loads); QSV_JIT_DBUF=1 enables it.
+bool jit_double_buffer() {
+    static const bool on = [] {
+        const char *e = std::getenv("QSV_JIT_DBUF");
+        return e && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+namespace {
+
 uint32_t swz_host(uint32_t i) {
     uint32_t h = i >> 3;
     h ^= h >> 3;
@@ -169,8 +204,78 @@ struct StageGen {
     std::vector<int> regq;          // register position k -> global qubit
     std::map<int, int> thread_bit;  // global qubit -> thread id bit (stage thread bits)
     std::vector<cd> pend;           // pending constant phase per register amplitude
+    double fp64 = 0;                // FP64 instructions emitted per thread (cost model)
+    // runtime diagonal accumulators: qG (thread-wide) and qA<k>_<b> (factor
+    // for amplitudes whose register bit k is b); they collect every diagonal
+    // factor that depends on thread/tile bits, applied once per stage
+    std::vector<int> acc;           // acc[2k+b]: accumulator in use
+    bool accG = false;
 
-    StageGen(std::ostringstream &out, int r, const std::vector<int> &t) : o(out), R(r), tq(t), pend(1u << r, cd(1, 0)) {}
+    StageGen(std::ostringstream &out, int r, const std::vector<int> &t)
+        : o(out), R(r), tq(t), pend(1u << r, cd(1, 0)), acc(2 * r, 0) {}
+
+    static std::string c2(cd c) { return "make_double2(" + lit(c.real()) + ", " + lit(c.imag()) + ")"; }
+
+    void declare_accumulators() {
+        o << "    double2 qG = make_double2(1.0, 0.0);";
+        for (int k = 0; k < R; ++k)
+            o << " double2 qA" << k << "_0 = qG, qA" << k << "_1 = qG;";
+        o << "\n";
+    }
+
+    // apply + reset the accumulators of register position k
+    void flush_acc(int k) {
+        for (int b = 0; b < 2; ++b) {
+            if (!acc[2 * k + b]) continue;
+            for (int rho = 0; rho < (1 << R); ++rho)
+                if (((rho >> k) & 1) == b) o << "    v" << rho << " = cmulc(v" << rho << ", qA" << k << "_" << b << ");\n";
+            o << "    qA" << k << "_" << b << " = make_double2(1.0, 0.0);\n";
+            acc[2 * k + b] = 0;
+            fp64 += 4.0 * (1 << (R - 1));
+        }
+    }
+
+    // stage end: one product table over the active accumulators, then one
+    // complex multiply per amplitude (plus its compile-time pending factor)
+    void flush_runtime() {
+        std::vector<int> used;
+        for (int k = 0; k < R; ++k)
+            if (acc[2 * k] || acc[2 * k + 1]) used.push_back(k);
+        if (used.empty() && !accG) return;
+        std::vector<std::string> tab = {accG ? "qG" : ""};
+        int id = 0;
+        for (size_t u = 0; u < used.size(); ++u) {
+            const int k = used[u];
+            // entry index: bit u <-> register bit of position used[u]
+            std::vector<std::string> next(2 * tab.size());
+            for (size_t j = 0; j < tab.size(); ++j)
+                for (int b = 0; b < 2; ++b) {
+                    const std::string &t = tab[j];
+                    const std::string a = "qA" + std::to_string(k) + "_" + std::to_string(b);
+                    std::string &dst = next[j | ((size_t)b << u)];
+                    if (!acc[2 * k + b]) {
+                        dst = t;
+                    } else if (t.empty()) {
+                        dst = a;
+                    } else {
+                        dst = "qT" + std::to_string(id++);
+                        o << "    const double2 " << dst << " = cmulc(" << t << ", " << a << ");\n";
+                        fp64 += 4;
+                    }
+                }
+            tab.swap(next);
+        }
+        for (int rho = 0; rho < (1 << R); ++rho) {
+            int idx = 0;
+            for (size_t u = 0; u < used.size(); ++u) idx |= ((rho >> used[u]) & 1) << u;
+            const std::string &t = tab[idx];
+            if (t.empty()) continue;
+            o << "    v" << rho << " = cmulc(v" << rho << ", " << t << ");\n";
+            fp64 += 4;
+        }
+        for (int k = 0; k < 2 * R; ++k) acc[k] = 0;
+        accG = false;
+    }
 
     int regpos(int q) const {
         for (int k = 0; k < R; ++k)
@@ -188,6 +293,7 @@ struct StageGen {
         const std::string v = "v" + std::to_string(rho);
         const double cr = c.real(), ci = c.imag();
         if (cr == 1.0 && ci == 0.0) return;
+        fp64 += (ci == 0.0 || cr == 0.0) ? 2 : 4;
         if (cr == -1.0 && ci == 0.0) {
             o << "    " << v << " = make_double2(-" << v << ".x, -" << v << ".y);\n";
         } else if (ci == 0.0) {
@@ -211,6 +317,7 @@ struct StageGen {
         }
     }
     void flush_all() {
+        flush_runtime();
         for (int r = 0; r < (1 << R); ++r) flush(r);
     }
 
@@ -240,6 +347,20 @@ struct StageGen {
                         any = true;
                     }
                 }
+                if (any) {
+                    int terms = 0, muls = 0;
+                    for (int c = 0; c < d; ++c) {
+                        const double mr = M[r * d + c].real(), mi = M[r * d + c].imag();
+                        for (double k : {mr, mi})
+                            if (k != 0.0) {
+                                ++terms;
+                                if (k != 1.0 && k != -1.0) ++muls;
+                            }
+                    }
+                    // fma chains: one op per term after the first, plus a multiply
+                    // when every term carries a coefficient
+                    fp64 += (terms - 1) + (muls == terms ? 1 : 0);
+                }
                 return any ? e.str() : std::string("0.0");
             };
             o << "      v" << idx[r] << " = make_double2(" << comp(false) << ", " << comp(true) << ");\n";
@@ -247,11 +368,125 @@ struct StageGen {
         o << "    }\n";
     }
 
+    // FP64 cost class of multiplying by a constant coefficient in a linear row
+    static int coeff_cost(cd z) {
+        const double a = z.real(), b = z.imag();
+        if ((b == 0.0 && (a == 1.0 || a == -1.0)) || (a == 0.0 && (b == 1.0 || b == -1.0))) return 1;
+        if (a == 0.0 || b == 0.0) return 2;
+        return 4;
+    }
+    // snap a coefficient to an exact unit / pure axis when it is within an ulp of it
+    static cd snap(cd z) {
+        const double eps = 2.3e-16 * std::abs(z);
+        double a = z.real(), b = z.imag();
+        if (std::fabs(a) <= eps) a = 0.0;
+        if (std::fabs(b) <= eps) b = 0.0;
+        for (double u : {1.0, -1.0}) {
+            if (std::fabs(a - u) <= 2.3e-16 && b == 0.0) a = u;
+            if (std::fabs(b - u) <= 2.3e-16 && a == 0.0) b = u;
+        }
+        return cd(a, b);
+    }
+
+    // linear map that first absorbs the inputs' pending factors into the
+    // compile-time coefficients, then factors one coefficient out of every
+    // output row (chosen to make the rest cheapest) and leaves it pending on
+    // that output.  H, sqrt(X), sqrt(Y) and phase-preceded gates become
+    // add/subtract rows; the pending factors are absorbed by the next gate or
+    // multiplied in once at the end of the stage.
+    void linear_absorb(const std::vector<int> &idx, const cd *M) {
+        const int d = (int)idx.size();
+        std::vector<cd> Mp(d * d), Mn(d * d);
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < d; ++c) Mp[r * d + c] = M[r * d + c] * pend[idx[c]];
+        std::vector<cd> newp(d, cd(1, 0));
+        for (int r = 0; r < d; ++r) {
+            double mx = 0;
+            for (int c = 0; c < d; ++c) mx = std::max(mx, std::abs(Mp[r * d + c]));
+            if (mx == 0.0) {
+                for (int c = 0; c < d; ++c) Mn[r * d + c] = 0;
+                continue;
+            }
+            int best = -1, best_cost = 1 << 30;
+            for (int k = 0; k < d; ++k) {
+                const cd ck = Mp[r * d + k];
+                if (std::abs(ck) < 0.5 * mx) continue;
+                int cost = 0;
+                for (int c = 0; c < d; ++c)
+                    if (c != k && Mp[r * d + c] != cd(0, 0)) cost += coeff_cost(snap(Mp[r * d + c] / ck));
+                if (cost < best_cost) {
+                    best_cost = cost;
+                    best = k;
+                }
+            }
+            const cd ck = Mp[r * d + best];
+            for (int c = 0; c < d; ++c)
+                Mn[r * d + c] = c == best ? cd(1, 0) : (Mp[r * d + c] == cd(0, 0) ? cd(0, 0) : snap(Mp[r * d + c] / ck));
+            newp[r] = ck;
+        }
+        linear(idx, Mn.data());
+        for (int r = 0; r < d; ++r) pend[idx[r]] = newp[r];
+    }
+
     std::string scalar_cond(uint64_t smask) const {
         std::string c;
         for (int q = 0; q < 64; ++q)
             if ((smask >> q) & 1) c += (c.empty() ? "" : " && ") + scalar_expr(q);
         return c;
+    }
+
+    // factor expression over the scalar target bits (nested selects of constants)
+    std::string select_expr(const std::vector<int> &dq, const std::vector<cd> &d, const std::vector<int> &sq,
+                            int reg_t, int reg_bit) const {
+        // enumerate scalar assignments; build a chain of ternaries
+        const int ns = (int)sq.size();
+        std::vector<cd> val(1u << ns);
+        for (int combo = 0; combo < (1 << ns); ++combo) {
+            int idx = 0;
+            for (size_t t = 0; t < dq.size(); ++t) {
+                int bit;
+                if ((int)t == reg_t) bit = reg_bit;
+                else {
+                    int si = 0;
+                    while (sq[si] != dq[t]) ++si;
+                    bit = (combo >> si) & 1;
+                }
+                idx = 2 * idx + bit;
+            }
+            val[combo] = d[idx];
+        }
+        std::function<std::string(int, int)> build = [&](int si, int prefix) -> std::string {
+            if (si == ns) return c2(val[prefix]);
+            const std::string a = build(si + 1, prefix), b = build(si + 1, prefix | (1 << si));
+            if (a == b) return a;
+            return "(" + scalar_expr(sq[si]) + " ? " + b + " : " + a + ")";
+        };
+        return build(0, 0);
+    }
+
+    void accumulate(const std::vector<int> &dq, const std::vector<cd> &d, const std::vector<int> &sq,
+                    const std::string &ccond) {
+        int reg_t = -1;
+        for (size_t t = 0; t < dq.size(); ++t)
+            if (regpos(dq[t]) >= 0) reg_t = (int)t;
+        const std::string one = "make_double2(1.0, 0.0)";
+        auto guard = [&](const std::string &e) { return ccond.empty() ? e : "((" + ccond + ") ? " + e + " : " + one + ")"; };
+        if (reg_t < 0) {
+            const std::string e = select_expr(dq, d, sq, -1, 0);
+            if (e == c2(cd(1, 0))) return;
+            o << "    qG = cmulc(qG, " << guard(e) << ");\n";
+            accG = true;
+            fp64 += 4;
+            return;
+        }
+        const int k = regpos(dq[reg_t]);
+        for (int b = 0; b < 2; ++b) {
+            const std::string e = select_expr(dq, d, sq, reg_t, b);
+            if (e == c2(cd(1, 0))) continue;
+            o << "    qA" << k << "_" << b << " = cmulc(qA" << k << "_" << b << ", " << guard(e) << ");\n";
+            acc[2 * k + b] = 1;
+            fp64 += 4;
+        }
     }
 
     void op(const GlobalOp &g) {
@@ -273,12 +508,20 @@ struct StageGen {
                 if (B < 0) groups.push_back({rho, rho | (1 << A)});
                 else groups.push_back({rho, rho | (1 << B), rho | (1 << A), rho | (1 << A) | (1 << B)});
             }
+            flush_acc(A);
+            if (B >= 0) flush_acc(B);
+            const std::string cond = scalar_cond(smask);
+            if (cond.empty()) {
+                for (auto &grp : groups) linear_absorb(grp, g.m);
+                return;
+            }
+            // a thread/tile-dependent control: pending factors must be applied
+            // on both sides of the branch, so materialise them first
             for (auto &grp : groups)
                 for (int r : grp) flush(r);
-            const std::string cond = scalar_cond(smask);
-            if (!cond.empty()) o << "    if (" << cond << ") {\n";
+            o << "    if (" << cond << ") {\n";
             for (auto &grp : groups) linear(grp, g.m);
-            if (!cond.empty()) o << "    }\n";
+            o << "    }\n";
             return;
         }
         // diagonal: factor(rho, scalars) = controls ? d[bits] : 1
@@ -288,11 +531,38 @@ struct StageGen {
             dq = {g.qa, g.qb};
             d = {g.m[0], g.m[1], g.m[2], g.m[3]};
         }
+        // fold the controls into the diagonal itself (a controlled diagonal is a
+        // diagonal over controls + targets that is 1 unless every control is
+        // set), so a register control costs nothing and a thread/tile control
+        // becomes one more select bit of a runtime accumulator
+        {
+            std::vector<int> cq;
+            for (int q = 0; q < 64; ++q)
+                if ((g.cmask >> q) & 1) cq.push_back(q);
+            if (!cq.empty() && cq.size() + dq.size() <= 8) {
+                const int nc = (int)cq.size(), nt = (int)dq.size();
+                std::vector<cd> full(1u << (nc + nt), cd(1, 0));
+                for (int t = 0; t < (1 << nt); ++t) full[(((1 << nc) - 1) << nt) | t] = d[t];
+                std::vector<int> all = cq;
+                all.insert(all.end(), dq.begin(), dq.end());
+                dq.swap(all);
+                d.swap(full);
+                rcm = 0;
+                smask = 0;
+            }
+        }
         std::vector<int> sq;  // scalar target qubits
         for (int q : dq)
             if (regpos(q) < 0) sq.push_back(q);
         const std::string ccond = scalar_cond(smask);
         const int ns = (int)sq.size();
+        const int nreg = (int)dq.size() - ns;
+        bool signs_only = true;  // +-1 factors: sign flips in a branch are cheaper than accumulating
+        for (const cd &x : d) signs_only &= x.imag() == 0.0 && (x.real() == 1.0 || x.real() == -1.0);
+        if ((ns > 0 || !ccond.empty()) && rcm == 0 && nreg <= 1 && !signs_only) {
+            accumulate(dq, d, sq, ccond);
+            return;
+        }
         for (int combo = 0; combo < (1 << ns); ++combo) {
             std::vector<cd> f(1u << R, cd(1, 0));
             bool any = false;
@@ -342,10 +612,10 @@ bool jit_available(std::string &why) {
     return true;
 }
 
-// Host rendering of the same pass (test infrastructure: tests compile it with
-// gcc and run it on CPU to check the generator against the oracle without a
-// GPU).  Identical op emission; the CTA becomes explicit loops over threads
-// between barriers.
+// Host rendering of the same kernels (test infrastructure: tests compile it
+// with gcc and run it on CPU to check the generator against the oracle
+// without a GPU).  Identical op emission; the CTA becomes explicit loops over
+// threads between barriers and the grid becomes a sequential tile loop.
 const char *kHostPrelude = R"(
 #include <stdint.h>
 typedef unsigned long long u64;
@@ -359,49 +629,101 @@ static inline unsigned swz(unsigned i) {
 }
 static inline double2 ldcs2(const double2 *p) { return *p; }
 static inline void stcs2(double2 *p, double2 v) { *p = v; }
+static inline void stwb2(double2 *p, double2 v) { *p = v; }
+static inline double2 cmulc(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
 )";
 
-std::string jit_source(const Plan &P, int pi, bool host) {
+// grid-wide barrier of the persistent super-pass kernel (all CTAs are
+// co-resident: cooperative launch).  Monotonic counter, reset per launch.
+const char *kGridSync = R"(
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &gen) {
+    __syncthreads();
+    gen += gridDim.x;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        unsigned spins = 0;
+        while (ld_acquire(bar) < gen) {
+            __nanosleep(64);
+            if (++spins > (1u << 27)) __trap();  // never hang the GPU: fail loudly
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+)";
+
+namespace {
+
+// Emits the processing of tiles for one pass: a (persistent, double-buffered
+// on the device) loop over `ntiles` tiles whose global base offset is
+// `base_of(t)`; the tile body is the pass's register stages.
+double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
+                    const std::function<std::string(const std::string &)> &base_of, bool stream_out = true) {
+    double fp64 = 0;
     const DevPass &dp = P.passes[pi];
-    const int n = P.n, m = dp.m, R = P.r, T = 1 << (m - R);
+    const int m = dp.m, R = P.r, T = 1 << (m - R);
     std::vector<int> tq(dp.tq, dp.tq + m);
-    std::ostringstream o;
-    o << "// libqsv specialised pass kernel: n=" << n << " m=" << m << " R=" << R << " pass=" << pi << "\n";
-    // tile base: deposit tile_id into the non-tile qubits
-    std::vector<int> ext;
-    for (int q = 0; q < n; ++q)
-        if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
     std::vector<int> low(tq.begin(), tq.begin() + (m - R)), high(tq.begin() + (m - R), tq.end());
     const std::string thread_loop = host ? "    for (unsigned tid = 0; tid < " + std::to_string(T) + "u; ++tid) {\n" : "";
     const std::string thread_end = host ? "    }\n" : "";
     const std::string barrier = host ? "" : "    __syncthreads();\n";
+    o << "  { // pass " << pi << "\n";
+    o << "  const u64 ntiles = " << ntiles << ";\n";
     if (host) {
-        o << kHostPrelude;
-        o << "extern \"C\" void qsv_pass_host(double2 *psi, u64 n_tiles) {\n";
-        o << "  static double2 tile[" << (1 << m) << "];\n";
-        o << "  for (u64 tile_id = 0; tile_id < n_tiles; ++tile_id) {\n";
-    } else {
-        o << kPrelude;
-        o << "extern \"C\" __global__ void __launch_bounds__(" << T
-          << ") qsv_pass(double2 *__restrict__ psi, u64 n_tiles) {\n";
-        o << "  extern __shared__ double2 tile[];\n";
-        o << "  const unsigned tid = threadIdx.x;\n";
-        o << "  const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
-        o << "  const unsigned tsl = swz(tid);\n";
-        o << "  for (u64 tile_id = blockIdx.x; tile_id < n_tiles; tile_id += gridDim.x) {\n";
-    }
-    o << "    const u64 base = " << deposit_expr("tile_id", ext, true) << ";\n";
-    o << barrier << thread_loop;
-    if (host) {
+        o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
+        o << "    const u64 base = " << base_of("t") << ";\n";
+        o << thread_loop;
         o << "    const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
         o << "    const unsigned tsl = swz(tid);\n";
+        o << "    double2 *p = psi + base + toff;\n";
+        for (int k = 0; k < (1 << R); ++k)
+            o << "    tile[tsl ^ " << swz_host((uint32_t)k * T) << "u] = ldcs2(p + " << deposit((uint64_t)k, high)
+              << "ull);\n";
+        o << thread_end;
+    } else {
+        // two tile buffers: cp.async streams tile t+grid into the spare buffer
+        // while tile t is computed
+        o << "  const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
+        o << "  const unsigned tsl = swz(tid);\n";
+        auto prefetch = [&](const std::string &tv, const std::string &buf_expr) {
+            o << "    { const double2 *g = psi + (" << base_of(tv) << ") + toff;\n";
+            o << "      const unsigned sb = sbase + ((" << buf_expr << ") << " << (m + 4) << ");\n";
+            for (int k = 0; k < (1 << R); ++k)
+                o << "      cp_async16(sb + 16u * (tsl ^ " << swz_host((uint32_t)k * T) << "u), g + "
+                  << deposit((uint64_t)k, high) << "ull);\n";
+            o << "    }\n";
+        };
+        if (jit_double_buffer()) {
+            o << "  u64 t = blockIdx.x;\n  unsigned buf = 0;\n";
+            o << "  if (t < ntiles) {\n";
+            prefetch("t", "0u");
+            o << "  }\n  cp_async_commit();\n";
+            o << "  for (; t < ntiles; t += gridDim.x) {\n";
+            o << "    double2 *tile = smem + (buf << " << m << ");\n";
+            o << "    cp_async_wait_all();\n    __syncthreads();\n";
+            o << "    { const u64 nt = t + gridDim.x;\n    if (nt < ntiles) {\n";
+            prefetch("nt", "buf ^ 1u");
+            o << "    }\n    cp_async_commit(); }\n";
+        } else {
+            // one buffer, more resident CTAs: latency hidden by occupancy
+            o << "  const unsigned buf = 0;\n";
+            o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
+            o << "    double2 *tile = smem;\n";
+            o << "    __syncthreads();\n";
+            prefetch("t", "0u");
+            o << "    cp_async_commit();\n    cp_async_wait_all();\n    __syncthreads();\n";
+        }
+        o << "    const u64 base = " << base_of("t") << ";\n";
+        o << "    double2 *p = psi + base + toff;\n";
     }
-    o << "    double2 *p = psi + base + toff;\n";
-    for (int k = 0; k < (1 << R); ++k) {
-        const uint64_t off = deposit((uint64_t)k, high);
-        o << "    tile[tsl ^ " << swz_host((uint32_t)k * T) << "u] = ldcs2(p + " << off << "ull);\n";
-    }
-    o << thread_end << barrier;
     for (int s = dp.stage_begin; s < dp.stage_end; ++s) {
         const DevStage &st = P.stages[s];
         StageGen g(o, R, tq);
@@ -423,8 +745,10 @@ std::string jit_source(const Plan &P, int pi, bool host) {
             c[rho] = swz_host(off);
             o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         }
+        g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all();
+        fp64 += g.fp64;
         for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
         o << thread_end << barrier << "    }\n";
     }
@@ -434,11 +758,98 @@ std::string jit_source(const Plan &P, int pi, bool host) {
         o << "    const unsigned tsl = swz(tid);\n";
         o << "    double2 *p = psi + base + toff;\n";
     }
-    for (int k = 0; k < (1 << R); ++k) {
-        const uint64_t off = deposit((uint64_t)k, high);
-        o << "    stcs2(p + " << off << "ull, tile[tsl ^ " << swz_host((uint32_t)k * T) << "u]);\n";
+    for (int k = 0; k < (1 << R); ++k)
+        // evict-first stores when the data leaves for HBM; write-back (L2
+        // resident) stores between the inner passes of a super-pass
+        o << "    " << (stream_out ? "stcs2" : "stwb2") << "(p + " << deposit((uint64_t)k, high) << "ull, tile[tsl ^ "
+          << swz_host((uint32_t)k * T)
+          << "u]);\n";
+    o << thread_end;
+    if (!host && jit_double_buffer()) o << "    buf ^= 1u;\n";
+    o << "  }\n  }\n";
+    return fp64;
+}
+
+std::string kernel_head(const Plan &P, int m, bool host, const char *name, const char *params) {
+    std::ostringstream o;
+    const int T = 1 << (m - P.r);
+    if (host) {
+        o << kHostPrelude << "extern \"C\" void " << name << "_host(" << params << ") {\n";
+        o << "  static double2 tile[" << (1 << m) << "];\n";
+    } else {
+        o << kPrelude << kGridSync;
+        // 512 resident threads per SM by default (16 warps, <= 128 registers);
+        // QSV_JIT_MIN_BLOCKS overrides the CTAs-per-SM hint
+        const char *mb = std::getenv("QSV_JIT_MIN_BLOCKS");
+        o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
+          << (mb ? std::atoi(mb) : std::max(1, 512 / T)) << ") "
+          << name << "(" << params << ") {\n";
+        o << "  extern __shared__ double2 smem[];\n";
+        o << "  const unsigned tid = threadIdx.x;\n";
+        o << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);\n";
     }
-    o << thread_end << "  }\n}\n";
+    return o.str();
+}
+
+}  // namespace
+
+std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
+    const DevPass &dp = P.passes[pi];
+    std::ostringstream o;
+    o << "// libqsv specialised pass kernel: n=" << P.n << " m=" << dp.m << " R=" << P.r << " pass=" << pi << "\n";
+    std::vector<int> ext;
+    for (int q = 0; q < P.n; ++q)
+        if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
+    o << kernel_head(P, dp.m, host, "qsv_pass", "double2 *__restrict__ psi, u64 n_tiles");
+    const double f = emit_tile_loop(o, P, pi, host, "n_tiles",
+                                    [&](const std::string &t) { return deposit_expr(t, ext, true); });
+    if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
+    o << "}\n";
+    return o.str();
+}
+
+int super_batch(const Plan &P) {
+    // super-tiles processed together: keep the batch within the L2 budget
+    // (default 64 MB of the 126 MB L2; QSV_L2_BYTES overrides)
+    const char *env = std::getenv("QSV_L2_BYTES");
+    const size_t budget = env ? (size_t)std::atoll(env) : ((size_t)64 << 20);
+    const int s = P.s, n = P.n;
+    int b = 0;
+    while (b < n - s && ((size_t)16 << (s + b + 1)) <= budget) ++b;
+    return b;  // log2 of the batch size
+}
+
+std::string jit_super_source(const Plan &P, int si, bool host) {
+    const SuperPass &sp = P.supers[si];
+    const int n = P.n, s = popc64(sp.mask), m = P.m, lb = super_batch(P);
+    std::ostringstream o;
+    o << "// libqsv super-pass kernel: n=" << n << " s=" << s << " m=" << m << " inner passes "
+      << sp.pass_begin << ".." << sp.pass_end - 1 << " batch=2^" << lb << "\n";
+    std::vector<int> outside;
+    for (int q = 0; q < n; ++q)
+        if (!((sp.mask >> q) & 1)) outside.push_back(q);
+    o << kernel_head(P, m, host, "qsv_super", "double2 *__restrict__ psi, u64 n_batches, unsigned *__restrict__ bar");
+    if (!host) o << "  unsigned gen = 0;\n";
+    o << "  for (u64 batch = 0; batch < n_batches; ++batch) {\n";
+    for (int pi = sp.pass_begin; pi < sp.pass_end; ++pi) {
+        const DevPass &dp = P.passes[pi];
+        std::vector<int> inner;  // super-tile qubits outside this pass's tile
+        for (int q = 0; q < n; ++q)
+            if (((sp.mask >> q) & 1) && !((dp.tile_mask >> q) & 1)) inner.push_back(q);
+        const int ib = (int)inner.size();  // = s - m
+        const std::string ntiles = "(1ull << " + std::to_string(ib + lb) + ")";
+        emit_tile_loop(
+            o, P, pi, host, ntiles,
+            [&, ib](const std::string &t) {
+                const std::string lowpart = "(" + t + " & ((1ull << " + std::to_string(ib) + ") - 1ull))";
+                const std::string stile =
+                    "((batch << " + std::to_string(lb) + ") + (" + t + " >> " + std::to_string(ib) + "))";
+                return "(" + deposit_expr(lowpart, inner, true) + ") | (" + deposit_expr(stile, outside, true) + ")";
+            },
+            pi + 1 == sp.pass_end);
+        if (!host) o << "  grid_sync(bar, gen);\n";
+    }
+    o << "  }\n}\n";
     return o.str();
 }
 
@@ -474,7 +885,7 @@ namespace {
 
 struct CacheEntry {
     CUfunction fn = nullptr;
-    int smem_set = 0;
+    int grid = 0;  // persistent grid: resident CTAs per SM x SMs
 };
 
 std::mutex g_cache_mu;
@@ -482,20 +893,60 @@ std::map<std::pair<int, std::string>, CacheEntry> g_cache;  // (device, source) 
 
 }  // namespace
 
+// a compile unit: one generated kernel
+struct Unit {
+    std::string src, name, cubin, log;
+    int m = 0;
+    bool super = false;
+    int index = 0;  // pass or super-pass index
+};
+
+bool use_supers(const Plan &P) { return P.s > P.m; }
+
+void jit_choose_supers(Plan &P, int sms) {
+    P.super_use.assign(P.supers.size(), 0);
+    if (!use_supers(P)) return;
+    // B200 sm_100a: 64 FP64 lanes/SM at ~1.9 GHz, ~60% sustained on this
+    // kernel shape; HBM ~6.0 TB/s achieved.  The persistent super kernel adds
+    // ~20% on its compute (tails + grid barriers, measured).
+    const double amps = std::ldexp(1.0, P.n);
+    const double fp64_rate = (double)sms * 64.0 * 1.9e9 * 0.6;
+    const double t_hbm = 32.0 * amps / 6.0e12;
+    for (size_t si = 0; si < P.supers.size(); ++si) {
+        const SuperPass &sp = P.supers[si];
+        if (sp.pass_end - sp.pass_begin < 2) continue;
+        double flat = 0, comp = 0;
+        for (int i = sp.pass_begin; i < sp.pass_end; ++i) {
+            double f = 0;
+            jit_source(P, i, false, &f);
+            const double t = amps * f / fp64_rate;
+            flat += std::max(t_hbm, t);
+            comp += t;
+        }
+        P.super_use[si] = std::max(t_hbm, 1.2 * comp) < flat ? 1 : 0;
+    }
+}
+
 int jit_prepare(Plan &P, int device, std::string &err) {
     if (P.jit_device == device && P.jit_funcs.size() == P.passes.size()) return QSV_OK;
     if (!jit_available(err)) return QSV_E_DEVICE;
     Driver &drv = driver();
-    const size_t np = P.passes.size();
-    std::vector<std::string> srcs(np), cubins(np), logs(np);
-    std::vector<void *> funcs(np, nullptr);
+    std::vector<Unit> units;
+    for (size_t i = 0; i < P.passes.size(); ++i)
+        units.push_back(Unit{jit_source(P, (int)i), "qsv_pass", {}, {}, P.passes[i].m, false, (int)i});
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    jit_choose_supers(P, sms);
+    for (size_t si = 0; si < P.supers.size(); ++si)
+        if (P.super_use[si])
+            units.push_back(Unit{jit_super_source(P, (int)si), "qsv_super", {}, {}, P.m, true, (int)si});
+    std::vector<CacheEntry> found(units.size());
     std::vector<int> todo;
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        for (size_t i = 0; i < np; ++i) {
-            srcs[i] = jit_source(P, (int)i);
-            auto it = g_cache.find({device, srcs[i]});
-            if (it != g_cache.end()) funcs[i] = it->second.fn;
+        for (size_t i = 0; i < units.size(); ++i) {
+            auto it = g_cache.find({device, units[i].src});
+            if (it != g_cache.end()) found[i] = it->second;
             else todo.push_back((int)i);
         }
     }
@@ -507,8 +958,8 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         for (unsigned t = 0; t < std::min<size_t>(hw, todo.size()); ++t)
             pool.emplace_back([&] {
                 for (size_t k; (k = next.fetch_add(1)) < todo.size();) {
-                    const int i = todo[k];
-                    cubins[i] = jit_compile_cubin(srcs[i], logs[i]);
+                    Unit &u = units[todo[k]];
+                    u.cubin = jit_compile_cubin(u.src, u.log);
                 }
             });
         for (auto &th : pool) th.join();
@@ -517,45 +968,81 @@ int jit_prepare(Plan &P, int device, std::string &err) {
     cudaFree(nullptr);  // make the primary context current for the driver API
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (int i : todo) {
-        if (cubins[i].empty()) {
-            err = "NVRTC failed for pass " + std::to_string(i) + ": " + logs[i];
+        Unit &u = units[i];
+        if (u.cubin.empty()) {
+            err = "NVRTC failed for " + u.name + " " + std::to_string(u.index) + ": " + u.log;
             return QSV_E_DEVICE;
         }
         CUmodule mod;
         CUfunction fn;
-        CUresult r = drv.ModuleLoadData(&mod, cubins[i].data());
-        if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&fn, mod, "qsv_pass");
-        const int smem = (int)((size_t)16 << P.passes[i].m);
+        CUresult r = drv.ModuleLoadData(&mod, u.cubin.data());
+        if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&fn, mod, u.name.c_str());
+        const int smem = (int)((size_t)(jit_double_buffer() ? 32 : 16) << u.m);  // tile buffer(s)
         if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
-        if (r != CUDA_SUCCESS) {
+        int per_sm = 0;
+        if (r == CUDA_SUCCESS)
+            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 1 << (u.m - P.r), (size_t)smem);
+        if (r != CUDA_SUCCESS || per_sm < 1) {
             const char *s = nullptr;
-            drv.GetErrorString(r, &s);
-            err = std::string("loading specialised kernel: ") + (s ? s : "?");
+            if (r != CUDA_SUCCESS) drv.GetErrorString(r, &s);
+            err = std::string("loading specialised kernel: ") + (s ? s : "zero occupancy");
             return QSV_E_DEVICE;
         }
-        g_cache[{device, srcs[i]}] = CacheEntry{fn, smem};
-        funcs[i] = fn;
+        found[i] = CacheEntry{fn, per_sm * sms};
+        g_cache[{device, u.src}] = found[i];
     }
-    P.jit_funcs = funcs;
+    P.jit_funcs.assign(P.passes.size(), nullptr);
+    P.jit_grids.assign(P.passes.size(), 0);
+    P.jit_super_funcs.assign(P.supers.size(), nullptr);
+    P.jit_super_grids.assign(P.supers.size(), 0);
+    for (size_t i = 0; i < units.size(); ++i) {
+        if (units[i].super) {
+            P.jit_super_funcs[units[i].index] = found[i].fn;
+            P.jit_super_grids[units[i].index] = found[i].grid;
+        } else {
+            P.jit_funcs[units[i].index] = found[i].fn;
+            P.jit_grids[units[i].index] = found[i].grid;
+        }
+    }
     P.jit_device = device;
     return QSV_OK;
+}
+
+static int cu_fail(CUresult r, const char *what, std::string &err) {
+    const char *s = nullptr;
+    driver().GetErrorString(r, &s);
+    err = std::string(what) + ": " + (s ? s : "?");
+    return QSV_E_DEVICE;
 }
 
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err) {
     const DevPass &dp = P.passes[pass];
     const int m = dp.m, T = 1 << (m - P.r);
     unsigned long long n_tiles = 1ull << (n - m);
-    const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, 0x7fffffffull);
+    const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, (unsigned long long)P.jit_grids[pass]);
     void *args[] = {&psi, &n_tiles};
     const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, T, 1, 1,
-                                             (unsigned)((size_t)16 << m), (CUstream)stream, args, nullptr);
-    if (r != CUDA_SUCCESS) {
-        const char *s = nullptr;
-        driver().GetErrorString(r, &s);
-        err = std::string("cuLaunchKernel: ") + (s ? s : "?");
+                                             (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
+                                             (CUstream)stream, args, nullptr);
+    return r == CUDA_SUCCESS ? QSV_OK : cu_fail(r, "cuLaunchKernel", err);
+}
+
+int jit_launch_super(const Plan &P, int si, void *psi, unsigned *bar, cudaStream_t stream, std::string &err) {
+    const int m = P.m, T = 1 << (m - P.r), s = popc64(P.supers[si].mask), lb = super_batch(P);
+    unsigned long long n_batches = 1ull << (P.n - s - lb);
+    cudaError_t ce = cudaMemsetAsync(bar, 0, sizeof(unsigned), stream);
+    if (ce != cudaSuccess) {
+        err = std::string("barrier reset: ") + cudaGetErrorString(ce);
         return QSV_E_DEVICE;
     }
-    return QSV_OK;
+    const unsigned long long tiles = 1ull << (s - m + lb);
+    const unsigned grid = (unsigned)std::min<unsigned long long>(tiles, (unsigned long long)P.jit_super_grids[si]);
+    void *args[] = {&psi, &n_batches, &bar};
+    // every CTA must be co-resident for the grid barrier: cooperative launch
+    const CUresult r = driver().LaunchCooperativeKernel((CUfunction)P.jit_super_funcs[si], grid, 1, 1, T, 1, 1,
+                                                        (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
+                                                        (CUstream)stream, args);
+    return r == CUDA_SUCCESS ? QSV_OK : cu_fail(r, "cuLaunchCooperativeKernel", err);
 }
 
 }  // namespace qsv

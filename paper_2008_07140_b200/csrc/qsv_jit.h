@@ -24,7 +24,13 @@ bool jit_available(std::string &why);
 
 // CUDA source of the specialised kernel for pass `pass` of plan P (extern "C"
 // entry point `qsv_pass`).  Pure host code (testable without a GPU).
-std::string jit_source(const Plan &P, int pass, bool host = false);
+std::string jit_source(const Plan &P, int pass, bool host = false, double *fp64_per_amp = nullptr);
+
+// Cost model: decides for every super-pass whether its inner passes run as one
+// L2-resident persistent kernel (one HBM pass) or as flat passes (one HBM pass
+// each), from the FP64 work the generator emits per amplitude.  Fills
+// P.super_use.  `sms` = multiprocessor count.
+void jit_choose_supers(Plan &P, int sms);
 
 // Compiles (or fetches from the cache) every pass kernel of P for `device`;
 // fills P.jit_funcs.  Returns QSV_OK or an error status with `err` set.
@@ -34,7 +40,24 @@ int jit_prepare(Plan &P, int device, std::string &err);
 // NVRTC log in `log`; empty cubin on failure.
 std::string jit_compile_cubin(const std::string &src, std::string &log);
 
-// Launches pass `pass` of a prepared plan.
+// Source of the persistent kernel of super-pass `si` (all its inner passes on
+// L2-resident super-tiles, grid barrier between inner passes).
+std::string jit_super_source(const Plan &P, int si, bool host = false);
+
+// log2 of the number of super-tiles processed together (L2 budget ~64 MB)
+int super_batch(const Plan &P);
+
+// cp.async double buffering of tiles in the generated kernels (QSV_JIT_DBUF)
+bool jit_double_buffer();
+
+// true when the plan's super-passes run as L2-resident persistent kernels
+bool use_supers(const Plan &P);
+
+// Launches pass `pass` of a prepared plan over the whole state.
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err);
+
+// Launches the persistent kernel of super-pass `si` (needs a 4-byte device
+// counter for the grid barrier).
+int jit_launch_super(const Plan &P, int si, void *psi, unsigned *bar, cudaStream_t stream, std::string &err);
 
 }  // namespace qsv

@@ -24,7 +24,11 @@ namespace qsv {
 
 static inline int popc(uint64_t x) { return std::popcount(x); }
 
-void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L) {
+void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int &s) {
+    // L2 super-tiles are opt-in (super_qubits > tile_qubits): on B200 the
+    // persistent super-pass kernel measured slower than flat passes for the
+    // FP64-bound RQC/QFT workloads (grid-barrier tails), see DESIGN.md
+    s = (opt && opt->super_qubits > 0) ? opt->super_qubits : 0;
     m = (opt && opt->tile_qubits > 0) ? opt->tile_qubits : 12;
     r = (opt && opt->reg_qubits > 0) ? opt->reg_qubits : 4;
     L = (opt && opt->low_qubits > 0) ? opt->low_qubits : 5;
@@ -338,89 +342,129 @@ DevOp lower_op(const StageOp &o, int n, uint64_t tmask, const int32_t *regpos_of
 
 }  // namespace
 
-Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L) {
+namespace {
+
+// Emits one pass (tile + register stages) for `taken` (program order) into P.
+// The tile holds the forced low qubits plus the non-diagonal targets of
+// `taken`, padded with the lowest qubits of `pool` (the super-tile).
+void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int> &taken, uint64_t tile_res,
+               uint64_t pool) {
+    const int n = P.n, m = P.m, r = P.r;
+    uint64_t tmask = tile_res;
+    for (int q = 0; q < n && popc(tmask) < m; ++q)
+        if ((pool >> q) & 1) tmask |= 1ull << q;
+
+    DevPass dp;
+    std::memset(&dp, 0, sizeof(dp));
+    dp.tile_mask = tmask;
+    dp.m = m;
+    {
+        int j = 0;
+        for (int q = 0; q < n; ++q)
+            if ((tmask >> q) & 1) dp.tq[j++] = q;
+    }
+    for (int e = 0; e < (1 << kLoTabBits); ++e) dp.lo_tab[e] = (e < (1 << m)) ? deposit(e, tmask) : 0;
+    for (int e = 0; e < (1 << kHiTabBits); ++e)
+        dp.hi_tab[e] = (m > kLoTabBits && e < (1 << (m - kLoTabBits))) ? deposit((uint64_t)e << kLoTabBits, tmask) : 0;
+    dp.stage_begin = (int32_t)P.stages.size();
+    P.pass_op_begin.push_back((int64_t)P.ops.size());
+
+    // stages over register qubits
+    std::vector<int> rem = taken;
+    int stage_in_pass = 0;
+    while (!rem.empty()) {
+        Absorber regs;
+        regs.capacity = r;
+        std::vector<int> st_taken, st_def;
+        for (int gi : rem) (regs.offer(recs[gi]) ? st_taken : st_def).push_back(gi);
+        uint64_t rmask = regs.resident;
+        // pad with the highest unused tile qubits
+        for (int q = n - 1; q >= 0 && popc(rmask) < r; --q)
+            if (((tmask >> q) & 1) && !((rmask >> q) & 1)) rmask |= 1ull << q;
+
+        std::vector<StageOp> sops;
+        for (int gi : st_taken) append_fused(sops, make_op(recs[gi]));
+
+        DevStage ds;
+        std::memset(&ds, 0, sizeof(ds));
+        int k = 0;
+        int32_t regpos_of_local[64];
+        for (int j = 0; j < 64; ++j) regpos_of_local[j] = -1;
+        for (int q = 0; q < n; ++q) {
+            if ((rmask >> q) & 1) {
+                const int lb = local_bit(tmask, q);
+                ds.rb[k] = lb;
+                regpos_of_local[lb] = k;
+                ds.reg_local_mask |= 1u << lb;
+                ++k;
+            }
+        }
+        ds.op_begin = (int32_t)P.ops.size();
+        for (const StageOp &o : sops) {
+            P.ops.push_back(lower_op(o, n, tmask, regpos_of_local));
+            P.gops.push_back(o);
+            P.op_stage.push_back(stage_in_pass);
+        }
+        ds.op_end = (int32_t)P.ops.size();
+        P.stages.push_back(ds);
+        P.stage_regs.push_back(rmask);
+        ++stage_in_pass;
+        rem.swap(st_def);
+    }
+    dp.stage_end = (int32_t)P.stages.size();
+    P.passes.push_back(dp);
+}
+
+}  // namespace
+
+// Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy
+// absorption with capacity s); its gates are then split into ordinary passes
+// whose tiles lie inside S.  The executor runs all inner passes of a
+// super-pass on one L2-resident super-tile (2^s amplitudes with the other
+// qubits fixed) before moving to the next, so HBM sees one read + one write
+// per super-pass while the inner passes stream through L2.  s >= n keeps the
+// whole state in one super-tile; s == m degenerates to one pass per
+// super-pass.
+Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s) {
     Plan P;
     P.n = n;
     P.m = m;
     P.r = r;
     P.L = L;
+    P.s = std::max(m, std::min(s, n));
     P.gates = (int64_t)recs.size();
     const uint64_t low = L > 0 ? ((1ull << L) - 1) : 0;
+    const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
 
     std::vector<int> remaining(recs.size());
     for (size_t i = 0; i < recs.size(); ++i) remaining[i] = (int)i;
 
     while (!remaining.empty()) {
-        Absorber tile;
-        tile.resident = low;
-        tile.capacity = m;
-        std::vector<int> taken, deferred;
-        for (int gi : remaining) (tile.offer(recs[gi]) ? taken : deferred).push_back(gi);
+        Absorber sup;
+        sup.resident = low;
+        sup.capacity = P.s;
+        std::vector<int> s_taken, s_def;
+        for (int gi : remaining) (sup.offer(recs[gi]) ? s_taken : s_def).push_back(gi);
+        uint64_t smask = sup.resident;
+        for (int q = 0; q < n && popc(smask) < P.s; ++q) smask |= 1ull << q;
+        smask &= all;
 
-        // pad the tile with the lowest unused qubits (coalescing)
-        uint64_t tmask = tile.resident;
-        for (int q = 0; q < n && popc(tmask) < m; ++q) tmask |= 1ull << q;
-
-        DevPass dp;
-        std::memset(&dp, 0, sizeof(dp));
-        dp.tile_mask = tmask;
-        dp.m = m;
-        {
-            int j = 0;
-            for (int q = 0; q < n; ++q)
-                if ((tmask >> q) & 1) dp.tq[j++] = q;
-        }
-        for (int e = 0; e < (1 << kLoTabBits); ++e) dp.lo_tab[e] = (e < (1 << m)) ? deposit(e, tmask) : 0;
-        for (int e = 0; e < (1 << kHiTabBits); ++e)
-            dp.hi_tab[e] = (m > kLoTabBits && e < (1 << (m - kLoTabBits))) ? deposit((uint64_t)e << kLoTabBits, tmask) : 0;
-        dp.stage_begin = (int32_t)P.stages.size();
-        P.pass_op_begin.push_back((int64_t)P.ops.size());
-
-        // stages over register qubits
-        std::vector<int> rem = taken;
-        int stage_in_pass = 0;
+        SuperPass spp;
+        spp.mask = smask;
+        spp.pass_begin = (int32_t)P.passes.size();
+        std::vector<int> rem = s_taken;
         while (!rem.empty()) {
-            Absorber regs;
-            regs.capacity = r;
-            std::vector<int> st_taken, st_def;
-            for (int gi : rem) (regs.offer(recs[gi]) ? st_taken : st_def).push_back(gi);
-            uint64_t rmask = regs.resident;
-            // pad with the highest unused tile qubits
-            for (int q = n - 1; q >= 0 && popc(rmask) < r; --q)
-                if (((tmask >> q) & 1) && !((rmask >> q) & 1)) rmask |= 1ull << q;
-
-            std::vector<StageOp> sops;
-            for (int gi : st_taken) append_fused(sops, make_op(recs[gi]));
-
-            DevStage ds;
-            std::memset(&ds, 0, sizeof(ds));
-            int k = 0;
-            int32_t regpos_of_local[64];
-            for (int j = 0; j < 64; ++j) regpos_of_local[j] = -1;
-            for (int q = 0; q < n; ++q) {
-                if ((rmask >> q) & 1) {
-                    const int lb = local_bit(tmask, q);
-                    ds.rb[k] = lb;
-                    regpos_of_local[lb] = k;
-                    ds.reg_local_mask |= 1u << lb;
-                    ++k;
-                }
-            }
-            ds.op_begin = (int32_t)P.ops.size();
-            for (const StageOp &o : sops) {
-                P.ops.push_back(lower_op(o, n, tmask, regpos_of_local));
-                P.gops.push_back(o);
-                P.op_stage.push_back(stage_in_pass);
-            }
-            ds.op_end = (int32_t)P.ops.size();
-            P.stages.push_back(ds);
-            P.stage_regs.push_back(rmask);
-            ++stage_in_pass;
-            rem.swap(st_def);
+            Absorber tile;
+            tile.resident = low;
+            tile.capacity = m;
+            std::vector<int> taken, deferred;
+            for (int gi : rem) (tile.offer(recs[gi]) ? taken : deferred).push_back(gi);
+            emit_pass(P, recs, taken, tile.resident, smask);
+            rem.swap(deferred);
         }
-        dp.stage_end = (int32_t)P.stages.size();
-        P.passes.push_back(dp);
-        remaining.swap(deferred);
+        spp.pass_end = (int32_t)P.passes.size();
+        P.supers.push_back(spp);
+        remaining.swap(s_def);
     }
     P.pass_op_begin.push_back((int64_t)P.ops.size());
     return P;

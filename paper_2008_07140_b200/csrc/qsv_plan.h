@@ -94,8 +94,16 @@ struct GateRec {
     uint64_t dmask = 0;  // qubits acted on diagonally (controls, targets of diagonal gates)
 };
 
+// A super-pass: inner passes [pass_begin, pass_end) whose tiles lie inside
+// the super-tile qubits `mask` (executed super-tile by super-tile through L2).
+struct SuperPass {
+    uint64_t mask = 0;
+    int32_t pass_begin = 0, pass_end = 0;
+};
+
 struct Plan {
-    int n = 0, m = 0, r = 0, L = 0;
+    int n = 0, m = 0, r = 0, L = 0, s = 0;
+    std::vector<SuperPass> supers;
     int64_t gates = 0;
     std::vector<DevPass> passes;
     std::vector<DevStage> stages;
@@ -109,6 +117,10 @@ struct Plan {
     int device = -1;
     // specialised kernels (qsv_jit.cpp), one CUfunction per pass
     std::vector<void *> jit_funcs;
+    std::vector<int> jit_grids;
+    std::vector<void *> jit_super_funcs;  // per super-pass (nullptr: run its inner passes flat)
+    std::vector<int> jit_super_grids;
+    std::vector<int> super_use;  // cost-model choice per super-pass (jit_choose_supers)
     int jit_device = -1;
 };
 
@@ -117,8 +129,8 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector
                std::string &msg);
 
 // Builds the fused schedule.  m, r, L already clamped to the state size.
-Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L);
+Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s);
 
-void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L);
+void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int &s);
 
 }  // namespace qsv

@@ -68,3 +68,54 @@ def run_plan_host(records: np.ndarray, n: int, psi: np.ndarray, **opts) -> np.nd
         return out
     finally:
         N.lib().qsv_plan_destroy(h)
+
+
+def super_source(h, si: int, host: bool) -> str:
+    L = N.lib()
+    need = C.c_int64()
+    N.check(L.qsv_plan_super_source(h, si, int(host), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    N.check(L.qsv_plan_super_source(h, si, int(host), buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+def super_batch_log2(n: int, s: int, budget: int = 64 << 20) -> int:
+    b = 0
+    while b < n - s and (16 << (s + b + 1)) <= budget:
+        b += 1
+    return b
+
+
+def run_plan_host_super(records: np.ndarray, n: int, psi: np.ndarray, budget: int = 64 << 20,
+                        **opts) -> np.ndarray:
+    """Execute the plan super-pass by super-pass through the generated
+    persistent super kernels (host rendering), like the GPU executor does."""
+    import os
+
+    os.environ["QSV_L2_BYTES"] = str(budget)
+    h = plan_handle(records, n, **opts)
+    try:
+        info = N.qsv_plan_info()
+        N.check(N.lib().qsv_plan_summary(h, C.byref(info)))
+        out = np.ascontiguousarray(psi, dtype=np.complex128).copy()
+        passes = []
+        for p in range(info.passes):
+            pi = N.qsv_pass_info()
+            N.check(N.lib().qsv_plan_pass(h, p, C.byref(pi)))
+            passes.append((pi.super_index, pi.m, bin(pi.super_mask).count("1")))
+        for si in range(info.super_passes):
+            mine = [p for p, (s_i, _, _) in enumerate(passes) if s_i == si]
+            s = passes[mine[0]][2]
+            if len(mine) > 1 and info.super_qubits > info.tile_qubits:
+                src = super_source(h, si, True)
+                lib = _compile(src.replace("qsv_super_host", "qsv_pass_host"))
+                lb = super_batch_log2(n, info.super_qubits, budget)
+                lib.qsv_pass_host.argtypes = [C.c_void_p, C.c_ulonglong, C.c_void_p]
+                lib.qsv_pass_host(out.ctypes.data, 1 << (n - s - lb), None)
+            else:
+                for p in mine:
+                    lib = _compile(kernel_source(h, p, True))
+                    lib.qsv_pass_host(out.ctypes.data, 1 << (n - passes[p][1]))
+        return out
+    finally:
+        N.lib().qsv_plan_destroy(h)

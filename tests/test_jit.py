@@ -90,7 +90,60 @@ def test_device_source_compiles_for_sm100a():
         src = kernel_source(h, 0, False)
     finally:
         N.lib().qsv_plan_destroy(h)
-    assert "qsv_pass" in src and "__launch_bounds__(256)" in src
+    assert "qsv_pass" in src and "__launch_bounds__(256," in src and "cp.async" in src
     size = C.c_int64()
     N.check(N.lib().qsv_jit_compile(src.encode(), C.byref(size)))
     assert size.value > 1000
+
+
+@pytest.mark.parametrize("n,m,s,budget", [(12, 6, 9, 64 << 20), (12, 6, 9, 16 << 9), (14, 7, 10, 16 << 11),
+                                          (13, 6, 13, 64 << 20)])
+def test_generated_super_pass_kernels(n, m, s, budget):
+    """Two-level schedule: persistent super-pass kernels (inner passes on
+    super-tiles, batches of super-tiles, grid barrier) vs the oracle."""
+    from jit_host import run_plan_host_super
+
+    prog = parse_program(workloads.rqc_for_qubits(n, 10, n))
+    psi = workloads.gaussian_state(n, 5)
+    ref = O.run_full(prog, initial=psi).state.amplitudes
+    out = run_plan_host_super(compile_gates(prog.gate_instructions()), n, psi, budget=budget, tile_qubits=m,
+                              reg_qubits=4, low_qubits=3, super_qubits=s)
+    assert np.abs(out - ref).max() <= 1e-12
+
+
+def test_super_plan_reduces_hbm_passes():
+    prog = parse_program(workloads.rqc_text(5, 6, 24, 0))
+    recs = compile_gates(prog.gate_instructions())
+    for s, most in ((21, 5), (0, 16)):
+        h = plan_handle(recs, 30, super_qubits=s)
+        info = N.qsv_plan_info()
+        N.check(N.lib().qsv_plan_summary(h, C.byref(info)))
+        N.lib().qsv_plan_destroy(h)
+        assert info.super_passes <= most, (s, info.super_passes)
+    src_h = plan_handle(recs, 30, super_qubits=21)
+    try:
+        from jit_host import super_source
+
+        src = super_source(src_h, 0, False)
+    finally:
+        N.lib().qsv_plan_destroy(src_h)
+    assert "grid_sync" in src and "qsv_super" in src
+    size = C.c_int64()
+    N.check(N.lib().qsv_jit_compile(src.encode(), C.byref(size)))
+
+
+@pytest.mark.parametrize("cfg", [dict(tile_qubits=6, reg_qubits=4, low_qubits=3),
+                                 dict(tile_qubits=7, reg_qubits=3, low_qubits=2, super_qubits=10)])
+def test_generated_qft_runtime_diagonals(cfg):
+    """QFT: controlled phases between register, thread and tile qubits go
+    through the runtime diagonal accumulators of the generated kernels."""
+    from jit_host import run_plan_host_super
+
+    n = 12
+    psi = workloads.gaussian_state(n, 9)
+    fwd = parse_program(workloads.qft_text(n))
+    out = run_plan_host_super(compile_gates(fwd.gate_instructions()), n, psi, **cfg)
+    assert np.abs(out - np.sqrt(1 << n) * np.fft.ifft(psi)).max() <= 1e-12
+    rt = parse_program(workloads.qft_text(n, round_trip=True))
+    out = run_plan_host_super(compile_gates(rt.gate_instructions()), n, psi, **cfg)
+    assert np.abs(out - psi).max() <= 1e-12
