@@ -203,8 +203,55 @@ def run_reference(args) -> None:
 # --------------------------------------------------------------------------
 
 
+def run_traj(args) -> None:
+    """BASELINE config 5: 1024 depolarising trajectories of the 4x6, 20-cycle RQC
+    (n=24, p=1e-3), split over ranks as independent replicas (no collective but
+    the final result gather)."""
+    import torch
+
+    from paper_2008_07140_b200 import workloads
+    from paper_2008_07140_b200.program import parse_program
+    from paper_2008_07140_b200.trajectories import run_trajectories
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    prog = parse_program(workloads.rqc_text(4, 6, 20, seed=SEED))
+    n_traj = args.trajectories
+    run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
+                           dedup=args.dedup)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    tot = torch.tensor([float(rep.gate_updates), float(rep.unique_runs), dt], dtype=torch.float64)
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = tot.cuda()
+        dist.all_reduce(tt[:2])
+        dist.all_reduce(tt[2:], op=dist.ReduceOp.MAX)
+        tot = tt.cpu()
+    updates, unique, dt = float(tot[0]), int(tot[1]), float(tot[2])
+    if rank == 0:
+        line = {"metric": METRIC, "value": updates / dt, "unit": UNIT, "n_gpus": world, "steps": 1,
+                "warmup": 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+                "config": {"workload": f"C5: {n_traj} depolarising trajectories, RQC 4x6 20 cycles, p=1e-3",
+                           "n_qubits": 24, "trajectories": n_traj, "unique_simulations": unique,
+                           "dedup": bool(args.dedup), "timing": "host wall clock around the batch"}}
+        print(json.dumps(line), flush=True)
+
+
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
+    if args.workload == "traj":
+        run_traj(args)
+        return
     if world > 1:
         from paper_2008_07140_b200 import distributed
 
@@ -341,7 +388,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--qubits", type=int, default=0)
-    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft"))
+    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj"))
+    ap.add_argument("--trajectories", type=int, default=1024)
+    ap.add_argument("--dedup", action="store_true")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--regs", type=int, default=0)
     ap.add_argument("--low", type=int, default=0)

@@ -1,0 +1,101 @@
+"""Batched depolarising-noise trajectories (BASELINE config 5).
+
+Every trajectory t replays the reference's trajectory semantics
+(`run_full(prog, default_rng(seed_t), make_noise_model("depolarizing", p))`,
+statevector.py:343-357 + noise.py:188-222) with the Pauli branch of every
+<=2-qubit gate pre-sampled on the host (`workloads.sample_pauli_insertions`)
+and inserted as explicit X/Y/Z gates before that gate, so each trajectory is a
+noiseless program run by the fused engine.
+
+Execution on one GPU: one device state is reused for all trajectories;
+trajectories without an error share one program, hence one plan whose
+specialised kernels are compiled once (cache by source); trajectories with
+errors each have a distinct gate list and run through the interpreted fused
+kernel (no per-trajectory NVRTC compile).  With `dedup=True` the error-free
+trajectories are simulated once and the result reused - reported separately
+(`TrajectoryReport.unique_runs`).  Across GPUs trajectories are independent
+replicas: rank r takes t = r, r+P, ... and results are gathered on rank 0.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import statevector as SV
+from .program import Program
+from .workloads import noisy_trajectory_program, sample_pauli_insertions, trajectory_seed
+
+
+@dataclass
+class TrajectoryReport:
+    n_qubits: int
+    trajectories: list          # trajectory ids handled here
+    errors: list                # number of inserted Paulis per trajectory
+    probe_qubits: tuple
+    tables: np.ndarray          # PMEASURE table over probe qubits per trajectory
+    norms: np.ndarray
+    kept: dict = field(default_factory=dict)   # trajectory id -> amplitudes
+    gate_updates: int = 0       # sum over trajectories of (gates incl. Paulis) * 2^n
+    unique_runs: int = 0
+    seconds: float = 0.0
+
+
+def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0, *,
+                     probe_qubits=(0, 1, 2), keep=(), dedup: bool = False, device: int = 0,
+                     stream=None, rank: int = 0, world: int = 1, state: SV.StateVector | None = None,
+                     options=None) -> TrajectoryReport:
+    n = program.qubit_count
+    mine = list(range(rank, n_traj, world))
+    if state is None:
+        state = SV.init_state(n, max_qubits=max(n, SV.DEFAULT_MAX_QUBITS), device=device, stream=stream)
+    L = N.lib()
+    opts_clean = options or N.options()
+    opts_noisy = N.options(fuse=True, jit=-1, tile_qubits=opts_clean.tile_qubits,
+                           reg_qubits=opts_clean.reg_qubits, low_qubits=opts_clean.low_qubits)
+    clean_gates = [i for i in program.instructions if i.is_gate]
+    clean_rec = SV.compile_gates(clean_gates)
+    clean_plan = C.c_void_p()
+    N.check(L.qsv_plan_create(clean_rec.ctypes.data, len(clean_rec), n, C.byref(opts_clean),
+                              C.byref(clean_plan)))
+    pq = np.asarray(probe_qubits, dtype=np.int32)
+    tables = np.zeros((len(mine), 1 << len(pq)))
+    norms = np.zeros(len(mine))
+    errors, kept = [], {}
+    clean_cache = None
+    updates = 0
+    unique = 0
+    t0 = time.perf_counter()
+    try:
+        for k, t in enumerate(mine):
+            seed = trajectory_seed(base_seed, t)
+            ins = sample_pauli_insertions(program, p, seed)
+            n_err = sum(len(v) for v in ins.values())
+            errors.append(n_err)
+            updates += (len(clean_gates) + n_err) << n
+            if n_err == 0 and dedup and clean_cache is not None and t not in keep:
+                tables[k], norms[k] = clean_cache
+                continue
+            state.set_basis(0)
+            stats = N.qsv_run_stats()
+            if n_err == 0:
+                N.check(L.qsv_plan_execute(state.handle, clean_plan, C.byref(opts_clean), C.byref(stats)))
+            else:
+                noisy = noisy_trajectory_program(program, p, seed)
+                rec = SV.compile_gates([i for i in noisy.instructions if i.is_gate])
+                N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats)))
+            unique += 1
+            tables[k] = SV.pmeasure(state, pq)
+            norms[k] = state.norm_sq()
+            if t in keep:
+                kept[t] = state.amplitudes
+            if n_err == 0:
+                clean_cache = (tables[k].copy(), norms[k])
+    finally:
+        L.qsv_plan_destroy(clean_plan)
+    return TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
+                            time.perf_counter() - t0)

@@ -187,3 +187,40 @@ def test_errors_and_ceiling():
     with pytest.raises(errors.ParseError):
         SV.apply_single_qubit(st, gates.H, 7)
     assert np.array_equal(SV.init_state(3).amplitudes, [1, 0, 0, 0, 0, 0, 0, 0])
+
+
+def test_trajectories_vs_oracle():
+    """C5 semantics on a small grid with many errors: every trajectory equals the
+    oracle running the reference noisy-gate rule with the same seed."""
+    from paper_2008_07140_b200.noise import make_noise_model
+    from paper_2008_07140_b200.trajectories import run_trajectories
+    from paper_2008_07140_b200.workloads import trajectory_seed
+
+    prog = parse_program(workloads.rqc_text(3, 4, 8, seed=2))
+    keep = tuple(range(12))
+    rep = run_trajectories(prog, 0.05, 12, base_seed=7, probe_qubits=(0, 5, 11), keep=keep)
+    assert sum(e > 0 for e in rep.errors) >= 3
+    for t in keep:
+        ref = O.run_full(prog, np.random.default_rng(trajectory_seed(7, t)), noise=("depolarizing", 0.05))
+        assert_parity(rep.kept[t], ref.state.amplitudes)
+        assert np.abs(rep.tables[t] - O.pmeasure(ref.state, (0, 5, 11))).max() <= 1e-12
+
+
+@pytest.mark.slow
+def test_trajectories_full_size_c5():
+    """BASELINE C5 shape (n=24, 4x6, 20 cycles, p=1e-3): a clean and two noisy
+    trajectories vs the oracle running the same explicit-Pauli programs (the
+    replay of the reference draw rule is pinned in test_program.py)."""
+    from paper_2008_07140_b200.trajectories import run_trajectories
+    from paper_2008_07140_b200.workloads import noisy_trajectory_program, trajectory_seed
+
+    prog = parse_program(workloads.rqc_text(4, 6, 20, seed=0))
+    probe = run_trajectories(prog, 1e-3, 24, base_seed=0, probe_qubits=(0, 23))
+    noisy = [t for t, e in zip(probe.trajectories, probe.errors) if e > 0]
+    clean = [t for t, e in zip(probe.trajectories, probe.errors) if e == 0]
+    check = clean[:1] + noisy[:2]
+    rep = run_trajectories(prog, 1e-3, max(check) + 1, base_seed=0, keep=tuple(check), probe_qubits=(0, 23))
+    for t in check:
+        traj = noisy_trajectory_program(prog, 1e-3, trajectory_seed(0, t))
+        ref = O.run_full(traj, workers=O.cpu_threads())
+        assert_parity(rep.kept[t], ref.state.amplitudes)
