@@ -127,6 +127,7 @@ int qsv_device_count(int *out);
 
 /* ---- state lifetime and data movement ---- */
 int qsv_create(int n_qubits, int device, void *stream, qsv_state **out);
+/* wraps caller-owned device memory (e.g. a torch tensor); its contents are left untouched */
 int qsv_create_on(int n_qubits, int device, void *stream, void *device_amplitudes, qsv_state **out);
 int qsv_destroy(qsv_state *st);
 int qsv_device_ptr(qsv_state *st, void **out);

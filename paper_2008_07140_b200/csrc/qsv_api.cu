@@ -335,7 +335,8 @@ static int create_impl(int n, int device, void *stream, void *mem, qsv_state **o
     }
     CUDA_TRY(cudaMalloc(&st->result, 32 * sizeof(double)));
     *out = st.release();
-    return qsv_set_basis(*out, 0);
+    // an owned buffer starts as |0...0> (init_state); wrapped caller memory keeps its contents
+    return mem ? QSV_OK : qsv_set_basis(*out, 0);
 }
 
 int qsv_create(int n_qubits, int device, void *stream, qsv_state **out) {

@@ -95,17 +95,22 @@ class CudaShard:
 
     def set_basis(self, index: int | None):
         """|index> restricted to this shard (None: all zeros)."""
-        self.N.check(self.N.lib().qsv_synchronize(self.h))
-        self.buf.zero_()
-        if index is not None:
-            self.buf[index] = 1.0
+        # torch work goes on the engine's stream, ordered with the libqsv kernels
+        with self.torch.cuda.stream(self.stream):
+            self.buf.zero_()
+            if index is not None:
+                self.buf[index] = 1.0
 
     def upload(self, host: np.ndarray):
-        self.buf.copy_(self.torch.from_numpy(np.ascontiguousarray(host)))
+        with self.torch.cuda.stream(self.stream):
+            self.buf.copy_(self.torch.from_numpy(np.ascontiguousarray(host)))
+        self.stream.synchronize()
 
     def download(self) -> np.ndarray:
         self.N.check(self.N.lib().qsv_synchronize(self.h))
-        return self.buf.cpu().numpy()
+        with self.torch.cuda.stream(self.stream):
+            out = self.buf.cpu().numpy()
+        return out
 
     def run(self, items, stats: dict | None = None):
         if not items:
@@ -153,6 +158,8 @@ class ShardedSimulator:
             raise ValueError(f"{n} qubits cannot be sharded over {self.world} ranks")
         self.n, self.g, self.n_local = n, g, n - g
         self.shard = shard
+        # gloo cannot exchange device tensors: stage the blocks through host memory
+        self.stage_host = dist.get_backend(group) == "gloo"
         self.perm = list(range(n))  # logical qubit -> physical position
         self.stats = ShardStats()
 
@@ -196,8 +203,14 @@ class ShardedSimulator:
         for r in range(self.world):
             splits.append(2 * chunk if (r & ~mask) == (self.rank & ~mask) else 0)
         t0 = time.perf_counter()
-        self.dist.all_to_all_single(recv, send, output_split_sizes=splits, input_split_sizes=splits,
-                                    group=self.group)
+        if self.stage_host and send.device.type != "cpu":
+            hs, hr = send.cpu(), send.new_empty(send.shape, device="cpu")
+            self.dist.all_to_all_single(hr, hs, output_split_sizes=splits, input_split_sizes=splits,
+                                        group=self.group)
+            recv.copy_(hr)
+        else:
+            self.dist.all_to_all_single(recv, send, output_split_sizes=splits, input_split_sizes=splits,
+                                        group=self.group)
         self.shard.commit_exchange()
         dt = time.perf_counter() - t0
         # physical positions G[i] <-> top[i] exchange their logical qubits
@@ -269,7 +282,7 @@ class ShardedSimulator:
         import torch
 
         v = torch.tensor([self.shard.norm_sq()], dtype=torch.float64,
-                         device=getattr(self.shard, "reduce_device", "cpu"))
+                         device="cpu" if self.stage_host else getattr(self.shard, "reduce_device", "cpu"))
         self.dist.all_reduce(v, group=self.group)
         return float(v.item())
 
@@ -279,7 +292,7 @@ class ShardedSimulator:
 
         # complex128 travels as float64 pairs (gloo/NCCL reductions are real)
         local = torch.from_numpy(self.shard.download().copy().view(np.float64))
-        dev = getattr(self.shard, "reduce_device", "cpu")
+        dev = "cpu" if self.stage_host else getattr(self.shard, "reduce_device", "cpu")
         local = local.to(dev)
         parts = [torch.empty_like(local) for _ in range(self.world)] if self.rank == 0 else None
         self.dist.gather(local, parts, dst=0, group=self.group)

@@ -224,3 +224,56 @@ def test_trajectories_full_size_c5():
         traj = noisy_trajectory_program(prog, 1e-3, trajectory_seed(0, t))
         ref = O.run_full(traj, workers=O.cpu_threads())
         assert_parity(rep.kept[t], ref.state.amplitudes)
+
+
+def _sharded_gpu_worker(rank, world, port, out):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_07140_b200.distributed import CudaShard, ShardedSimulator
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
+            prog = parse_program(text)
+            g = world.bit_length() - 1
+            sim = ShardedSimulator(prog.qubit_count, CudaShard(prog.qubit_count - g, 0))
+            sim.set_basis(1)
+            sim.run(prog)
+            amps = sim.gather_amplitudes()
+            if rank == 0:
+                res[name] = (amps, len(sim.stats.swaps))
+            sim.shard.close()
+        if rank == 0:
+            np.save(out, np.array([res], dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_path_on_gpu(world, tmp_path):
+    """CudaShard (libqsv on the GPU) + global<->local qubit swaps, P ranks sharing
+    the one GPU of this box; blocks are exchanged over gloo through host memory
+    (no kernel ever waits on another rank)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "sharded.npy")
+    mp.spawn(_sharded_gpu_worker, args=(world, port, out), nprocs=world, join=True)
+    res = np.load(out, allow_pickle=True)[0]
+    for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
+        prog = parse_program(text)
+        init = np.zeros(1 << prog.qubit_count, complex)
+        init[1] = 1
+        ref = O.run_full(prog, initial=init).state.amplitudes
+        amps, swaps = res[name]
+        assert swaps > 0
+        assert_parity(amps, ref)
