@@ -373,7 +373,7 @@ def run_gpu(args) -> None:
                    "reg_qubits": int(info.reg_qubits), "low_qubits": int(info.low_qubits),
                    "l2": "state (16 GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": int(launches + args.steps),  # pass kernels + set_basis per step
+        "gpu_launches": int(launches),  # fused pass kernels (|0..0> is synthesised by the first pass)
         "clocks": clocks,
     }
     L.qsv_plan_destroy(plan)

@@ -49,6 +49,10 @@ struct qsv_state {
     size_t work_bytes = 0;
     double *result = nullptr;  // 32 doubles
     unsigned *barrier = nullptr;  // grid-barrier counter of super-pass kernels
+    // lazily initialised basis state: qsv_set_basis records the index and the
+    // first fused pass synthesises |index> in shared memory instead of
+    // reading the (known) state; anything else materialises it first
+    int64_t pending_basis = -1;
     void *plan_buf = nullptr;  // scratch for one-shot plans
     size_t plan_buf_bytes = 0;
     int sm_count = 148;
@@ -74,6 +78,15 @@ int ensure_work(qsv_state *st, size_t bytes) {
     st->work_bytes = 0;
     CUDA_TRY(cudaMalloc(&st->work, bytes));
     st->work_bytes = bytes;
+    return QSV_OK;
+}
+
+int materialize(qsv_state *st) {
+    if (st->pending_basis < 0) return QSV_OK;
+    set_basis_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(),
+                                                                                      (uint64_t)st->pending_basis);
+    st->pending_basis = -1;
+    CUDA_TRY(cudaGetLastError());
     return QSV_OK;
 }
 
@@ -196,6 +209,10 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
             use_jit = false;  // auto mode: the interpreted pass kernel runs the same plan
         }
     }
+    if (!use_jit || jit_double_buffer()) {
+        const int rc = materialize(st);
+        if (rc) return rc;
+    }
     LaunchTimer tm;
     tm.on = profile;
     tm.s = st->stream;
@@ -204,7 +221,9 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
         const SuperPass &sp = P.supers[si];
         if (use_jit && use_supers(P) && P.jit_super_funcs[si]) {
             // all inner passes on L2-resident super-tiles: one HBM pass
-            int rc = ensure_barrier(st);
+            int rc = materialize(st);
+            if (rc) return rc;
+            rc = ensure_barrier(st);
             if (rc) return rc;
             std::string err;
             tm.begin();
@@ -220,8 +239,10 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
             int rc;
             if (use_jit) {
                 std::string err;
-                rc = jit_launch(P, i, st->amps, st->n, st->stream, err);
+                const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+                rc = jit_launch(P, i, st->amps, st->n, st->stream, err, basis);
                 if (rc) return fail(rc, err);
+                st->pending_basis = -1;
             } else {
                 rc = launch_pass(st, P, i, dp, ds, dop);
             }
@@ -244,6 +265,8 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
 }
 
 int launch_gate(qsv_state *st, const GateRec &g) {
+    const int mrc = materialize(st);
+    if (mrc) return mrc;
     GateArgs a;
     std::memset(&a, 0, sizeof(a));
     a.nt = g.nt;
@@ -275,7 +298,9 @@ int launch_gate(qsv_state *st, const GateRec &g) {
 }
 
 int reduce(qsv_state *st, int mode, int k, const void *other, double *out2) {
-    int rc = ensure_work(st, sizeof(double) * 2 * kReduceBlocks);
+    int rc = materialize(st);
+    if (rc) return rc;
+    rc = ensure_work(st, sizeof(double) * 2 * kReduceBlocks);
     if (rc) return rc;
     reduce_kernel<<<kReduceBlocks, kReduceThreads, 0, st->stream>>>(st->amps, (const double2 *)other, st->size(),
                                                                     mode, k, st->work);
@@ -335,8 +360,10 @@ static int create_impl(int n, int device, void *stream, void *mem, qsv_state **o
     }
     CUDA_TRY(cudaMalloc(&st->result, 32 * sizeof(double)));
     *out = st.release();
-    // an owned buffer starts as |0...0> (init_state); wrapped caller memory keeps its contents
-    return mem ? QSV_OK : qsv_set_basis(*out, 0);
+    // an owned buffer starts as |0...0> (init_state, lazily materialised);
+    // wrapped caller memory keeps its contents
+    if (!mem) (*out)->pending_basis = 0;
+    return QSV_OK;
 }
 
 int qsv_create(int n_qubits, int device, void *stream, qsv_state **out) {
@@ -364,21 +391,22 @@ int qsv_destroy(qsv_state *st) {
 
 int qsv_device_ptr(qsv_state *st, void **out) {
     *out = st->amps;
-    return QSV_OK;
+    const int rc = set_device(st->device);
+    return rc ? rc : materialize(st);
 }
 
 int qsv_set_basis(qsv_state *st, uint64_t index) {
     if (index >= st->size()) return fail(QSV_E_PARSE, "basis index out of range");
-    int rc = set_device(st->device);
-    if (rc) return rc;
-    set_basis_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), index);
-    CUDA_TRY(cudaGetLastError());
+    st->pending_basis = (int64_t)index;  // materialised lazily (see qsv_state)
     return QSV_OK;
 }
 
 int qsv_upload(qsv_state *st, const void *host, uint64_t offset, uint64_t count) {
     if (offset + count > st->size()) return fail(QSV_E_PARSE, "upload range out of bounds");
     int rc = set_device(st->device);
+    if (rc) return rc;
+    if (offset == 0 && count == st->size()) st->pending_basis = -1;  // fully overwritten
+    rc = materialize(st);
     if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(st->amps + offset, host, count * 16, cudaMemcpyHostToDevice, st->stream));
     CUDA_TRY(cudaStreamSynchronize(st->stream));
@@ -389,12 +417,16 @@ int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
     if (offset + count > st->size()) return fail(QSV_E_PARSE, "download range out of bounds");
     int rc = set_device(st->device);
     if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
     CUDA_TRY(cudaMemcpyAsync(host, st->amps + offset, count * 16, cudaMemcpyDeviceToHost, st->stream));
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QSV_OK;
 }
 
 int qsv_synchronize(qsv_state *st) {
+    const int rc = materialize(st);
+    if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QSV_OK;
 }
@@ -523,6 +555,8 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     if (rc) return fail(rc, msg);
     const bool fuse = !opt || opt->fuse;
     if (!fuse) {
+        rc = materialize(st);
+        if (rc) return rc;
         LaunchTimer tm;
         tm.on = opt && opt->profile;
         tm.s = st->stream;
@@ -649,6 +683,8 @@ int qsv_collapse(qsv_state *st, int k, int outcome, double scale) {
     if (k < 0 || k >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
     int rc = set_device(st->device);
     if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
     collapse_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), k,
                                                                                     outcome, scale);
     CUDA_TRY(cudaGetLastError());
@@ -657,6 +693,8 @@ int qsv_collapse(qsv_state *st, int k, int outcome, double scale) {
 
 int qsv_scale(qsv_state *st, double scale) {
     int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
     if (rc) return rc;
     collapse_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), -1, 0,
                                                                                     scale);
@@ -669,6 +707,8 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
     for (int p = 0; p < m; ++p)
         if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "pmeasure qubit out of range");
     int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
     if (rc) return rc;
     const size_t bins = (size_t)1 << m;
     int *d_q = nullptr;
@@ -701,6 +741,8 @@ int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *ou
         if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
     if (nq == 2 && qubits[0] == qubits[1]) return fail(QSV_E_PARSE, "repeated qubit");
     int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
     if (rc) return rc;
     const int D = 1 << nq, vals = 2 * D * D;
     const int blocks = kReduceBlocks;

@@ -121,6 +121,11 @@ __device__ __forceinline__ double2 ldcs2(const double2 *p) {
 __device__ __forceinline__ void stcs2(double2 *p, double2 v) {
     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+__device__ __forceinline__ double2 ldwb2(const double2 *p) {
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
 __device__ __forceinline__ void stwb2(double2 *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
@@ -177,16 +182,10 @@ inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
 
 }  // namespace
 
-// tile double buffering (cp.async prefetch of the next tile into a second
-// buffer).  Off by default: one buffer with two resident CTAs per SM measured
-// faster on B200 (occupancy hides the tile loads); QSV_JIT_DBUF=1 enables it.
-bool jit_double_buffer() {
-    static const bool on = [] {
-        const char *e = std::getenv("QSV_JIT_DBUF");
-        return e && std::atoi(e) != 0;
-    }();
-    return on;
-}
+// Tile double buffering (cp.async prefetch of the next tile into a second smem
+// buffer) was measured and dropped: the first stage now loads straight into
+// registers and occupancy (2 CTAs/SM) hides the load latency.
+bool jit_double_buffer() { return false; }
 
 namespace {
 
@@ -630,6 +629,7 @@ static inline unsigned swz(unsigned i) {
 static inline double2 ldcs2(const double2 *p) { return *p; }
 static inline void stcs2(double2 *p, double2 v) { *p = v; }
 static inline void stwb2(double2 *p, double2 v) { *p = v; }
+static inline double2 ldwb2(const double2 *p) { return *p; }
 static inline double2 cmulc(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -665,107 +665,94 @@ namespace {
 // Emits the processing of tiles for one pass: a (persistent, double-buffered
 // on the device) loop over `ntiles` tiles whose global base offset is
 // `base_of(t)`; the tile body is the pass's register stages.
+// Emits the processing of all tiles of one pass: a persistent loop over
+// `ntiles` tiles whose global base offset is `base_of(t)`.  The FIRST stage
+// loads its 2^R amplitudes straight from global memory into registers and the
+// LAST stage stores them straight back (a single-stage pass never touches
+// shared memory); only the re-layouts between stages go through the swizzled
+// shared-memory tile.  Returns the FP64 instructions emitted per thread per
+// tile (cost model).
 double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
-                    const std::function<std::string(const std::string &)> &base_of, bool stream_out = true) {
+                      const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
+                      bool basis_param = false) {
     double fp64 = 0;
     const DevPass &dp = P.passes[pi];
-    const int m = dp.m, R = P.r, T = 1 << (m - R);
+    const int m = dp.m, R = P.r;
     std::vector<int> tq(dp.tq, dp.tq + m);
-    std::vector<int> low(tq.begin(), tq.begin() + (m - R)), high(tq.begin() + (m - R), tq.end());
-    const std::string thread_loop = host ? "    for (unsigned tid = 0; tid < " + std::to_string(T) + "u; ++tid) {\n" : "";
+    const std::string thread_loop = host ? "    for (unsigned tid = 0; tid < " + std::to_string(1 << (m - R)) + "u; ++tid) {\n" : "";
     const std::string thread_end = host ? "    }\n" : "";
     const std::string barrier = host ? "" : "    __syncthreads();\n";
-    o << "  { // pass " << pi << "\n";
+    const int S = dp.stage_end - dp.stage_begin;
+    o << "  { // pass " << pi << ": " << S << " stage(s)\n";
     o << "  const u64 ntiles = " << ntiles << ";\n";
-    if (host) {
-        o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
-        o << "    const u64 base = " << base_of("t") << ";\n";
-        o << thread_loop;
-        o << "    const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
-        o << "    const unsigned tsl = swz(tid);\n";
-        o << "    double2 *p = psi + base + toff;\n";
-        for (int k = 0; k < (1 << R); ++k)
-            o << "    tile[tsl ^ " << swz_host((uint32_t)k * T) << "u] = ldcs2(p + " << deposit((uint64_t)k, high)
-              << "ull);\n";
-        o << thread_end;
-    } else {
-        // two tile buffers: cp.async streams tile t+grid into the spare buffer
-        // while tile t is computed
-        o << "  const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
-        o << "  const unsigned tsl = swz(tid);\n";
-        auto prefetch = [&](const std::string &tv, const std::string &buf_expr) {
-            o << "    { const double2 *g = psi + (" << base_of(tv) << ") + toff;\n";
-            o << "      const unsigned sb = sbase + ((" << buf_expr << ") << " << (m + 4) << ");\n";
-            for (int k = 0; k < (1 << R); ++k)
-                o << "      cp_async16(sb + 16u * (tsl ^ " << swz_host((uint32_t)k * T) << "u), g + "
-                  << deposit((uint64_t)k, high) << "ull);\n";
-            o << "    }\n";
-        };
-        if (jit_double_buffer()) {
-            o << "  u64 t = blockIdx.x;\n  unsigned buf = 0;\n";
-            o << "  if (t < ntiles) {\n";
-            prefetch("t", "0u");
-            o << "  }\n  cp_async_commit();\n";
-            o << "  for (; t < ntiles; t += gridDim.x) {\n";
-            o << "    double2 *tile = smem + (buf << " << m << ");\n";
-            o << "    cp_async_wait_all();\n    __syncthreads();\n";
-            o << "    { const u64 nt = t + gridDim.x;\n    if (nt < ntiles) {\n";
-            prefetch("nt", "buf ^ 1u");
-            o << "    }\n    cp_async_commit(); }\n";
-        } else {
-            // one buffer, more resident CTAs: latency hidden by occupancy
-            o << "  const unsigned buf = 0;\n";
-            o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
-            o << "    double2 *tile = smem;\n";
-            o << "    __syncthreads();\n";
-            prefetch("t", "0u");
-            o << "    cp_async_commit();\n    cp_async_wait_all();\n    __syncthreads();\n";
-        }
-        o << "    const u64 base = " << base_of("t") << ";\n";
-        o << "    double2 *p = psi + base + toff;\n";
-    }
+    if (host) o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
+    else o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
+    o << "    const u64 base = " << base_of("t") << ";\n";
     for (int s = dp.stage_begin; s < dp.stage_end; ++s) {
         const DevStage &st = P.stages[s];
+        const bool first = s == dp.stage_begin, last = s + 1 == dp.stage_end;
         StageGen g(o, R, tq);
         g.regq.resize(R);
         for (int k = 0; k < R; ++k) g.regq[k] = tq[st.rb[k]];
-        std::vector<int> nonreg;
+        std::vector<int> nonreg, nonreg_q;
         for (int j = 0; j < m; ++j)
-            if (!((st.reg_local_mask >> j) & 1)) nonreg.push_back(j);
+            if (!((st.reg_local_mask >> j) & 1)) {
+                nonreg.push_back(j);
+                nonreg_q.push_back(tq[j]);
+            }
         for (size_t j = 0; j < nonreg.size(); ++j) g.thread_bit[tq[nonreg[j]]] = (int)j;
+        // per register amplitude: smem slot (swizzled local index) and global offset
+        std::vector<uint32_t> c(1u << R);
+        std::vector<uint64_t> goff(1u << R);
+        for (int rho = 0; rho < (1 << R); ++rho) {
+            uint32_t off = 0;
+            uint64_t go = 0;
+            for (int k = 0; k < R; ++k)
+                if ((rho >> k) & 1) {
+                    off |= 1u << st.rb[k];
+                    go |= 1ull << tq[st.rb[k]];
+                }
+            c[rho] = swz_host(off);
+            goff[rho] = go;
+        }
         o << "    { // stage " << (s - dp.stage_begin) << " registers:";
         for (int k = 0; k < R; ++k) o << " q" << g.regq[k];
         o << "\n" << thread_loop;
-        o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n";
-        std::vector<uint32_t> c(1u << R);
-        for (int rho = 0; rho < (1 << R); ++rho) {
-            uint32_t off = 0;
-            for (int k = 0; k < R; ++k)
-                if ((rho >> k) & 1) off |= 1u << st.rb[k];
-            c[rho] = swz_host(off);
-            o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
+        if (!first || !last) o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n";
+        if (first || last) o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+        if (first) {
+            if (basis_param) {
+                // the state is |basis>: synthesise the registers instead of
+                // reading 2^n amplitudes that are known
+                o << "    const u64 gb = (u64)(gp - psi);\n";
+                for (int rho = 0; rho < (1 << R); ++rho)
+                    o << "    double2 v" << rho << " = basis != ~0ull ? make_double2(gb + " << goff[rho]
+                      << "ull == basis ? 1.0 : 0.0, 0.0) : ldcs2(gp + " << goff[rho] << "ull);\n";
+            } else {
+                for (int rho = 0; rho < (1 << R); ++rho)
+                    o << "    double2 v" << rho << " = " << (stream_out ? "ldcs2" : "ldwb2") << "(gp + " << goff[rho]
+                      << "ull);\n";
+            }
+        } else {
+            for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         }
         g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all();
         fp64 += g.fp64;
-        for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
-        o << thread_end << barrier << "    }\n";
+        if (last) {
+            // evict-first stores when the data leaves for HBM; write-back (L2
+            // resident) stores between the inner passes of a super-pass
+            for (int rho = 0; rho < (1 << R); ++rho)
+                o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gp + " << goff[rho] << "ull, v" << rho << ");\n";
+            o << thread_end << "    }\n";
+        } else {
+            // the previous tile's last stage may still read the shared tile
+            if (first) o << barrier;
+            for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
+            o << thread_end << barrier << "    }\n";
+        }
     }
-    o << thread_loop;
-    if (host) {
-        o << "    const u64 toff = " << deposit_expr("tid", low, true) << ";\n";
-        o << "    const unsigned tsl = swz(tid);\n";
-        o << "    double2 *p = psi + base + toff;\n";
-    }
-    for (int k = 0; k < (1 << R); ++k)
-        // evict-first stores when the data leaves for HBM; write-back (L2
-        // resident) stores between the inner passes of a super-pass
-        o << "    " << (stream_out ? "stcs2" : "stwb2") << "(p + " << deposit((uint64_t)k, high) << "ull, tile[tsl ^ "
-          << swz_host((uint32_t)k * T)
-          << "u]);\n";
-    o << thread_end;
-    if (!host && jit_double_buffer()) o << "    buf ^= 1u;\n";
     o << "  }\n  }\n";
     return fp64;
 }
@@ -785,8 +772,8 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
           << (mb ? std::atoi(mb) : std::max(1, 512 / T)) << ") "
           << name << "(" << params << ") {\n";
         o << "  extern __shared__ double2 smem[];\n";
+        o << "  double2 *tile = smem;\n";
         o << "  const unsigned tid = threadIdx.x;\n";
-        o << "  const unsigned sbase = (unsigned)__cvta_generic_to_shared(smem);\n";
     }
     return o.str();
 }
@@ -800,9 +787,11 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
     std::vector<int> ext;
     for (int q = 0; q < P.n; ++q)
         if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
-    o << kernel_head(P, dp.m, host, "qsv_pass", "double2 *__restrict__ psi, u64 n_tiles");
-    const double f = emit_tile_loop(o, P, pi, host, "n_tiles",
-                                    [&](const std::string &t) { return deposit_expr(t, ext, true); });
+    o << kernel_head(P, dp.m, host, "qsv_pass",
+                     host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis");
+    const double f = emit_tile_loop(
+        o, P, pi, host, "n_tiles", [&](const std::string &t) { return deposit_expr(t, ext, true); }, true,
+        !host && !jit_double_buffer());
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
     o << "}\n";
     return o.str();
@@ -1015,12 +1004,13 @@ static int cu_fail(CUresult r, const char *what, std::string &err) {
     return QSV_E_DEVICE;
 }
 
-int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err) {
+int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
+               unsigned long long basis) {
     const DevPass &dp = P.passes[pass];
     const int m = dp.m, T = 1 << (m - P.r);
     unsigned long long n_tiles = 1ull << (n - m);
     const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, (unsigned long long)P.jit_grids[pass]);
-    void *args[] = {&psi, &n_tiles};
+    void *args[] = {&psi, &n_tiles, &basis};
     const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, T, 1, 1,
                                              (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
                                              (CUstream)stream, args, nullptr);

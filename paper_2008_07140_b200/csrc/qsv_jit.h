@@ -53,8 +53,11 @@ bool jit_double_buffer();
 // true when the plan's super-passes run as L2-resident persistent kernels
 bool use_supers(const Plan &P);
 
-// Launches pass `pass` of a prepared plan over the whole state.
-int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err);
+// Launches pass `pass` of a prepared plan over the whole state.  `basis` !=
+// ~0 means the state is the basis state |basis> and is not read (single-buffer
+// kernels synthesise the tiles; see jit_basis_fusable).
+int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
+               unsigned long long basis = ~0ull);
 
 // Launches the persistent kernel of super-pass `si` (needs a 4-byte device
 // counter for the grid barrier).
