@@ -213,6 +213,23 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
         const int rc = materialize(st);
         if (rc) return rc;
     }
+    if (!use_jit && P.r > 4) {
+        // the interpreted kernel holds at most 16 amplitudes per thread:
+        // re-plan the same gates with 4 register qubits
+        Plan Q = build_plan(P.recs, P.n, P.m, 4, P.L, P.s);
+        void *buf = nullptr;
+        CUDA_TRY(cudaMalloc(&buf, plan_bytes(Q)));
+        DevPass *qp;
+        DevStage *qs;
+        DevOp *qo;
+        int rc = upload_plan(st, Q, buf, &qp, &qs, &qo);
+        qsv_options o2 = opt ? *opt : qsv_options{};
+        o2.jit = -1;
+        if (!rc) rc = execute_plan(st, Q, qp, qs, qo, &o2, stats);
+        cudaStreamSynchronize(st->stream);
+        cudaFree(buf);
+        return rc;
+    }
     LaunchTimer tm;
     tm.on = profile;
     tm.s = st->stream;

@@ -129,6 +129,9 @@ __device__ __forceinline__ double2 ldwb2(const double2 *p) {
 __device__ __forceinline__ void stwb2(double2 *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void *g, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async16(unsigned saddr, const void *g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
@@ -630,6 +633,7 @@ static inline double2 ldcs2(const double2 *p) { return *p; }
 static inline void stcs2(double2 *p, double2 v) { *p = v; }
 static inline void stwb2(double2 *p, double2 v) { *p = v; }
 static inline double2 ldwb2(const double2 *p) { return *p; }
+static inline void prefetch_l2(const void *, unsigned) {}
 static inline double2 cmulc(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -736,6 +740,16 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         } else {
             for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         }
+        if (first && stream_out && !host) {
+            // TMA bulk prefetch of this CTA's NEXT tile into L2 (contiguous runs
+            // of 2^lr amplitudes), so HBM streaming overlaps this tile's math
+            int lr = 0;
+            while (lr < m && tq[lr] == lr) ++lr;
+            std::vector<int> runq(tq.begin() + lr, tq.end());
+            o << "    { const u64 nt = t + gridDim.x;\n";
+            o << "      if (nt < ntiles && tid < " << (1u << (m - lr)) << "u) prefetch_l2(psi + (" << base_of("nt")
+              << ") + (" << deposit_expr("tid", runq, true) << "), " << (16u << lr) << "u); }\n";
+        }
         g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all();
@@ -765,11 +779,11 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
         o << "  static double2 tile[" << (1 << m) << "];\n";
     } else {
         o << kPrelude << kGridSync;
-        // 512 resident threads per SM by default (16 warps, <= 128 registers);
-        // QSV_JIT_MIN_BLOCKS overrides the CTAs-per-SM hint
+        // two resident CTAs per SM by default (one for 512-thread CTAs);
+        // QSV_JIT_MIN_BLOCKS overrides the hint
         const char *mb = std::getenv("QSV_JIT_MIN_BLOCKS");
         o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
-          << (mb ? std::atoi(mb) : std::max(1, 512 / T)) << ") "
+          << (mb ? std::atoi(mb) : (T >= 512 ? 1 : 2)) << ") "
           << name << "(" << params << ") {\n";
         o << "  extern __shared__ double2 smem[];\n";
         o << "  double2 *tile = smem;\n";

@@ -30,7 +30,10 @@ void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int 
     // FP64-bound RQC/QFT workloads (grid-barrier tails), see DESIGN.md
     s = (opt && opt->super_qubits > 0) ? opt->super_qubits : 0;
     m = (opt && opt->tile_qubits > 0) ? opt->tile_qubits : 12;
-    r = (opt && opt->reg_qubits > 0) ? opt->reg_qubits : 4;
+    // 32 amplitudes per thread for the specialised kernels (measured best on
+    // B200: fewer stages and barriers), 16 for the interpreted kernel
+    const bool jit = opt ? (opt->jit > 0 || (opt->jit == 0 && n >= 16)) : n >= 16;
+    r = (opt && opt->reg_qubits > 0) ? opt->reg_qubits : (jit ? 5 : 4);
     L = (opt && opt->low_qubits > 0) ? opt->low_qubits : 5;
     m = std::min(std::min(m, kMaxTileQubits), n);
     r = std::max(std::min(std::min(r, kMaxRegQubits), m), std::min(2, m));
@@ -427,6 +430,7 @@ void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int>
 // super-pass.
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s) {
     Plan P;
+    P.recs = recs;
     P.n = n;
     P.m = m;
     P.r = r;

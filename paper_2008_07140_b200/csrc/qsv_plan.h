@@ -27,7 +27,7 @@ namespace qsv {
 using cd = std::complex<double>;
 
 constexpr int kMaxTileQubits = 13;  // 2^13 * 16 B = 128 KiB shared memory
-constexpr int kMaxRegQubits = 4;    // 16 amplitudes (64 registers) per thread
+constexpr int kMaxRegQubits = 5;    // up to 32 amplitudes per thread (R = 5: specialised kernels only)
 constexpr int kLoTabBits = 6;       // local-index -> offset tables: 6 low bits ...
 constexpr int kHiTabBits = kMaxTileQubits - kLoTabBits;  // ... + 7 high bits
 
@@ -103,6 +103,7 @@ struct SuperPass {
 
 struct Plan {
     int n = 0, m = 0, r = 0, L = 0, s = 0;
+    std::vector<GateRec> recs;  // the gate records the plan was built from
     std::vector<SuperPass> supers;
     int64_t gates = 0;
     std::vector<DevPass> passes;
