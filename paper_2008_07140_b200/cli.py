@@ -27,12 +27,20 @@ from . import noise, program, rqc
 from .errors import SimulatorError
 
 
+# Probabilities below this print as "0".  The reference prints exact zeros as
+# "0" (cli.py:31-33); where it cancels exactly, FMA-contracted GPU arithmetic
+# leaves residues of ~1e-34, i.e. amplitudes ~1e-17 - far below the 1e-10
+# parity tolerance - so they are treated as zero when printed.
+ZERO_PRINT = 1e-24
+
+
 def format_pmeasure(table: np.ndarray, warn=None) -> str:
     m = (len(table) - 1).bit_length()
     total = float(table.sum())
     if warn is not None and abs(total - 1.0) > 1e-9:
         warn(f"probability table sums to {total!r}, expected 1")
-    return "\n".join(f"{format(i, f'0{m}b')}: {'0' if p == 0 else f'{p:.6g}'}" for i, p in enumerate(table))
+    return "\n".join(f"{format(i, f'0{m}b')}: {'0' if abs(p) < ZERO_PRINT else f'{p:.6g}'}"
+                     for i, p in enumerate(table))
 
 
 class _Log:
