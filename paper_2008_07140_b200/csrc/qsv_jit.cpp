@@ -691,7 +691,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     o << "  const u64 ntiles = " << ntiles << ";\n";
     if (host) o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
     else o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
-    o << "    const u64 base = " << base_of("t") << ";\n";
+    // QSV_JIT_DIAG_L2=1 (diagnostic only, wrong results): every CTA re-processes its
+    // first tile, so the kernel runs out of L2 and its time is compute + smem + barriers
+    static const bool diag_l2 = std::getenv("QSV_JIT_DIAG_L2") != nullptr;
+    o << "    const u64 base = " << (diag_l2 && !host ? base_of("(u64)blockIdx.x") : base_of("t")) << ";\n";
     for (int s = dp.stage_begin; s < dp.stage_end; ++s) {
         const DevStage &st = P.stages[s];
         const bool first = s == dp.stage_begin, last = s + 1 == dp.stage_end;

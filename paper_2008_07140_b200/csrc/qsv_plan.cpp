@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <bit>
+#include <cstdlib>
 #include <cstring>
 
 namespace qsv {
@@ -89,19 +90,31 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n, std::vector<GateRe
 
 namespace {
 
+// Rough FP64 work per amplitude of one gate in a specialised pass (cost
+// model for balancing passes): a non-diagonal 1-qubit gate is 2-4 FP64
+// operations per amplitude after coefficient absorption, a dense 2-qubit gate
+// ~8, diagonals are mostly absorbed.
+inline double gate_work(const GateRec &g) {
+    if (g.diag) return 0.25;
+    return g.nt == 1 ? 3.0 : 8.0;
+}
+
 struct Absorber {
     uint64_t resident = 0;  // qubits currently resident (tile or registers)
     int capacity = 0;
     uint64_t blockN = 0, blockD = 0;
+    double budget = 0, work = 0;  // optional cap on the summed gate_work (0: none)
 
     // true when gate g is taken
     bool offer(const GateRec &g) {
         const uint64_t touched = g.nmask | g.dmask;
         bool blocked = (touched & blockN) || (g.nmask & blockD);
+        if (!blocked && budget > 0 && work + gate_work(g) > budget) blocked = true;
         if (!blocked) {
             const uint64_t need = g.nmask & ~resident;
             if (popc(resident | need) <= capacity) {
                 resident |= need;
+                work += gate_work(g);
                 return true;
             }
         }
@@ -431,6 +444,7 @@ void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int>
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s) {
     Plan P;
     P.recs = recs;
+    if (const char *b = std::getenv("QSV_PASS_BUDGET")) P.pass_budget = std::atof(b);
     P.n = n;
     P.m = m;
     P.r = r;
@@ -461,6 +475,7 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, in
             Absorber tile;
             tile.resident = low;
             tile.capacity = m;
+            tile.budget = P.pass_budget;
             std::vector<int> taken, deferred;
             for (int gi : rem) (tile.offer(recs[gi]) ? taken : deferred).push_back(gi);
             emit_pass(P, recs, taken, tile.resident, smask);

@@ -104,6 +104,7 @@ struct SuperPass {
 struct Plan {
     int n = 0, m = 0, r = 0, L = 0, s = 0;
     std::vector<GateRec> recs;  // the gate records the plan was built from
+    double pass_budget = 0;     // cap on estimated FP64 work per pass (0: none)
     std::vector<SuperPass> supers;
     int64_t gates = 0;
     std::vector<DevPass> passes;
