@@ -140,6 +140,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+// sign flip of a double by an XOR mask on its sign bit: an integer op, keeps
+// the FP64 pipe free (a negation would otherwise issue a DADD)
+__device__ __forceinline__ double xsg(double x, u64 m) {
+    return __longlong_as_double(__double_as_longlong(x) ^ (long long)m);
+}
 )";
 
 std::string lit(double x) {
@@ -212,9 +217,64 @@ struct StageGen {
     // factor that depends on thread/tile bits, applied once per stage
     std::vector<int> acc;           // acc[2k+b]: accumulator in use
     bool accG = false;
+    // runtime sign flips (CZ-like diagonals on thread/tile qubits): each
+    // register amplitude carries a pending set of runtime sign variables
+    // (bit i <-> variable sg<id[i]>), applied to the sign bits with integer
+    // XORs only when the amplitude meets a differently signed partner in a
+    // gate, and at stage end
+    std::vector<uint64_t> psign;
+    std::vector<std::string> svar;  // condition of each live variable
+    std::vector<int> svar_id;       // its emitted name
+    std::map<uint64_t, std::string> smask;
+    int next_id = 0;
 
     StageGen(std::ostringstream &out, int r, const std::vector<int> &t)
-        : o(out), R(r), tq(t), pend(1u << r, cd(1, 0)), acc(2 * r, 0) {}
+        : o(out), R(r), tq(t), pend(1u << r, cd(1, 0)), acc(2 * r, 0), psign(1u << r, 0) {}
+
+    void apply_sign(int rho) {
+        apply_sign_set(rho, psign[rho]);
+        psign[rho] = 0;
+    }
+    void apply_sign_set(int rho, uint64_t set) {
+        if (!set) return;
+        auto it = smask.find(set);
+        if (it == smask.end()) {
+            std::string e;
+            for (int i = 0; i < 64; ++i)
+                if ((set >> i) & 1) e += (e.empty() ? "" : " ^ ") + std::string("sg") + std::to_string(svar_id[i]);
+            const std::string name = "sm" + std::to_string(next_id++);
+            o << "    const u64 " << name << " = " << e << ";\n";
+            it = smask.emplace(set, name).first;
+        }
+        const std::string v = "v" + std::to_string(rho);
+        o << "    " << v << " = make_double2(xsg(" << v << ".x, " << it->second << "), xsg(" << v << ".y, "
+          << it->second << "));\n";
+    }
+    void apply_signs() {
+        for (int r = 0; r < (1 << R); ++r) apply_sign(r);
+        svar.clear();
+        svar_id.clear();
+        smask.clear();
+    }
+    // a group of amplitudes entering one gate: a common sign commutes with it.
+    // Otherwise every member's sign is applied (keeping the most frequent set
+    // pending instead was measured to cost more flips later in the stage).
+    void signs_for_group(const std::vector<int> &grp) {
+        bool same = true;
+        for (int r : grp) same &= psign[r] == psign[grp[0]];
+        if (!same)
+            for (int r : grp) apply_sign(r);
+    }
+    int sign_var(const std::string &cond) {
+        for (size_t i = 0; i < svar.size(); ++i)
+            if (svar[i] == cond) return (int)i;
+        if (svar.size() == 64) apply_signs();
+        const int id = next_id++;
+        o << "    const u64 sg" << id << " = (u64)(" << cond << ") << 63;\n";
+        svar.push_back(cond);
+        svar_id.push_back(id);
+        return (int)svar.size() - 1;
+    }
 
     static std::string c2(cd c) { return "make_double2(" + lit(c.real()) + ", " + lit(c.imag()) + ")"; }
 
@@ -293,16 +353,23 @@ struct StageGen {
 
     void mul_const(int rho, cd c) {
         const std::string v = "v" + std::to_string(rho);
+        c = snap(c);
         const double cr = c.real(), ci = c.imag();
         if (cr == 1.0 && ci == 0.0) return;
-        fp64 += (ci == 0.0 || cr == 0.0) ? 2 : 4;
-        if (cr == -1.0 && ci == 0.0) {
-            o << "    " << v << " = make_double2(-" << v << ".x, -" << v << ".y);\n";
+        fp64 += flush_cost(c);
+        const char *neg = "0x8000000000000000ull";
+        if (std::fabs(cr) == 1.0 && std::fabs(ci) == 1.0) {
+            // (a + ib)(x + iy), a, b = +-1: two adds
+            auto sg = [](double k) { return k > 0 ? " + " : " - "; };
+            o << "    { const double2 t = " << v << "; " << v << " = make_double2(" << (cr > 0 ? "" : "-") << "t.x"
+              << sg(-ci) << "t.y, " << (cr > 0 ? "" : "-") << "t.y" << sg(ci) << "t.x); }\n";
+        } else if (cr == -1.0 && ci == 0.0) {
+            o << "    " << v << " = make_double2(xsg(" << v << ".x, " << neg << "), xsg(" << v << ".y, " << neg << "));\n";
         } else if (ci == 0.0) {
             o << "    " << v << " = make_double2(" << v << ".x * " << lit(cr) << ", " << v << ".y * " << lit(cr) << ");\n";
         } else if (cr == 0.0) {
-            if (ci == 1.0) o << "    " << v << " = make_double2(-" << v << ".y, " << v << ".x);\n";
-            else if (ci == -1.0) o << "    " << v << " = make_double2(" << v << ".y, -" << v << ".x);\n";
+            if (ci == 1.0) o << "    " << v << " = make_double2(xsg(" << v << ".y, " << neg << "), " << v << ".x);\n";
+            else if (ci == -1.0) o << "    " << v << " = make_double2(" << v << ".y, xsg(" << v << ".x, " << neg << "));\n";
             else
                 o << "    " << v << " = make_double2(-" << v << ".y * " << lit(ci) << ", " << v << ".x * " << lit(ci)
                   << ");\n";
@@ -318,9 +385,50 @@ struct StageGen {
             pend[rho] = cd(1, 0);
         }
     }
-    void flush_all() {
+    // FP64 cost of the stage-end multiply by c (after snap)
+    static int flush_cost(cd c) {
+        const double a = c.real(), b = c.imag();
+        if ((b == 0.0 && std::fabs(a) == 1.0) || (a == 0.0 && std::fabs(b) == 1.0)) return 0;  // sign bits only
+        if (a == 0.0 || b == 0.0 || (std::fabs(a) == 1.0 && std::fabs(b) == 1.0)) return 2;
+        return 4;
+    }
+    // Stage end.  Amplitudes stored between stages/passes are the true ones
+    // divided by a uniform real scale `sigma` that is carried forward, so
+    // when every pending factor of the stage has the same magnitude (H,
+    // RX/RY(pi/2), sqrt(X), T, CZ... all do) only its phase is multiplied in:
+    // +-1 / +-i then cost no FP64 at all and (+-1 +-i) two adds.  The final
+    // stage of the plan multiplies the scale back in.
+    void flush_all(double &sigma, bool final) {
         flush_runtime();
-        for (int r = 0; r < (1 << R); ++r) flush(r);
+        const int A = 1 << R;
+        double mu = 0;
+        if (!final) {
+            const double m0 = std::abs(pend[0]);
+            bool uniform = m0 > 0;
+            for (int r = 1; r < A && uniform; ++r) uniform = std::fabs(std::abs(pend[r]) - m0) <= kSnap * m0;
+            // keep the carried scale within +-2^200
+            const double next = std::fabs(std::log2(sigma * m0));
+            if (uniform && next < 200) {
+                int best = 1 << 30;
+                for (double cand : {m0, m0 * std::sqrt(0.5)}) {
+                    int c = 0;
+                    for (int r = 0; r < A; ++r) c += flush_cost(snap(pend[r] / cand));
+                    if (c < best) {
+                        best = c;
+                        mu = cand;
+                    }
+                }
+            }
+        }
+        if (final) {
+            for (int r = 0; r < A; ++r) pend[r] *= sigma;
+            sigma = 1.0;
+        } else if (mu > 0) {
+            for (int r = 0; r < A; ++r) pend[r] /= mu;
+            sigma *= mu;
+        }
+        for (int r = 0; r < A; ++r) flush(r);
+        apply_signs();
     }
 
     // complex linear map on register amplitudes idx[0..d) : out_r = sum_c M[r*d+c] in_c
@@ -377,18 +485,28 @@ struct StageGen {
         if (a == 0.0 || b == 0.0) return 2;
         return 4;
     }
-    // snap a coefficient to an exact unit / pure axis when it is within an ulp of it
+    // Canonicalise a coefficient that products of gate matrices left a few
+    // ulps off an exact form: a zero component, a unit, or equal |re| = |im|
+    // (the pi/4 phases of T-type gates).  kSnap (relative) is far below the
+    // 1e-10 parity tolerance and far above accumulated rounding.
+    static constexpr double kSnap = 1e-13;
     static cd snap(cd z) {
-        const double eps = 2.3e-16 * std::abs(z);
+        const double eps = kSnap * std::abs(z);
         double a = z.real(), b = z.imag();
         if (std::fabs(a) <= eps) a = 0.0;
         if (std::fabs(b) <= eps) b = 0.0;
         for (double u : {1.0, -1.0}) {
-            if (std::fabs(a - u) <= 2.3e-16 && b == 0.0) a = u;
-            if (std::fabs(b - u) <= 2.3e-16 && a == 0.0) b = u;
+            if (std::fabs(a - u) <= kSnap && b == 0.0) a = u;
+            if (std::fabs(b - u) <= kSnap && a == 0.0) b = u;
+        }
+        if (a != 0.0 && b != 0.0 && std::fabs(std::fabs(a) - std::fabs(b)) <= eps) {
+            const double h = 0.5 * (std::fabs(a) + std::fabs(b));
+            a = std::copysign(h, a);
+            b = std::copysign(h, b);
         }
         return cd(a, b);
     }
+    static bool diag_phase(cd z) { return z.real() != 0.0 && std::fabs(z.real()) == std::fabs(z.imag()); }
 
     // linear map that first absorbs the inputs' pending factors into the
     // compile-time coefficients, then factors one coefficient out of every
@@ -401,6 +519,7 @@ struct StageGen {
         std::vector<cd> Mp(d * d), Mn(d * d);
         for (int r = 0; r < d; ++r)
             for (int c = 0; c < d; ++c) Mp[r * d + c] = M[r * d + c] * pend[idx[c]];
+        if (d == 2 && pair_rotated(idx, Mp)) return;
         std::vector<cd> newp(d, cd(1, 0));
         for (int r = 0; r < d; ++r) {
             double mx = 0;
@@ -428,6 +547,47 @@ struct StageGen {
         }
         linear(idx, Mn.data());
         for (int r = 0; r < d; ++r) pend[idx[r]] = newp[r];
+    }
+
+    // A 2x2 block whose rows, each normalised on the same column k, read
+    // (1, c0) and (1, c1) with c0, c1 on one pi/4 diagonal (c_r = a_r (+-1 +-i),
+    // a_r real - always the case for a unitary block whose off-column phase is
+    // an odd multiple of pi/4): rotate the other input once, w = (+-1 +-i) x_o
+    // (two adds), then each row is x_k + a_r w (two FMAs): 6 FP64 per pair
+    // instead of 8.
+    bool pair_rotated(const std::vector<int> &idx, const std::vector<cd> &Mp) {
+        for (int k = 0; k < 2; ++k) {
+            const int oc = 1 - k;
+            if (std::abs(Mp[k]) == 0.0 || std::abs(Mp[2 + k]) == 0.0) continue;
+            if (std::abs(Mp[k]) < 0.5 * std::abs(Mp[oc]) || std::abs(Mp[2 + k]) < 0.5 * std::abs(Mp[2 + oc])) continue;
+            const cd c0 = snap(Mp[oc] / Mp[k]), c1 = snap(Mp[2 + oc] / Mp[2 + k]);
+            if (!diag_phase(c0) || !diag_phase(c1)) continue;
+            const cd u(c0.real() > 0 ? 1.0 : -1.0, c0.imag() > 0 ? 1.0 : -1.0);  // c0 = a0 u, a0 > 0
+            const double a0 = (c0 * std::conj(u)).real() / 2.0, a1 = (c1 * std::conj(u)).real() / 2.0;
+            if (std::fabs((c1 * std::conj(u)).imag()) > kSnap * std::abs(c1)) continue;  // c1 not along u
+            const std::string xo = "i" + std::to_string(oc), xk = "i" + std::to_string(k);
+            // w = u * x_o with u = (ur + i ui), ur, ui = +-1
+            auto sgn = [](double v) { return v > 0 ? " + " : " - "; };
+            o << "    { const double2 i0 = v" << idx[0] << "; const double2 i1 = v" << idx[1] << ";\n";
+            o << "      const double2 w = make_double2(" << (u.real() > 0 ? "" : "-") << xo << ".x" << sgn(-u.imag()) << xo
+              << ".y, " << (u.real() > 0 ? "" : "-") << xo << ".y" << sgn(u.imag()) << xo << ".x);\n";
+            for (int r = 0; r < 2; ++r) {
+                const double a = r == 0 ? a0 : a1;
+                auto term = [&](const char *comp) {
+                    const std::string wc = std::string("w.") + comp;
+                    if (a == 1.0) return xk + "." + comp + " + " + wc;
+                    if (a == -1.0) return xk + "." + comp + " - " + wc;
+                    return xk + "." + comp + " + " + wc + " * " + lit(a);
+                };
+                o << "      v" << idx[r] << " = make_double2(" << term("x") << ", " << term("y") << ");\n";
+            }
+            o << "    }\n";
+            fp64 += 6;
+            pend[idx[0]] = Mp[k];
+            pend[idx[1]] = Mp[2 + k];
+            return true;
+        }
+        return false;
     }
 
     std::string scalar_cond(uint64_t smask) const {
@@ -512,6 +672,7 @@ struct StageGen {
             }
             flush_acc(A);
             if (B >= 0) flush_acc(B);
+            for (auto &grp : groups) signs_for_group(grp);
             const std::string cond = scalar_cond(smask);
             if (cond.empty()) {
                 for (auto &grp : groups) linear_absorb(grp, g.m);
@@ -593,6 +754,13 @@ struct StageGen {
             std::string cond = ccond;
             for (int si = 0; si < ns; ++si)
                 cond += (cond.empty() ? "" : " && ") + std::string((combo >> si) & 1 ? "" : "!") + scalar_expr(sq[si]);
+            if (signs_only) {
+                // runtime sign: one more pending sign variable, no FP64
+                const int var = sign_var(cond);
+                for (int rho = 0; rho < (1 << R); ++rho)
+                    if (f[rho] == cd(-1, 0)) psign[rho] ^= 1ull << var;
+                continue;
+            }
             o << "    if (" << cond << ") {\n";
             for (int rho = 0; rho < (1 << R); ++rho) mul_const(rho, f[rho]);
             o << "    }\n";
@@ -637,6 +805,13 @@ static inline void prefetch_l2(const void *, unsigned) {}
 static inline double2 cmulc(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
+static inline double xsg(double x, u64 m) {
+    u64 b;
+    __builtin_memcpy(&b, &x, 8);
+    b ^= m;
+    __builtin_memcpy(&x, &b, 8);
+    return x;
+}
 )";
 
 // grid-wide barrier of the persistent super-pass kernel (all CTAs are
@@ -678,8 +853,10 @@ namespace {
 // tile (cost model).
 double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
                       const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
-                      bool basis_param = false) {
+                      bool basis_param = false, bool prefetch = true, double scale_in = 1.0,
+                      bool final_pass = true, double *scale_out = nullptr) {
     double fp64 = 0;
+    double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
     const int m = dp.m, R = P.r;
     std::vector<int> tq(dp.tq, dp.tq + m);
@@ -743,19 +920,20 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         } else {
             for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         }
-        if (first && stream_out && !host) {
+        if (first && stream_out && !host && prefetch) {
             // TMA bulk prefetch of this CTA's NEXT tile into L2 (contiguous runs
             // of 2^lr amplitudes), so HBM streaming overlaps this tile's math
             int lr = 0;
             while (lr < m && tq[lr] == lr) ++lr;
             std::vector<int> runq(tq.begin() + lr, tq.end());
             o << "    { const u64 nt = t + gridDim.x;\n";
-            o << "      if (nt < ntiles && tid < " << (1u << (m - lr)) << "u) prefetch_l2(psi + (" << base_of("nt")
+            o << "      if (nt < ntiles && " << (basis_param ? "basis == ~0ull && " : "") << "tid < " << (1u << (m - lr))
+              << "u) prefetch_l2(psi + (" << base_of("nt")
               << ") + (" << deposit_expr("tid", runq, true) << "), " << (16u << lr) << "u); }\n";
         }
         g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
-        g.flush_all();
+        g.flush_all(sigma, final_pass && last);
         fp64 += g.fp64;
         if (last) {
             // evict-first stores when the data leaves for HBM; write-back (L2
@@ -771,6 +949,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         }
     }
     o << "  }\n  }\n";
+    if (scale_out) *scale_out = sigma;
     return fp64;
 }
 
@@ -782,11 +961,13 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
         o << "  static double2 tile[" << (1 << m) << "];\n";
     } else {
         o << kPrelude << kGridSync;
-        // two resident CTAs per SM by default (one for 512-thread CTAs);
-        // QSV_JIT_MIN_BLOCKS overrides the hint
+        // two resident CTAs per SM by default; one when the CTA has 512
+        // threads or its tile takes more than half of the 228 KB of shared
+        // memory (a second CTA could not be resident, so capping registers
+        // for it would only cause spills).  QSV_JIT_MIN_BLOCKS overrides.
         const char *mb = std::getenv("QSV_JIT_MIN_BLOCKS");
-        o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
-          << (mb ? std::atoi(mb) : (T >= 512 ? 1 : 2)) << ") "
+        const bool one = T >= 512 || (16u << m) > (113u << 10);
+        o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (mb ? std::atoi(mb) : (one ? 1 : 2)) << ") "
           << name << "(" << params << ") {\n";
         o << "  extern __shared__ double2 smem[];\n";
         o << "  double2 *tile = smem;\n";
@@ -797,6 +978,25 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
 
 }  // namespace
 
+constexpr double kPrefetchMinFp64 = 55.0;
+
+// The uniform scale each pass's kernel finds the state stored with (chained
+// through dry runs of the generator: pass i's last stage decides pass i+1's).
+const std::vector<double> &pass_scales(const Plan &P) {
+    const size_t np = P.passes.size();
+    if (P.jit_scale_in.size() != np + 1) {
+        std::vector<double> sc(np + 1, 1.0);
+        for (size_t pi = 0; pi < np; ++pi) {
+            std::ostringstream dry;
+            emit_tile_loop(
+                dry, P, (int)pi, false, "n", [](const std::string &) { return std::string("0"); }, true, false, false,
+                sc[pi], pi + 1 == np, &sc[pi + 1]);
+        }
+        P.jit_scale_in = sc;
+    }
+    return P.jit_scale_in;
+}
+
 std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
     const DevPass &dp = P.passes[pi];
     std::ostringstream o;
@@ -806,9 +1006,23 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
         if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
     o << kernel_head(P, dp.m, host, "qsv_pass",
                      host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis");
-    const double f = emit_tile_loop(
-        o, P, pi, host, "n_tiles", [&](const std::string &t) { return deposit_expr(t, ext, true); }, true,
-        !host && !jit_double_buffer());
+    auto base_of = [&](const std::string &t) { return deposit_expr(t, ext, true); };
+    // L2 prefetch of the next tile pays only in compute-bound passes (measured
+    // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
+    // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
+    const double sc = pass_scales(P)[pi];
+    const bool final_pass = pi + 1 == (int)P.passes.size();
+    bool prefetch;
+    if (const char *e = std::getenv("QSV_JIT_PREFETCH")) {
+        prefetch = std::atoi(e) != 0;
+    } else {
+        std::ostringstream dry;
+        prefetch = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
+                       (double)(1 << P.r) >=
+                   kPrefetchMinFp64;
+    }
+    const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
+                                    sc, final_pass);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
     o << "}\n";
     return o.str();
@@ -852,7 +1066,7 @@ std::string jit_super_source(const Plan &P, int si, bool host) {
                     "((batch << " + std::to_string(lb) + ") + (" + t + " >> " + std::to_string(ib) + "))";
                 return "(" + deposit_expr(lowpart, inner, true) + ") | (" + deposit_expr(stile, outside, true) + ")";
             },
-            pi + 1 == sp.pass_end);
+            pi + 1 == sp.pass_end, false, false, pass_scales(P)[pi], pi + 1 == (int)P.passes.size());
         if (!host) o << "  grid_sync(bar, gen);\n";
     }
     o << "  }\n}\n";
@@ -994,6 +1208,8 @@ int jit_prepare(Plan &P, int device, std::string &err) {
             err = std::string("loading specialised kernel: ") + (s ? s : "zero occupancy");
             return QSV_E_DEVICE;
         }
+        // QSV_JIT_CTAS_PER_SM (diagnostic): cap the persistent grid's CTAs per SM
+        if (const char *c = std::getenv("QSV_JIT_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(c)));
         found[i] = CacheEntry{fn, per_sm * sms};
         g_cache[{device, u.src}] = found[i];
     }

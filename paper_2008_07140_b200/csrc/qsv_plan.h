@@ -123,6 +123,9 @@ struct Plan {
     std::vector<void *> jit_super_funcs;  // per super-pass (nullptr: run its inner passes flat)
     std::vector<int> jit_super_grids;
     std::vector<int> super_use;  // cost-model choice per super-pass (jit_choose_supers)
+    // deferred uniform scale carried into each pass by the specialised kernels
+    // (+ the plan's output, always 1); filled on first use by qsv_jit.cpp
+    mutable std::vector<double> jit_scale_in;
     int jit_device = -1;
 };
 
