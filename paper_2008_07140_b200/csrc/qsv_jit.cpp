@@ -899,12 +899,75 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             c[rho] = swz_host(off);
             goff[rho] = go;
         }
+        // Global memory is accessed straight from the registers of the first /
+        // last stage unless the stage holds qubit 0 in registers: a warp's lanes
+        // would then stride through memory in 16-byte pieces (measured: C2 pass
+        // with q0 q2 q4 in registers 8.5 -> 7.4 ms when staged; a stage holding
+        // only q1 loses from staging), so the tile goes through shared memory
+        // in the natural layout (thread tid <-> local indices tid + k*T).
+        int run = 0;
+        while (run < (int)nonreg.size() && nonreg[run] == run && tq[run] == run) ++run;
+        static const int stage_min = std::getenv("QSV_JIT_STAGE_MIN") ? std::atoi(std::getenv("QSV_JIT_STAGE_MIN")) : 1;
+        const bool staged_in = first && run < stage_min, staged_out = last && run < stage_min;
+        const int T = 1 << (m - R);
+        std::vector<int> lowq(tq.begin(), tq.begin() + (m - R));
+        std::vector<uint64_t> goffc(1u << R);
+        std::vector<uint32_t> cc(1u << R);
+        for (int k = 0; k < (1 << R); ++k) {
+            uint64_t go = 0;
+            for (int j = 0; j < R; ++j)
+                if ((k >> j) & 1) go |= 1ull << tq[m - R + j];
+            goffc[k] = go;
+            cc[k] = swz_host((uint32_t)k << (m - R));
+        }
         o << "    { // stage " << (s - dp.stage_begin) << " registers:";
         for (int k = 0; k < R; ++k) o << " q" << g.regq[k];
-        o << "\n" << thread_loop;
-        if (!first || !last) o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n";
-        if (first || last) o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
-        if (first) {
+        o << (staged_in || staged_out ? " (staged through shared memory)" : "") << "\n";
+        const bool staged_basis = staged_in && basis_param;  // device code only (host rendering has no basis)
+        if (staged_basis) {
+            // |basis>: synthesise the registers directly; otherwise stage the load
+            // (the branch is uniform: basis is a kernel argument)
+            o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n    double2";
+            for (int rho = 0; rho < (1 << R); ++rho) o << (rho ? ", v" : " v") << rho;
+            o << ";\n    if (basis != ~0ull) {\n";
+            o << "    const u64 gb = base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+            for (int rho = 0; rho < (1 << R); ++rho)
+                o << "    v" << rho << " = make_double2(gb + " << goff[rho] << "ull == basis ? 1.0 : 0.0, 0.0);\n";
+            o << "    } else {\n" << barrier << "    {\n";
+            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
+            for (int k = 0; k < (1 << R); ++k)
+                o << "    tile[tsc ^ " << cc[k] << "u] = " << (stream_out ? "ldcs2" : "ldwb2") << "(gpc + " << goffc[k]
+                  << "ull);\n";
+            o << "    }\n" << barrier;
+            for (int rho = 0; rho < (1 << R); ++rho) o << "    v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
+            o << "    }\n";
+            if (last && !staged_out) o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+        } else if (staged_in) {
+            // the previous tile's last stage may still read the shared tile
+            o << barrier << thread_loop << "    {\n";
+            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
+            if (basis_param) o << "    const u64 gb = (u64)(gpc - psi);\n";
+            for (int k = 0; k < (1 << R); ++k) {
+                o << "    tile[tsc ^ " << cc[k] << "u] = ";
+                if (basis_param)
+                    o << "basis != ~0ull ? make_double2(gb + " << goffc[k] << "ull == basis ? 1.0 : 0.0, 0.0) : ";
+                o << (stream_out ? "ldcs2" : "ldwb2") << "(gpc + " << goffc[k] << "ull);\n";
+            }
+            o << "    }\n" << thread_end << barrier;
+        }
+        if (!staged_basis) {
+        o << thread_loop;
+        if (!first || !last || staged_in || staged_out)
+            o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n";
+        if ((first && !staged_in) || (last && !staged_out))
+            o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+        }
+        if (staged_basis) {
+        } else if (staged_in) {
+            for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
+        } else if (first) {
             if (basis_param) {
                 // the state is |basis>: synthesise the registers instead of
                 // reading 2^n amplitudes that are known
@@ -935,7 +998,20 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all(sigma, final_pass && last);
         fp64 += g.fp64;
-        if (last) {
+        if (last && staged_out) {
+            // each thread overwrites only the slots it read this stage; a
+            // first stage read global memory, and the previous tile's last
+            // stage may still read the shared tile
+            if (first && !staged_in) o << barrier;
+            for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
+            o << thread_end << barrier << thread_loop << "    {\n";
+            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
+            for (int k = 0; k < (1 << R); ++k)
+                o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gpc + " << goffc[k] << "ull, tile[tsc ^ " << cc[k]
+                  << "u]);\n";
+            o << "    }\n" << thread_end << "    }\n";
+        } else if (last) {
             // evict-first stores when the data leaves for HBM; write-back (L2
             // resident) stores between the inner passes of a super-pass
             for (int rho = 0; rho < (1 << R); ++rho)
@@ -943,7 +1019,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             o << thread_end << "    }\n";
         } else {
             // the previous tile's last stage may still read the shared tile
-            if (first) o << barrier;
+            if (first && !staged_in) o << barrier;
             for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
             o << thread_end << barrier << "    }\n";
         }
