@@ -360,6 +360,66 @@ DevOp lower_op(const StageOp &o, int n, uint64_t tmask, const int32_t *regpos_of
 
 namespace {
 
+inline uint64_t padded_tile(uint64_t res, uint64_t pool, int n, int m) {
+    for (int q = 0; q < n && popc(res) < m; ++q)
+        if ((pool >> q) & 1) res |= 1ull << q;
+    return res;
+}
+
+inline bool conflict(const GateRec &a, const GateRec &b) {
+    return (a.nmask & (b.nmask | b.dmask)) || (b.nmask & (a.nmask | a.dmask));
+}
+
+// Greedy absorption front-loads the FP64 work: the first passes take every
+// gate they can and run compute-bound while the last ones are HBM-bound.  A
+// pass costs ~max(HBM time, FP64 time), so gates at the tail of a heavy pass
+// are pushed into the next pass when that lowers the summed cost: a gate may
+// move when its non-diagonal targets lie in the next pass's tile and no later
+// gate of its own pass depends on it; it becomes the first gate of the next
+// pass (everything there that conflicts with it was blocked behind it).  The
+// threshold (QSV_BALANCE_WORK, gate_work units) is the work at which a pass
+// turns compute-bound.  Opt-in: on C2 the receiving passes slowed down far more
+// than the FP64 model predicts (extra stages / runtime factors), net +2-5 ms.
+void balance_passes(const std::vector<GateRec> &recs, std::vector<std::vector<int>> &gates,
+                    const std::vector<uint64_t> &res, uint64_t pool, int n, int m) {
+    const char *env = std::getenv("QSV_BALANCE_WORK");
+    const double H = env ? std::atof(env) : 0.0;
+    if (H <= 0 || gates.size() < 2) return;
+    std::vector<double> w(gates.size(), 0.0);
+    for (size_t k = 0; k < gates.size(); ++k)
+        for (int gi : gates[k]) w[k] += gate_work(recs[gi]);
+    auto cost = [&](double a, double b) { return std::max(H, a) + std::max(H, b); };
+    for (int sweep = 0; sweep < 8; ++sweep) {
+        bool moved = false;
+        for (size_t k = gates.size() - 1; k-- > 0;) {
+            const uint64_t next_tile = padded_tile(res[k + 1], pool, n, m);
+            std::vector<int> &cur = gates[k];
+            std::vector<int> moving;  // program order is restored below
+            uint64_t later_n = 0, later_d = 0;  // qubits of the gates staying after position j
+            for (size_t j = cur.size(); j-- > 0;) {
+                const GateRec &g = recs[cur[j]];
+                const double gw = gate_work(g);
+                const bool free_of_later = !((g.nmask | g.dmask) & later_n) && !(g.nmask & later_d);
+                if (free_of_later && !(g.nmask & ~next_tile) && cost(w[k] - gw, w[k + 1] + gw) < cost(w[k], w[k + 1]) - 1e-9) {
+                    w[k] -= gw;
+                    w[k + 1] += gw;
+                    moving.push_back(cur[j]);
+                    cur.erase(cur.begin() + (long)j);
+                    moved = true;
+                } else {
+                    later_n |= g.nmask;
+                    later_d |= g.dmask;
+                }
+            }
+            if (!moving.empty()) {
+                std::reverse(moving.begin(), moving.end());
+                gates[k + 1].insert(gates[k + 1].begin(), moving.begin(), moving.end());
+            }
+        }
+        if (!moved) break;
+    }
+}
+
 // Emits one pass (tile + register stages) for `taken` (program order) into P.
 // The tile holds the forced low qubits plus the non-diagonal targets of
 // `taken`, padded with the lowest qubits of `pool` (the super-tile).
@@ -457,6 +517,34 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, in
     std::vector<int> remaining(recs.size());
     for (size_t i = 0; i < recs.size(); ++i) remaining[i] = (int)i;
 
+    if (P.s == m) {
+        // flat schedule (no L2 super-tiles): one pass per super-pass entry,
+        // balanced across the whole circuit
+        std::vector<std::vector<int>> pass_gates;
+        std::vector<uint64_t> pass_res;
+        while (!remaining.empty()) {
+            Absorber tile;
+            tile.resident = low;
+            tile.capacity = m;
+            tile.budget = P.pass_budget;
+            std::vector<int> taken, deferred;
+            for (int gi : remaining) (tile.offer(recs[gi]) ? taken : deferred).push_back(gi);
+            pass_gates.push_back(taken);
+            pass_res.push_back(tile.resident);
+            remaining.swap(deferred);
+        }
+        balance_passes(recs, pass_gates, pass_res, all, n, m);
+        for (size_t k = 0; k < pass_gates.size(); ++k) {
+            if (pass_gates[k].empty()) continue;
+            SuperPass spp;
+            spp.mask = padded_tile(pass_res[k], all, n, m);
+            spp.pass_begin = (int32_t)P.passes.size();
+            emit_pass(P, recs, pass_gates[k], pass_res[k], all);
+            spp.pass_end = (int32_t)P.passes.size();
+            P.supers.push_back(spp);
+        }
+    }
+
     while (!remaining.empty()) {
         Absorber sup;
         sup.resident = low;
@@ -471,6 +559,8 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, in
         spp.mask = smask;
         spp.pass_begin = (int32_t)P.passes.size();
         std::vector<int> rem = s_taken;
+        std::vector<std::vector<int>> pass_gates;
+        std::vector<uint64_t> pass_res;
         while (!rem.empty()) {
             Absorber tile;
             tile.resident = low;
@@ -478,9 +568,13 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, in
             tile.budget = P.pass_budget;
             std::vector<int> taken, deferred;
             for (int gi : rem) (tile.offer(recs[gi]) ? taken : deferred).push_back(gi);
-            emit_pass(P, recs, taken, tile.resident, smask);
+            pass_gates.push_back(taken);
+            pass_res.push_back(tile.resident);
             rem.swap(deferred);
         }
+        balance_passes(recs, pass_gates, pass_res, smask, n, m);
+        for (size_t k = 0; k < pass_gates.size(); ++k)
+            if (!pass_gates[k].empty()) emit_pass(P, recs, pass_gates[k], pass_res[k], smask);
         spp.pass_end = (int32_t)P.passes.size();
         P.supers.push_back(spp);
         remaining.swap(s_def);

@@ -122,3 +122,26 @@ def test_state_calls_fail_loudly_without_gpu():
 
     with pytest.raises(errors.DeviceError):
         init_state(3)
+
+
+@pytest.mark.parametrize("work", [6.0, 20.0])
+def test_plan_balanced_passes_keep_the_result(monkeypatch, work):
+    """Opt-in pass balancing (QSV_BALANCE_WORK) moves gates between passes; the
+    emulated plan must equal the unbalanced one (checked against the oracle
+    elsewhere), and gates must really have moved."""
+    n = 12
+    prog = parse_program(workloads.rqc_for_qubits(n, 10, 3))
+    recs = compile_gates(prog.gate_instructions())
+    psi0 = workloads.gaussian_state(n, 5)
+    cfg = dict(tile_qubits=7, reg_qubits=3, low_qubits=2)
+    monkeypatch.setenv("QSV_BALANCE_WORK", "0")
+    _, flat = build_plan(recs, n, **cfg)
+    monkeypatch.setenv("QSV_BALANCE_WORK", str(work))
+    _, bal = build_plan(recs, n, **cfg)
+    outs = []
+    for passes in (flat, bal):
+        psi = psi0.copy()
+        execute(passes, n, psi)
+        outs.append(psi)
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-12
+    assert [len(p["ops"]) for p in flat] != [len(p["ops"]) for p in bal]
