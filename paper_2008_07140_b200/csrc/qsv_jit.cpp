@@ -107,12 +107,6 @@ Driver &driver() {
 
 const char *kPrelude = R"(
 typedef unsigned long long u64;
-__device__ __forceinline__ unsigned swz(unsigned i) {
-    unsigned h = i >> 3;
-    h ^= h >> 3;
-    h ^= h >> 6;
-    return i ^ (h & 7u);
-}
 __device__ __forceinline__ double2 ldcs2(const double2 *p) {
     double2 r;
     asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
@@ -197,12 +191,74 @@ bool jit_double_buffer() { return false; }
 
 namespace {
 
-uint32_t swz_host(uint32_t i) {
-    uint32_t h = i >> 3;
-    h ^= h >> 3;
-    h ^= h >> 6;
-    return i ^ (h & 7u);
+// Shared-memory slot map of one pass: slot(e) = e ^ G(e), G linear from the
+// local bits >= 3 into the low 3 bits (16-byte slots, 8 per 128-byte bank
+// row).  A stage's 128-bit accesses are conflict-free when the three local
+// bits carried by lanes 0-2 of a warp map to independent bank bits; the map
+// is chosen per pass so that this holds for every stage's lane layout (the
+// fixed XOR fold i ^ (i>>3) ^ (i>>6) ^ (i>>9) fails whenever two of those
+// bits are congruent mod 3: 2-way conflicts, measured 271M on one C2 pass).
+struct SmemMap {
+    uint32_t g[32];
+    SmemMap() {
+        for (int j = 0; j < 32; ++j) g[j] = 1u << ((j + 3) % 3);
+    }
+    uint32_t vec(int p) const { return p < 3 ? (1u << p) : g[p - 3]; }
+    uint32_t map(uint32_t e) const {
+        uint32_t x = e;
+        for (int p = 3; p < 32; ++p)
+            if ((e >> p) & 1) x ^= g[p - 3];
+        return x;
+    }
+    // slot of the local index deposit(tid, bits) as a runtime expression
+    std::string tid_expr(const std::vector<int> &bits) const;
+};
+
+bool independent3(uint32_t a, uint32_t b, uint32_t c) {
+    return a && b && c && a != b && (a ^ b) != c && a != c && b != c;
 }
+
+// lane_sets: for each stage, the local bits carried by lanes 0, 1, 2
+SmemMap choose_smem_map(const std::vector<std::vector<int>> &lane_sets) {
+    SmemMap M;
+    std::vector<int> vars;  // high positions that appear in some lane set
+    for (const auto &ls : lane_sets)
+        for (int p : ls)
+            if (p >= 3 && std::find(vars.begin(), vars.end(), p) == vars.end()) vars.push_back(p);
+    auto ok_all = [&](size_t assigned) {
+        for (const auto &ls : lane_sets) {
+            if (ls.size() < 3) continue;
+            bool ready = true;
+            for (int p : ls)
+                if (p >= 3) ready &= std::find(vars.begin(), vars.begin() + (long)assigned, p) != vars.begin() + (long)assigned;
+            if (ready && !independent3(M.vec(ls[0]), M.vec(ls[1]), M.vec(ls[2]))) return false;
+        }
+        return true;
+    };
+    std::function<bool(size_t)> solve = [&](size_t k) -> bool {
+        if (k == vars.size()) return true;
+        const int j = vars[k] - 3;
+        const uint32_t def = 1u << (vars[k] % 3);
+        for (uint32_t t = 0; t < 8; ++t) {
+            M.g[j] = t == 0 ? def : (t == def ? 0 : t);  // the default first
+            if (M.g[j] && ok_all(k + 1) && solve(k + 1)) return true;
+        }
+        M.g[j] = def;
+        return false;
+    };
+    if (!solve(0)) return SmemMap();  // not found: default map (correct, may conflict)
+    return M;
+}
+
+std::string SmemMap::tid_expr(const std::vector<int> &bits) const {
+    std::string e = "(" + deposit_expr("tid", bits, false) + ")";
+    for (size_t k = 0; k < bits.size(); ++k) {
+        const uint32_t v = bits[k] >= 3 ? g[bits[k] - 3] : 0u;
+        if (v) e += " ^ (((tid >> " + std::to_string(k) + ") & 1u) * " + std::to_string(v) + "u)";
+    }
+    return e;
+}
+
 
 struct StageGen {
     std::ostringstream &o;
@@ -791,12 +847,6 @@ const char *kHostPrelude = R"(
 typedef unsigned long long u64;
 struct double2 { double x, y; };
 static inline double2 make_double2(double x, double y) { double2 r; r.x = x; r.y = y; return r; }
-static inline unsigned swz(unsigned i) {
-    unsigned h = i >> 3;
-    h ^= h >> 3;
-    h ^= h >> 6;
-    return i ^ (h & 7u);
-}
 static inline double2 ldcs2(const double2 *p) { return *p; }
 static inline void stcs2(double2 *p, double2 v) { *p = v; }
 static inline void stwb2(double2 *p, double2 v) { *p = v; }
@@ -872,6 +922,19 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     // first tile, so the kernel runs out of L2 and its time is compute + smem + barriers
     static const bool diag_l2 = std::getenv("QSV_JIT_DIAG_L2") != nullptr;
     o << "    const u64 base = " << (diag_l2 && !host ? base_of("(u64)blockIdx.x") : base_of("t")) << ";\n";
+    SmemMap smap;
+    {
+        std::vector<std::vector<int>> lane_sets;
+        for (int s = dp.stage_begin; s < dp.stage_end; ++s) {
+            std::vector<int> ls;
+            for (int j = 0; j < m && ls.size() < 3; ++j)
+                if (!((P.stages[s].reg_local_mask >> j) & 1)) ls.push_back(j);
+            lane_sets.push_back(ls);
+        }
+        smap = choose_smem_map(lane_sets);
+    }
+    std::vector<int> natural(m - R);
+    for (int j = 0; j < m - R; ++j) natural[j] = j;
     for (int s = dp.stage_begin; s < dp.stage_end; ++s) {
         const DevStage &st = P.stages[s];
         const bool first = s == dp.stage_begin, last = s + 1 == dp.stage_end;
@@ -896,7 +959,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
                     off |= 1u << st.rb[k];
                     go |= 1ull << tq[st.rb[k]];
                 }
-            c[rho] = swz_host(off);
+            c[rho] = smap.map(off);
             goff[rho] = go;
         }
         // Global memory is accessed straight from the registers of the first /
@@ -918,7 +981,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             for (int j = 0; j < R; ++j)
                 if ((k >> j) & 1) go |= 1ull << tq[m - R + j];
             goffc[k] = go;
-            cc[k] = swz_host((uint32_t)k << (m - R));
+            cc[k] = smap.map((uint32_t)k << (m - R));
         }
         o << "    { // stage " << (s - dp.stage_begin) << " registers:";
         for (int k = 0; k < R; ++k) o << " q" << g.regq[k];
@@ -927,14 +990,14 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         if (staged_basis) {
             // |basis>: synthesise the registers directly; otherwise stage the load
             // (the branch is uniform: basis is a kernel argument)
-            o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n    double2";
+            o << "    const unsigned tsw = " << smap.tid_expr(nonreg) << ";\n    double2";
             for (int rho = 0; rho < (1 << R); ++rho) o << (rho ? ", v" : " v") << rho;
             o << ";\n    if (basis != ~0ull) {\n";
             o << "    const u64 gb = base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
             for (int rho = 0; rho < (1 << R); ++rho)
                 o << "    v" << rho << " = make_double2(gb + " << goff[rho] << "ull == basis ? 1.0 : 0.0, 0.0);\n";
             o << "    } else {\n" << barrier << "    {\n";
-            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
             o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
             for (int k = 0; k < (1 << R); ++k)
                 o << "    tile[tsc ^ " << cc[k] << "u] = " << (stream_out ? "ldcs2" : "ldwb2") << "(gpc + " << goffc[k]
@@ -946,7 +1009,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         } else if (staged_in) {
             // the previous tile's last stage may still read the shared tile
             o << barrier << thread_loop << "    {\n";
-            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
             o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
             if (basis_param) o << "    const u64 gb = (u64)(gpc - psi);\n";
             for (int k = 0; k < (1 << R); ++k) {
@@ -960,7 +1023,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         if (!staged_basis) {
         o << thread_loop;
         if (!first || !last || staged_in || staged_out)
-            o << "    const unsigned tsw = swz(" << deposit_expr("tid", nonreg, false) << ");\n";
+            o << "    const unsigned tsw = " << smap.tid_expr(nonreg) << ";\n";
         if ((first && !staged_in) || (last && !staged_out))
             o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
         }
@@ -1005,7 +1068,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             if (first && !staged_in) o << barrier;
             for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
             o << thread_end << barrier << thread_loop << "    {\n";
-            o << "    const unsigned tsc = swz(tid);\n";
+            o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
             o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
             for (int k = 0; k < (1 << R); ++k)
                 o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gpc + " << goffc[k] << "ull, tile[tsc ^ " << cc[k]
