@@ -68,6 +68,7 @@ _SIGNATURES = {
     "qsv_set_basis": ([_P, C.c_uint64], C.c_int),
     "qsv_upload": ([_P, _P, C.c_uint64, C.c_uint64], C.c_int),
     "qsv_download": ([_P, _P, C.c_uint64, C.c_uint64], C.c_int),
+    "qsv_download_async": ([_P, _P, C.c_uint64, C.c_uint64], C.c_int),
     "qsv_synchronize": ([_P], C.c_int),
     "qsv_apply_gate": ([_P, _P], C.c_int),
     "qsv_run": ([_P, _P, C.c_int64, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),

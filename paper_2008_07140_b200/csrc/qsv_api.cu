@@ -438,7 +438,7 @@ int qsv_upload(qsv_state *st, const void *host, uint64_t offset, uint64_t count)
     return QSV_OK;
 }
 
-int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
+int qsv_download_async(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
     if (offset + count > st->size()) return fail(QSV_E_PARSE, "download range out of bounds");
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -450,6 +450,12 @@ int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
         CUDA_TRY(cudaMemcpyAsync((char *)host + done * 16, st->amps + offset + done, k * 16, cudaMemcpyDeviceToHost,
                                  st->stream));
     }
+    return QSV_OK;
+}
+
+int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
+    const int rc = qsv_download_async(st, host, offset, count);
+    if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QSV_OK;
 }
@@ -652,15 +658,20 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, opt ? opt->jit : 0,
                                                  st->device);
     Plan &P = cp->plan;
+    bool jit_ready = false;
     {
         // first use of a cached plan: specialise its kernels once
         const int jm = opt ? opt->jit : 0;
         if (jm > 0 || (jm == 0 && st->n >= kJitAutoQubits)) {
             std::lock_guard<std::mutex> lk(cp->mu);
             std::string err;
-            jit_prepare(P, st->device, err);  // failures are reported by execute_plan
+            jit_ready = jit_prepare(P, st->device, err) == QSV_OK;  // failures are reported by execute_plan
         }
     }
+    // the specialised kernels carry the whole plan in their code: the device
+    // op tables are only uploaded for the interpreted kernel (a pageable
+    // host->device copy would also stall the host behind the stream)
+    if (jit_ready) return execute_plan(st, P, nullptr, nullptr, nullptr, opt, stats);
     const size_t bytes = plan_bytes(P);
     if (st->plan_buf_bytes < bytes) {
         if (st->plan_buf) {

@@ -216,6 +216,7 @@ class RunResult:
     tables: list[tuple[tuple[int, ...], np.ndarray]] = field(default_factory=list)
     state: StateVector | None = None
     stats: dict = field(default_factory=dict)
+    amplitudes: np.ndarray | None = None  # host copy (run_batch)
 
 
 def _gate_triplet(inst):
@@ -333,3 +334,62 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
         apply_instruction(state, inst, None, rng, noise, result)
     _flush(state, batch, opts, result.stats)
     return result
+
+
+def run_batch(programs, outputs, *, device: int = 0, max_qubits: int = DEFAULT_MAX_QUBITS,
+              rng: np.random.Generator | None = None, states=None, **run_kw) -> list[RunResult]:
+    """Run several programs and bring every final state to host memory.
+
+    The reference equivalent is a loop of `run_full(program)` followed by
+    reading `result.state.amplitudes` (statevector.py:397-430).  Here two
+    device states alternate, each on its own stream: program i's device->host
+    copy (PCIe, ~5x longer than simulating C2) overlaps program i+1's fused
+    passes.  `outputs[i]` must be a pinned, C-contiguous complex128 host array
+    of 2^n amplitudes (e.g. ``torch.empty(2**n, dtype=torch.complex128,
+    pin_memory=True).numpy()``); it is complete when this function returns.
+    Programs may be given as text (parsed in turn).  A buffer may be repeated
+    every second program (its earlier result is then overwritten, in order).
+    All programs must have the same qubit count.  The returned results carry
+    `amplitudes` (= outputs[i]) instead of a device `state`.  Extra keywords
+    go to `run_full`; `states` optionally supplies the two device states
+    (kept open; otherwise they are created and freed here).
+    """
+    from .program import parse_program
+
+    programs = list(programs)
+    if not programs:
+        return []
+    if len(outputs) != len(programs):
+        raise ValueError("one output buffer per program")
+    # program texts are parsed as their turn comes (host work that overlaps the
+    # previous download)
+    first = programs[0] if not isinstance(programs[0], str) else parse_program(programs[0])
+    n = first.qubit_count
+
+    for out in outputs:
+        if out.dtype != np.complex128 or not out.flags.c_contiguous or out.size != 1 << n:
+            raise ValueError("outputs must be C-contiguous complex128 arrays of 2^n amplitudes")
+    own = states is None
+    if own:
+        states = [init_state(n, max_qubits=max_qubits, device=device) for _ in range(min(2, len(programs)))]
+    results = []
+    try:
+        for i, (prog, out) in enumerate(zip(programs, outputs)):
+            if isinstance(prog, str):
+                prog = first if i == 0 else parse_program(prog)
+            if prog.qubit_count != n:
+                raise ValueError("run_batch needs programs of one qubit count")
+            st = states[i % len(states)]
+            # the state's stream orders this run after its previous download
+            res = run_full(prog, rng, state=st, max_qubits=max_qubits, **run_kw)
+            N.check(N.lib().qsv_download_async(st.handle, out.ctypes.data, 0, out.size))
+            res.state = None
+            res.amplitudes = out
+            results.append(res)
+        for st in states:
+            st.synchronize()
+    finally:
+        if own:
+            for st in states:
+                st.close()
+    return results

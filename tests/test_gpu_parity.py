@@ -119,6 +119,25 @@ def test_rqc_vs_oracle_larger(n, depth, seed):
         res.state.close()
 
 
+def test_run_batch_overlapped_downloads():
+    """run_batch (two device states, downloads overlapping the next run) returns
+    the same amplitudes as run_full for each program, incl. a reused buffer."""
+    import torch
+
+    n = 18
+    texts = [workloads.rqc_for_qubits(n, 10, s) for s in (1, 2, 3)]
+    bufs = [torch.empty(1 << n, dtype=torch.complex128, pin_memory=True).numpy() for _ in range(2)]
+    outs = [bufs[0], bufs[1], bufs[0]]
+    res = SV.run_batch(texts, outs)
+    assert all(r.amplitudes is outs[i] and r.state is None for i, r in enumerate(res))
+    # buffers 0 and 1 hold programs 2 and 1 (program 0's result was overwritten in order)
+    for i, buf in ((1, bufs[1]), (2, bufs[0])):
+        ref = O.run_full(parse_program(texts[i]), workers=O.cpu_threads())
+        assert_parity(buf, ref.state.amplitudes)
+    with pytest.raises(ValueError):
+        SV.run_batch(texts[:1], [np.zeros(4, np.complex128)])
+
+
 def test_qft_round_trip_22():
     n = 22
     psi0 = workloads.gaussian_state(n, 11)
