@@ -1092,7 +1092,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     return fp64;
 }
 
-std::string kernel_head(const Plan &P, int m, bool host, const char *name, const char *params) {
+constexpr double kThreeCtaMinFp64 = 60.0;
+
+std::string kernel_head(const Plan &P, int m, bool host, const char *name, const char *params,
+                        double fp64_per_amp = 0) {
     std::ostringstream o;
     const int T = 1 << (m - P.r);
     if (host) {
@@ -1100,13 +1103,18 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
         o << "  static double2 tile[" << (1 << m) << "];\n";
     } else {
         o << kPrelude << kGridSync;
-        // two resident CTAs per SM by default; one when the CTA has 512
+        // Resident CTAs per SM: two by default; one when the CTA has 512
         // threads or its tile takes more than half of the 228 KB of shared
-        // memory (a second CTA could not be resident, so capping registers
-        // for it would only cause spills).  QSV_JIT_MIN_BLOCKS overrides.
+        // memory (capping registers for a CTA that cannot be resident only
+        // spills); three for compute-bound passes of 128-thread CTAs with
+        // tiles <= 64 KB (registers capped at 168: a few bytes of spill, 12
+        // warps/SM; measured on C2: passes >= ~60 FP64/amp gain 5-7 %, lighter
+        // passes lose up to 20 %).  QSV_JIT_MIN_BLOCKS overrides.
         const char *mb = std::getenv("QSV_JIT_MIN_BLOCKS");
         const bool one = T >= 512 || (16u << m) > (113u << 10);
-        o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (mb ? std::atoi(mb) : (one ? 1 : 2)) << ") "
+        const bool three = !one && T <= 128 && (16u << m) <= (64u << 10) && fp64_per_amp >= kThreeCtaMinFp64;
+        o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
+          << (mb ? std::atoi(mb) : (one ? 1 : three ? 3 : 2)) << ") "
           << name << "(" << params << ") {\n";
         o << "  extern __shared__ double2 smem[];\n";
         o << "  double2 *tile = smem;\n";
@@ -1143,23 +1151,24 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
     std::vector<int> ext;
     for (int q = 0; q < P.n; ++q)
         if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
-    o << kernel_head(P, dp.m, host, "qsv_pass",
-                     host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis");
     auto base_of = [&](const std::string &t) { return deposit_expr(t, ext, true); };
+    const double sc = pass_scales(P)[pi];
+    const bool final_pass = pi + 1 == (int)P.passes.size();
+    // FP64 work per amplitude (dry run) decides the compute-bound tuning
+    double cost;
+    {
+        std::ostringstream dry;
+        cost = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
+               (double)(1 << P.r);
+    }
+    o << kernel_head(P, dp.m, host, "qsv_pass",
+                     host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis",
+                     cost);
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
-    const double sc = pass_scales(P)[pi];
-    const bool final_pass = pi + 1 == (int)P.passes.size();
-    bool prefetch;
-    if (const char *e = std::getenv("QSV_JIT_PREFETCH")) {
-        prefetch = std::atoi(e) != 0;
-    } else {
-        std::ostringstream dry;
-        prefetch = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
-                       (double)(1 << P.r) >=
-                   kPrefetchMinFp64;
-    }
+    const char *e = std::getenv("QSV_JIT_PREFETCH");
+    const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
                                     sc, final_pass);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
