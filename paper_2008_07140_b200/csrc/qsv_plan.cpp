@@ -550,6 +550,74 @@ void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int>
 
 }  // namespace
 
+namespace {
+
+bool is_plain_swap(const GateRec &g) {
+    if (g.nt != 2 || g.cmask) return false;
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const bool one = (a == 0 && b == 0) || (a == 3 && b == 3) || (a == 1 && b == 2) || (a == 2 && b == 1);
+            if (g.u[a * 4 + b] != cd(one ? 1.0 : 0.0, 0.0)) return false;
+        }
+    return true;
+}
+
+GateRec swap_rec(int a, int b) {
+    GateRec g;
+    g.nt = 2;
+    g.t[0] = a;
+    g.t[1] = b;
+    for (int k = 0; k < 16; ++k) g.u[k] = 0;
+    g.u[0] = g.u[6] = g.u[9] = g.u[15] = 1;
+    g.nmask = (1ull << a) | (1ull << b);
+    return g;
+}
+
+}  // namespace
+
+// SWAP gates (uncontrolled) move no data here: they permute the map from
+// logical to physical qubits and every later gate is renamed through it
+// (QFT's bit-reversal SWAP layers, C4, disappear entirely: the forward and
+// the inverse layer cancel).  If the final map is not the identity, explicit
+// SWAPs on physical qubits restore the order at the end.
+std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &in, int n) {
+    bool any = false;
+    for (const GateRec &g : in) any |= is_plain_swap(g);
+    if (!any || (std::getenv("QSV_RELABEL_SWAPS") && std::atoi(std::getenv("QSV_RELABEL_SWAPS")) == 0)) return in;
+    std::vector<int> phys(n);  // logical -> physical
+    for (int q = 0; q < n; ++q) phys[q] = q;
+    auto remap = [&](uint64_t mask) {
+        uint64_t out = 0;
+        for (int q = 0; q < n; ++q)
+            if ((mask >> q) & 1) out |= 1ull << phys[q];
+        return out;
+    };
+    std::vector<GateRec> out;
+    out.reserve(in.size());
+    for (const GateRec &g : in) {
+        if (is_plain_swap(g)) {
+            std::swap(phys[g.t[0]], phys[g.t[1]]);
+            continue;
+        }
+        GateRec h = g;
+        for (int k = 0; k < g.nt; ++k) h.t[k] = phys[g.t[k]];
+        h.cmask = remap(g.cmask);
+        h.nmask = remap(g.nmask);
+        h.dmask = remap(g.dmask);
+        out.push_back(h);
+    }
+    // restore: logical a back to physical a
+    for (int a = 0; a < n; ++a) {
+        if (phys[a] == a) continue;
+        int b = 0;
+        while (phys[b] != a) ++b;  // logical b currently sits on physical a
+        out.push_back(swap_rec(phys[a], a));
+        phys[b] = phys[a];
+        phys[a] = a;
+    }
+    return out;
+}
+
 // Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy
 // absorption with capacity s); its gates are then split into ordinary passes
 // whose tiles lie inside S.  The executor runs all inner passes of a
@@ -558,16 +626,17 @@ void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int>
 // per super-pass while the inner passes stream through L2.  s >= n keeps the
 // whole state in one super-tile; s == m degenerates to one pass per
 // super-pass.
-Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s) {
+Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L, int s) {
     Plan P;
-    P.recs = recs;
+    P.recs = recs_in;
     if (const char *b = std::getenv("QSV_PASS_BUDGET")) P.pass_budget = std::atof(b);
     P.n = n;
     P.m = m;
     P.r = r;
     P.L = L;
     P.s = std::max(m, std::min(s, n));
-    P.gates = (int64_t)recs.size();
+    P.gates = (int64_t)recs_in.size();
+    const std::vector<GateRec> recs = relabel_swaps(recs_in, n);
     const uint64_t low = L > 0 ? ((1ull << L) - 1) : 0;
     const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
 

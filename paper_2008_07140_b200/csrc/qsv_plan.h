@@ -136,6 +136,9 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector
 // Builds the fused schedule.  m, r, L already clamped to the state size.
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s);
 
+// SWAP gates folded into a logical->physical qubit map (see qsv_plan.cpp).
+std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &recs, int n);
+
 void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int &s);
 
 }  // namespace qsv

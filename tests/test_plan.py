@@ -145,3 +145,40 @@ def test_plan_balanced_passes_keep_the_result(monkeypatch, work):
         outs.append(psi)
     assert np.abs(outs[0] - outs[1]).max() <= 1e-12
     assert [len(p["ops"]) for p in flat] != [len(p["ops"]) for p in bal]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_plan_swaps_relabel_qubits(seed):
+    """Uncontrolled SWAPs become a qubit relabelling (no data movement) with
+    restoring SWAPs at the end; controlled SWAPs stay gates."""
+    rng = np.random.default_rng(seed)
+    n = 9
+    swap = np.eye(4)[[0, 2, 1, 3]]
+    items = []
+    for _ in range(80):
+        qs = [int(q) for q in rng.permutation(n)]
+        k = rng.integers(0, 4)
+        if k == 0:
+            items.append((swap, (qs[0], qs[1]), ()))
+        elif k == 1:
+            items.append((swap, (qs[0], qs[1]), (qs[2],)))
+        elif k == 2:
+            z = rng.standard_normal((2, 2)) + 1j * rng.standard_normal((2, 2))
+            q2, _ = np.linalg.qr(z)
+            items.append((q2, (qs[0],), tuple(qs[1:1 + int(rng.integers(0, 2))])))
+        else:
+            items.append((np.diag(np.exp(1j * rng.uniform(0, 6, 4))), (qs[0], qs[1]), ()))
+    recs = N.gate_records(items)
+    psi0 = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
+    ref = O.OracleState(n, psi0.copy(), 0)
+    for u, t, c in items:
+        O.apply_gate(ref, u, t, c)
+    for cfg in CONFIGS:
+        info, passes = build_plan(recs, n, **cfg)
+        psi = psi0.copy()
+        execute(passes, n, psi)
+        assert np.abs(psi - ref.amplitudes).max() <= 1e-12, cfg
+    # QFT round trip: the forward and inverse SWAP layers cancel, no SWAP op remains
+    prog = parse_program(workloads.qft_text(12, round_trip=True))
+    _, passes = build_plan(compile_gates(prog.gate_instructions()), 12, tile_qubits=8, reg_qubits=4, low_qubits=3)
+    assert not any(o["kind"] == 2 and np.allclose(o["m"][:16].reshape(4, 4), swap) for p in passes for o in p["ops"])
