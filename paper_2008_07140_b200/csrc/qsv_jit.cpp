@@ -6,6 +6,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cctype>
 #include <atomic>
 #include <cinttypes>
 #include <cmath>
@@ -1221,6 +1222,20 @@ std::string jit_super_source(const Plan &P, int si, bool host) {
     return o.str();
 }
 
+// spill stores reported by ptxas -v in an NVRTC log ("N bytes spill stores")
+size_t spill_bytes(const std::string &log) {
+    size_t total = 0;
+    for (size_t at = log.find("bytes spill stores"); at != std::string::npos; at = log.find("bytes spill stores", at + 1)) {
+        size_t b = at;
+        while (b > 0 && log[b - 1] == ' ') --b;
+        size_t e = b;
+        while (b > 0 && std::isdigit((unsigned char)log[b - 1])) --b;
+        if (b < e) total += std::stoul(log.substr(b, e - b));
+    }
+    return total;
+}
+constexpr size_t kMaxSpillBytes = 128;
+
 std::string jit_compile_cubin(const std::string &src, std::string &log) {
     Nvrtc &api = nvrtc();
     if (!api.ok) {
@@ -1232,8 +1247,9 @@ std::string jit_compile_cubin(const std::string &src, std::string &log) {
         log = "nvrtcCreateProgram failed";
         return {};
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--extra-device-vectorization"};
-    const nvrtcResult rc = api.CompileProgram(prog, 5, opts);
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--extra-device-vectorization",
+                          "--ptxas-options=-v", "-diag-suppress=177"};
+    const nvrtcResult rc = api.CompileProgram(prog, 7, opts);
     size_t ls = 0;
     api.GetProgramLogSize(prog, &ls);
     log.assign(ls, '\0');
@@ -1328,6 +1344,18 @@ int jit_prepare(Plan &P, int device, std::string &err) {
                 for (size_t k; (k = next.fetch_add(1)) < todo.size();) {
                     Unit &u = units[todo[k]];
                     u.cubin = jit_compile_cubin(u.src, u.log);
+                    // a three-CTA register cap that spills (accumulator-heavy
+                    // passes, e.g. QFT: 1.2 KB of local memory, +20 % time) is
+                    // recompiled for two CTAs per SM (cache key stays u.src)
+                    const std::string three = "__launch_bounds__(128, 3)";
+                    const size_t at = u.src.find(three);
+                    if (!u.cubin.empty() && at != std::string::npos && spill_bytes(u.log) > kMaxSpillBytes) {
+                        std::string src2 = u.src;
+                        src2.replace(at, three.size(), "__launch_bounds__(128, 2)");
+                        std::string log2;
+                        std::string cubin2 = jit_compile_cubin(src2, log2);
+                        if (!cubin2.empty()) u.cubin.swap(cubin2);
+                    }
                 }
             });
         for (auto &th : pool) th.join();
