@@ -165,8 +165,28 @@ int qsv_plan_super_source(const qsv_plan *plan, int64_t super_pass, int host, ch
                           int64_t *needed);
 /* FP64 instructions per amplitude the specialised kernel of one pass executes (cost model) */
 int qsv_plan_pass_cost(const qsv_plan *plan, int64_t pass, double *fp64_per_amp);
+/* distributed layout (sharded state, n_local of n_qubits qubits local per rank): cut the stream
+ * into SEGMENTS that each run with one fixed set of n_local local logical qubits; between
+ * segments the leaving/entering qubits are exchanged (global<->local qubit swap).
+ * gate_segment[n_gates] receives the segment of every gate, segment_local[n_gates] the local
+ * qubit mask of every segment, *n_segments their number.  initial_local = current local set;
+ * free_initial=1 lets the first segment pick its own (basis-state input).  No reference
+ * counterpart (the reference has no distributed mode). */
+int qsv_plan_segments(const qsv_gate *gates, int64_t n_gates, int n_qubits, int n_local, uint64_t initial_local,
+                      int free_initial, int32_t *gate_segment, uint64_t *segment_local, int64_t *n_segments);
 /* compile CUDA source for sm_100a with NVRTC (no GPU needed); *cubin_bytes = image size */
 int qsv_jit_compile(const char *src, int64_t *cubin_bytes);
+
+/* ---- peer exchange for the sharded layout (one process per GPU, NVLink copy engines) ----
+ * No reference counterpart (the reference is single-node).  The global<->local
+ * qubit swap of distributed.py pushes contiguous blocks into the peers' receive buffers. */
+/* CUDA IPC handle (64 bytes) of the allocation holding device_ptr, and device_ptr's byte offset in it */
+int qsv_ipc_mem_handle(void *device_ptr, void *handle64, uint64_t *offset);
+/* maps a peer allocation into this process on `device`; *out = base + offset */
+int qsv_ipc_mem_open(const void *handle64, uint64_t offset, int device, void **out);
+int qsv_ipc_mem_close(void *mapped);
+/* asynchronous copy between any two device pointers (UVA; peer pointers go over NVLink) */
+int qsv_copy_async(void *dst, const void *src, uint64_t bytes, void *stream);
 
 /* ---- readout (synchronous) ---- */
 int qsv_norm_sq(qsv_state *st, double *out);

@@ -90,6 +90,12 @@ _SIGNATURES = {
     "qsv_plan_super_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_plan_pass_cost": ([_P, C.c_int64, C.POINTER(C.c_double)], C.c_int),
     "qsv_jit_compile": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_plan_segments": ([_P, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_int, _P, _P, C.POINTER(C.c_int64)],
+                          C.c_int),
+    "qsv_ipc_mem_handle": ([_P, _P, C.POINTER(C.c_uint64)], C.c_int),
+    "qsv_ipc_mem_open": ([_P, C.c_uint64, C.c_int, C.POINTER(_P)], C.c_int),
+    "qsv_ipc_mem_close": ([_P], C.c_int),
+    "qsv_copy_async": ([_P, _P, C.c_uint64, _P], C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -1,6 +1,9 @@
 // C ABI of libqsv.so (declared in include/qsv.h).  Launch logic for the
 // kernels in qsv_kernels.cuh and the schedule built by qsv_plan.cpp.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <map>
 
 #include <algorithm>
 #include <cstdio>
@@ -490,6 +493,84 @@ int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const 
     auto p = std::make_unique<qsv_plan>();
     p->p = build_plan(recs, n_qubits, m, r, L, s);
     *out = p.release();
+    return QSV_OK;
+}
+
+// ---- peer exchange (sharded layout, distributed.py P2PTransport) ----------
+// The global<->local qubit swap pushes contiguous blocks straight into the
+// peers' receive buffers with the copy engines over NVLink (cudaMemcpyAsync
+// between UVA pointers of CUDA-IPC-mapped allocations): no SM is taken from
+// the fused pass kernels running on the compute stream meanwhile.
+
+int qsv_ipc_mem_handle(void *device_ptr, void *handle64, uint64_t *offset) {
+    if (!device_ptr || !handle64 || !offset) return fail(QSV_E_PARSE, "null argument");
+    // driver API resolved at run time (libqsv does not link libcuda)
+    using range_fn = int (*)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn range = [] {
+        void *h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+        return h ? (range_fn)dlsym(h, "cuMemGetAddressRange_v2") : nullptr;
+    }();
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (!range || range(&base, &size, (unsigned long long)device_ptr) != 0)
+        return fail(QSV_E_DEVICE, "cuMemGetAddressRange failed (not a device allocation?)");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base));
+    std::memcpy(handle64, &h, sizeof(h));
+    *offset = (uint64_t)((unsigned long long)device_ptr - base);
+    return QSV_OK;
+}
+
+std::mutex g_ipc_mu;
+std::map<void *, void *> g_ipc_base;  // mapped pointer -> base returned by cudaIpcOpenMemHandle
+
+int qsv_ipc_mem_open(const void *handle64, uint64_t offset, int device, void **out) {
+    if (!handle64 || !out) return fail(QSV_E_PARSE, "null argument");
+    int rc = set_device(device);
+    if (rc) return rc;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    void *base = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *out = (char *)base + offset;
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    g_ipc_base[*out] = base;
+    return QSV_OK;
+}
+
+int qsv_ipc_mem_close(void *mapped) {
+    void *base = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_ipc_mu);
+        auto it = g_ipc_base.find(mapped);
+        if (it == g_ipc_base.end()) return fail(QSV_E_PARSE, "pointer was not opened by qsv_ipc_mem_open");
+        base = it->second;
+        g_ipc_base.erase(it);
+    }
+    CUDA_TRY(cudaIpcCloseMemHandle(base));
+    return QSV_OK;
+}
+
+int qsv_copy_async(void *dst, const void *src, uint64_t bytes, void *stream) {
+    CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+    return QSV_OK;
+}
+
+int qsv_plan_segments(const qsv_gate *gates, int64_t n_gates, int n_qubits, int n_local, uint64_t initial_local,
+                      int free_initial, int32_t *gate_segment, uint64_t *segment_local, int64_t *n_segments) {
+    if (n_qubits < 1 || n_qubits > 63) return fail(QSV_E_TOO_MANY_QUBITS, "qubit count out of range");
+    if (n_local < 2 || n_local > n_qubits) return fail(QSV_E_PARSE, "local qubit count out of range");
+    std::vector<GateRec> recs;
+    std::string msg;
+    int rc = to_records(gates, n_gates, n_qubits, recs, msg);
+    if (rc) return fail(rc, msg);
+    std::vector<int32_t> seg;
+    std::vector<uint64_t> loc;
+    rc = plan_segments(recs, n_qubits, n_local, initial_local, free_initial != 0, seg, loc);
+    if (rc) return fail(rc, "initial local set must hold exactly n_local qubits");
+    std::copy(seg.begin(), seg.end(), gate_segment);
+    std::copy(loc.begin(), loc.end(), segment_local);
+    *n_segments = (int64_t)loc.size();
     return QSV_OK;
 }
 

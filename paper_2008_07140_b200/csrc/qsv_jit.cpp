@@ -905,7 +905,7 @@ namespace {
 double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
                       const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
                       bool basis_param = false, bool prefetch = true, double scale_in = 1.0,
-                      bool final_pass = true, double *scale_out = nullptr) {
+                      bool final_pass = true, double *scale_out = nullptr, int gang = 1) {
     double fp64 = 0;
     double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
@@ -917,8 +917,15 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     const int S = dp.stage_end - dp.stage_begin;
     o << "  { // pass " << pi << ": " << S << " stage(s)\n";
     o << "  const u64 ntiles = " << ntiles << ";\n";
+    // gang > 1: the CTA holds `gang` tiles side by side (sub-tile `sub`), its
+    // warps run every stage in lock step (one code region in flight per SM);
+    // a sub-tile past the end recomputes the last tile without storing it
+    const std::string guard = (!host && gang > 1) ? "if (act) " : "";
     if (host) o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
-    else o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
+    else if (gang == 1) o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
+    else
+        o << "  for (u64 tg = (u64)blockIdx.x * " << gang << "u; tg < ntiles; tg += (u64)gridDim.x * " << gang
+          << "u) {\n    const bool act = tg + sub < ntiles;\n    const u64 t = act ? tg + sub : ntiles - 1;\n";
     // QSV_JIT_DIAG_L2=1 (diagnostic only, wrong results): every CTA re-processes its
     // first tile, so the kernel runs out of L2 and its time is compute + smem + barriers
     static const bool diag_l2 = std::getenv("QSV_JIT_DIAG_L2") != nullptr;
@@ -1053,10 +1060,13 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             int lr = 0;
             while (lr < m && tq[lr] == lr) ++lr;
             std::vector<int> runq(tq.begin() + lr, tq.end());
-            o << "    { const u64 nt = t + gridDim.x;\n";
-            o << "      if (nt < ntiles && " << (basis_param ? "basis == ~0ull && " : "") << "tid < " << (1u << (m - lr))
+            // (fewer than 5 forced low qubits: more runs than threads, each
+            // thread prefetches several)
+            o << "    { const u64 nt = t + (u64)gridDim.x * " << gang << "u;\n";
+            o << "      if (nt < ntiles" << (basis_param ? " && basis == ~0ull" : "") << ")\n";
+            o << "      for (unsigned j = tid; j < " << (1u << (m - lr)) << "u; j += " << T
               << "u) prefetch_l2(psi + (" << base_of("nt")
-              << ") + (" << deposit_expr("tid", runq, true) << "), " << (16u << lr) << "u); }\n";
+              << ") + (" << deposit_expr("j", runq, true) << "), " << (16u << lr) << "u); }\n";
         }
         g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
@@ -1068,7 +1078,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             // stage may still read the shared tile
             if (first && !staged_in) o << barrier;
             for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
-            o << thread_end << barrier << thread_loop << "    {\n";
+            o << thread_end << barrier << thread_loop << "    " << guard << "{\n";
             o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
             o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
             for (int k = 0; k < (1 << R); ++k)
@@ -1078,8 +1088,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         } else if (last) {
             // evict-first stores when the data leaves for HBM; write-back (L2
             // resident) stores between the inner passes of a super-pass
+            o << "    " << guard << "{\n";
             for (int rho = 0; rho < (1 << R); ++rho)
                 o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gp + " << goff[rho] << "ull, v" << rho << ");\n";
+            o << "    }\n";
             o << thread_end << "    }\n";
         } else {
             // the previous tile's last stage may still read the shared tile
@@ -1096,7 +1108,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
 constexpr double kThreeCtaMinFp64 = 60.0;
 
 std::string kernel_head(const Plan &P, int m, bool host, const char *name, const char *params,
-                        double fp64_per_amp = 0) {
+                        double fp64_per_amp = 0, int gang = 1) {
     std::ostringstream o;
     const int T = 1 << (m - P.r);
     if (host) {
@@ -1114,12 +1126,21 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
         const char *mb = std::getenv("QSV_JIT_MIN_BLOCKS");
         const bool one = T >= 512 || (16u << m) > (113u << 10);
         const bool three = !one && T <= 128 && (16u << m) <= (64u << 10) && fp64_per_amp >= kThreeCtaMinFp64;
+        if (gang > 1) {
+            o << "// gang=" << gang << "\n";
+            o << "extern \"C\" __global__ void __launch_bounds__(" << gang * T << ", 1) " << name << "(" << params
+              << ") {\n";
+            o << "  extern __shared__ double2 smem[];\n";
+            o << "  const unsigned tid = threadIdx.x & " << (T - 1) << "u, sub = threadIdx.x >> " << (m - P.r) << ";\n";
+            o << "  double2 *tile = smem + ((size_t)sub << " << m << ");\n";
+        } else {
         o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
           << (mb ? std::atoi(mb) : (one ? 1 : three ? 3 : 2)) << ") "
           << name << "(" << params << ") {\n";
         o << "  extern __shared__ double2 smem[];\n";
         o << "  double2 *tile = smem;\n";
         o << "  const unsigned tid = threadIdx.x;\n";
+        }
     }
     return o.str();
 }
@@ -1162,16 +1183,28 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
         cost = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
                (double)(1 << P.r);
     }
+    // QSV_JIT_GANG=G: compute-bound passes run G tiles per CTA in lock step
+    // (one CTA per SM) instead of independent CTAs
+    int gang = 1;
+    if (!host) {
+        static const int env_gang = std::getenv("QSV_JIT_GANG") ? std::atoi(std::getenv("QSV_JIT_GANG")) : 1;
+        const int T = 1 << (dp.m - P.r);
+        static const double gang_min =
+            std::getenv("QSV_JIT_GANG_MIN") ? std::atof(std::getenv("QSV_JIT_GANG_MIN")) : kThreeCtaMinFp64;
+        if (env_gang > 1 && cost >= gang_min && env_gang * T <= 1024 &&
+            ((size_t)env_gang << (dp.m + 4)) <= ((size_t)227 << 10))
+            gang = env_gang;
+    }
     o << kernel_head(P, dp.m, host, "qsv_pass",
                      host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis",
-                     cost);
+                     cost, gang);
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
     const char *e = std::getenv("QSV_JIT_PREFETCH");
     const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
-                                    sc, final_pass);
+                                    sc, final_pass, nullptr, gang);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
     o << "}\n";
     return o.str();
@@ -1270,7 +1303,14 @@ namespace {
 struct CacheEntry {
     CUfunction fn = nullptr;
     int grid = 0;  // persistent grid: resident CTAs per SM x SMs
+    int gang = 1;  // tiles per CTA
 };
+
+// tiles per CTA of a generated pass kernel (the "// gang=G" marker)
+int source_gang(const std::string &src) {
+    const size_t at = src.find("// gang=");
+    return at == std::string::npos ? 1 : std::atoi(src.c_str() + at + 8);
+}
 
 std::mutex g_cache_mu;
 std::map<std::pair<int, std::string>, CacheEntry> g_cache;  // (device, source) -> kernel
@@ -1373,11 +1413,12 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         CUfunction fn;
         CUresult r = drv.ModuleLoadData(&mod, u.cubin.data());
         if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&fn, mod, u.name.c_str());
-        const int smem = (int)((size_t)(jit_double_buffer() ? 32 : 16) << u.m);  // tile buffer(s)
+        const int gang = u.super ? 1 : source_gang(u.src);
+        const int smem = gang * (int)((size_t)(jit_double_buffer() ? 32 : 16) << u.m);  // tile buffer(s)
         if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
         int per_sm = 0;
         if (r == CUDA_SUCCESS)
-            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 1 << (u.m - P.r), (size_t)smem);
+            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gang << (u.m - P.r), (size_t)smem);
         if (r != CUDA_SUCCESS || per_sm < 1) {
             const char *s = nullptr;
             if (r != CUDA_SUCCESS) drv.GetErrorString(r, &s);
@@ -1386,11 +1427,12 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         }
         // QSV_JIT_CTAS_PER_SM (diagnostic): cap the persistent grid's CTAs per SM
         if (const char *c = std::getenv("QSV_JIT_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(c)));
-        found[i] = CacheEntry{fn, per_sm * sms};
+        found[i] = CacheEntry{fn, per_sm * sms, gang};
         g_cache[{device, u.src}] = found[i];
     }
     P.jit_funcs.assign(P.passes.size(), nullptr);
     P.jit_grids.assign(P.passes.size(), 0);
+    P.jit_gangs.assign(P.passes.size(), 1);
     P.jit_super_funcs.assign(P.supers.size(), nullptr);
     P.jit_super_grids.assign(P.supers.size(), 0);
     for (size_t i = 0; i < units.size(); ++i) {
@@ -1400,6 +1442,7 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         } else {
             P.jit_funcs[units[i].index] = found[i].fn;
             P.jit_grids[units[i].index] = found[i].grid;
+            P.jit_gangs[units[i].index] = found[i].gang;
         }
     }
     P.jit_device = device;
@@ -1418,10 +1461,12 @@ int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, s
     const DevPass &dp = P.passes[pass];
     const int m = dp.m, T = 1 << (m - P.r);
     unsigned long long n_tiles = 1ull << (n - m);
-    const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, (unsigned long long)P.jit_grids[pass]);
+    const int gang = pass < (int)P.jit_gangs.size() ? P.jit_gangs[pass] : 1;
+    const unsigned grid = (unsigned)std::min<unsigned long long>((n_tiles + gang - 1) / gang,
+                                                                 (unsigned long long)P.jit_grids[pass]);
     void *args[] = {&psi, &n_tiles, &basis};
-    const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, T, 1, 1,
-                                             (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
+    const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, gang * T, 1, 1,
+                                             gang * (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
                                              (CUstream)stream, args, nullptr);
     return r == CUDA_SUCCESS ? QSV_OK : cu_fail(r, "cuLaunchKernel", err);
 }

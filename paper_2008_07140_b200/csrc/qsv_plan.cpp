@@ -618,6 +618,63 @@ std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &in, int n) {
     return out;
 }
 
+// Distributed layout (distributed.py).  With the state sharded
+// over 2^g ranks only n - g qubits are local; a gate may act non-diagonally
+// only on local qubits.  The stream is cut into SEGMENTS, each run with one
+// fixed LOCAL SET of `capacity` logical qubits; between segments the qubits
+// leaving / entering the local set are exchanged (one all-to-all).  Each
+// segment takes every remaining gate its local set admits under the same
+// dependency/blocking rule as the pass planner; the set itself starts from the
+// previous one with the first blocked gate's targets brought in (evicting the
+// local qubits whose next non-diagonal use is furthest away, Belady), then the
+// single-swap local search maximises the gates absorbed.  With `free_initial`
+// (the state is a basis state, layout-free) the first set is chosen freely.
+int plan_segments(const std::vector<GateRec> &recs, int n, int capacity, uint64_t init_local, bool free_initial,
+                  std::vector<int32_t> &gate_seg, std::vector<uint64_t> &seg_local) {
+    const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    gate_seg.assign(recs.size(), -1);
+    seg_local.clear();
+    std::vector<int> rem(recs.size());
+    for (size_t i = 0; i < recs.size(); ++i) rem[i] = (int)i;
+    uint64_t local = init_local & all;
+    if (popc(local) != capacity) return QSV_E_PARSE;
+    bool first = true;
+    while (!rem.empty()) {
+        uint64_t cand = local;
+        if (first && free_initial) {
+            Absorber a;
+            a.capacity = capacity;
+            for (int gi : rem) a.offer(recs[gi]);
+            cand = padded_tile(a.resident, all, n, capacity);
+        }
+        first = false;
+        // next non-diagonal use of every qubit (position in rem)
+        std::vector<size_t> next(n, rem.size());
+        for (size_t k = rem.size(); k-- > 0;)
+            for (int q = 0; q < n; ++q)
+                if ((recs[rem[k]].nmask >> q) & 1) next[q] = k;
+        const GateRec &g0 = recs[rem[0]];
+        uint64_t need = g0.nmask & ~cand;
+        while (need) {
+            int victim = -1;
+            for (int q = 0; q < n; ++q)
+                if (((cand >> q) & 1) && !((g0.nmask >> q) & 1) && (victim < 0 || next[q] > next[victim])) victim = q;
+            const uint64_t in = need & (~need + 1);
+            cand = (cand & ~(1ull << victim)) | in;
+            need ^= in;
+        }
+        cand = search_tile(recs, rem, cand, 0, n, all);
+        std::vector<int> taken, deferred;
+        scan_fixed_tile(recs, rem, cand, &taken, &deferred);
+        if (taken.empty()) return QSV_E_UNSUPPORTED;  // unreachable: rem[0] always fits
+        for (int gi : taken) gate_seg[gi] = (int32_t)seg_local.size();
+        seg_local.push_back(cand);
+        local = cand;
+        rem.swap(deferred);
+    }
+    return QSV_OK;
+}
+
 // Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy
 // absorption with capacity s); its gates are then split into ordinary passes
 // whose tiles lie inside S.  The executor runs all inner passes of a

@@ -120,6 +120,7 @@ struct Plan {
     // specialised kernels (qsv_jit.cpp), one CUfunction per pass
     std::vector<void *> jit_funcs;
     std::vector<int> jit_grids;
+    std::vector<int> jit_gangs;  // tiles per CTA of each pass kernel
     std::vector<void *> jit_super_funcs;  // per super-pass (nullptr: run its inner passes flat)
     std::vector<int> jit_super_grids;
     std::vector<int> super_use;  // cost-model choice per super-pass (jit_choose_supers)
@@ -140,5 +141,10 @@ Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, in
 std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &recs, int n);
 
 void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int &s);
+
+// Distributed layout: segments of the stream that each run with one fixed set of
+// `capacity` local qubits (see qsv_plan.cpp).  gate_seg[i] = segment of gate i.
+int plan_segments(const std::vector<GateRec> &recs, int n, int capacity, uint64_t init_local, bool free_initial,
+                  std::vector<int32_t> &gate_seg, std::vector<uint64_t> &seg_local);
 
 }  // namespace qsv

@@ -1,31 +1,51 @@
 """Sharded full-amplitude state across P = 2^g GPUs (one process per GPU).
 
-Layout.  The state of n logical qubits is split by the top g
+Layout.  The state of n qubits is split by the top g
 PHYSICAL index bits: rank r holds the 2^(n-g) amplitudes whose global bits
-equal r, contiguously, in a device buffer driven by libqsv.  A
-logical->physical qubit map `perm` records where every logical qubit lives;
-physical positions [0, n_local) are local, [n_local, n) are global (rank
-bits).  The reference has no distributed mode (MPI is a SPEC.md:233
-non-goal); the nearest analogue is its cross-chunk ownership
-(statevector.py:5-8, 185-187), where a global qubit plays the role of a
-chunk-index bit.
+equal r, contiguously, in a device buffer driven by libqsv.  The reference has
+no distributed mode (MPI is a SPEC.md:233 non-goal); the nearest analogue is
+its cross-chunk ownership (statevector.py:5-8, 185-187), where a global qubit
+plays the role of a chunk-index bit.
 
-Per gate, on every rank:
+Two maps are kept on every rank:
+* `dq`: logical qubit -> DATA qubit.  An uncontrolled SWAP moves no data: it
+  exchanges two entries of `dq` (QFT's bit-reversal layer is free);
+* `perm`: data qubit -> physical position; [0, n_local) are local positions,
+  [n_local, n) global (rank bits).
+
+Schedule.  libqsv's segment planner (`qsv_plan_segments`, C++) cuts the
+gate stream into SEGMENTS that each run with one fixed set of n_local local
+data qubits, taking every gate the set admits under the fused scheduler's
+commutation rule (gates acting diagonally on a shared qubit commute); the set
+changes only when no further gate fits (C3 random circuits: ONE exchange of
+g qubits per circuit).  Within a segment:
 * a control on a global qubit is a per-rank constant - the gate is skipped
   where it is 0 and the control dropped where it is 1 (cf. the reference's
   high-control chunk skip, statevector.py:170-172);
 * a diagonal factor on a global qubit is a per-rank constant (cf. _k_scale,
-  statevector.py:128-132): no communication;
-* a non-diagonal target on a global qubit triggers a GLOBAL<->LOCAL QUBIT SWAP
-  with the top local qubits: each rank cuts its buffer into 2^s contiguous
-  blocks and exchanges them with the 2^s ranks that differ in the swapped
-  global bits (all-to-all of contiguous blocks, NCCL over NVLink on the GPU
-  path), after which `perm` is updated.
+  statevector.py:128-132);
+* runs of local gates go to the native fused scheduler (`qsv_run`).
 
-Runs of local gates between swaps go to the native fused scheduler (one
-`qsv_run` per run).  The local engine is pluggable: `CudaShard` (libqsv on
-this rank's GPU, the product path) or any object with the same methods (the
-gloo CPU tests plug in the oracle).
+Exchange (global <-> local qubit swap).  Leaving qubits V are first moved
+(SWAP gates appended to the previous run - the fused planner turns them into
+relabellings materialised by its last pass) onto the exchange positions
+X = [n_local - c - s, n_local - c) just below the c CHUNK positions at the
+top.  Chunk i (the contiguous quarter/eighth/... of the buffer with top bits
+= i) is then exchanged as 2^s contiguous blocks with the 2^s ranks that differ
+in the entering qubits' global bits, and the next segment's gates that do not
+act non-diagonally on chunk positions (its PREFIX) run on chunk i as soon as
+chunk i has arrived, while chunk i+1 is in flight.  Transports:
+* `P2PTransport` - CUDA IPC mappings of the peers' buffers; the copy engines
+  push every block straight into the peer's receive buffer over NVLink
+  (no SM taken from the pass kernels), cross-process events order chunk i's
+  arrival before its prefix on the compute stream;
+* `AllToAllTransport` - `torch.distributed.all_to_all_single` per chunk
+  (NCCL on GPUs; gloo on CPU tensors for the tests, or staged through host
+  memory for GPU buffers under gloo).
+
+The local engine is pluggable: `CudaShard` (libqsv on this rank's GPU, the
+product path) or any object with the same methods (the gloo CPU tests plug
+in the oracle).
 """
 
 from __future__ import annotations
@@ -45,12 +65,17 @@ def _is_diag(u) -> bool:
     return gates.is_diagonal(u)
 
 
+def _is_plain_swap(u, controls) -> bool:
+    return not controls and u.shape == (4, 4) and np.array_equal(u, gates.SWAP)
+
+
 @dataclass
 class SwapRecord:
     global_positions: tuple
     local_positions: tuple
     bytes_sent: int
-    seconds: float = 0.0
+    chunks: int = 1
+    prefix_gates: int = 0
 
 
 @dataclass
@@ -59,13 +84,32 @@ class ShardStats:
     gate_runs: int = 0
     local_gates: int = 0
     skipped_gates: int = 0
+    relabelled_swaps: int = 0
+    placement_swaps: int = 0
+    segments: int = 0
+
+
+def plan_segments(items, n: int, n_local: int, local_mask: int, free_initial: bool):
+    """libqsv segment planner over (u, targets, controls) items on DATA qubits.
+    Returns (segment of every item, local data-qubit mask of every segment)."""
+    from . import _native as N
+
+    rec = N.gate_records(items)
+    seg = np.zeros(max(1, len(rec)), dtype=np.int32)
+    loc = np.zeros(max(1, len(rec)), dtype=np.uint64)
+    ns = C.c_int64()
+    N.check(N.lib().qsv_plan_segments(rec.ctypes.data, len(rec), n, n_local, C.c_uint64(local_mask),
+                                      int(free_initial), seg.ctypes.data, loc.ctypes.data, C.byref(ns)))
+    return seg[:len(rec)].tolist(), [int(x) for x in loc[:ns.value]]
 
 
 class CudaShard:
     """This rank's 2^n_local amplitudes in device memory, driven by libqsv.
 
-    The buffer is a torch tensor (so torch.distributed/NCCL can exchange it
-    in place); libqsv wraps the same memory with `qsv_create_on`."""
+    Two equally sized buffers (torch tensors, so torch.distributed/NCCL can
+    exchange them in place) alternate as state and receive buffer; libqsv
+    wraps each (and each chunk of each) with `qsv_create_on` handles that all
+    run on this shard's compute stream."""
 
     def __init__(self, n_local: int, device: int, stream=None, options=None):
         import torch
@@ -78,20 +122,37 @@ class CudaShard:
         self.device = device
         self.stream = stream or torch.cuda.Stream(device=device)
         self.options = options or N.options()
-        self.buf = torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")
-        self.spare = torch.empty_like(self.buf)
-        self._wrap()
+        self.bufs = [torch.zeros(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}"),
+                     torch.empty(1 << n_local, dtype=torch.complex128, device=f"cuda:{device}")]
+        self.cur = 0  # index of the state buffer
+        self._handles = {}  # (buffer, chunk_log2, chunk) -> qsv handle
 
-    def _wrap(self):
-        h = C.c_void_p()
-        self.N.check(self.N.lib().qsv_create_on(self.n_local, self.device, C.c_void_p(self.stream.cuda_stream),
-                                                C.c_void_p(self.buf.data_ptr()), C.byref(h)))
-        self.h = h
+    @property
+    def buf(self):
+        return self.bufs[self.cur]
+
+    def handle(self, chunk=None):
+        c, i = chunk if chunk else (0, 0)
+        key = (self.cur, c, i)
+        h = self._handles.get(key)
+        if h is None:
+            h = C.c_void_p()
+            nsub = self.n_local - c
+            ptr = self.buf.data_ptr() + (i << nsub) * 16
+            self.N.check(self.N.lib().qsv_create_on(nsub, self.device, C.c_void_p(self.stream.cuda_stream),
+                                                    C.c_void_p(ptr), C.byref(h)))
+            self._handles[key] = h
+        return h
+
+    @property
+    def h(self):
+        return self.handle()
 
     def close(self):
-        if getattr(self, "h", None) is not None and self.h.value:
-            self.N.lib().qsv_destroy(self.h)
-            self.h = C.c_void_p()
+        for h in self._handles.values():
+            if h.value:
+                self.N.lib().qsv_destroy(h)
+        self._handles.clear()
 
     def set_basis(self, index: int | None):
         """|index> restricted to this shard (None: all zeros)."""
@@ -107,33 +168,33 @@ class CudaShard:
         self.stream.synchronize()
 
     def download(self) -> np.ndarray:
-        self.N.check(self.N.lib().qsv_synchronize(self.h))
+        self.stream.synchronize()
         with self.torch.cuda.stream(self.stream):
             out = self.buf.cpu().numpy()
         return out
 
-    def run(self, items, stats: dict | None = None):
+    def run(self, items, stats: dict | None = None, chunk=None):
         if not items:
             return
         rec = self.N.gate_records(items)
         st = self.N.qsv_run_stats()
-        self.N.check(self.N.lib().qsv_run(self.h, rec.ctypes.data, len(rec), C.byref(self.options), C.byref(st)))
+        self.N.check(self.N.lib().qsv_run(self.handle(chunk), rec.ctypes.data, len(rec), C.byref(self.options),
+                                          C.byref(st)))
         if stats is not None:
             for k, v in st.as_dict().items():
                 stats[k] = stats.get(k, 0) + v
 
     def exchange_buffers(self):
-        """(send, recv) float64 views for an all-to-all; libqsv is drained first."""
-        self.N.check(self.N.lib().qsv_synchronize(self.h))
+        """(send, recv) float64 views for an all-to-all, ordered after the
+        compute stream's pending work on the caller's current stream."""
         self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
-        return self.torch.view_as_real(self.buf).reshape(-1), self.torch.view_as_real(self.spare).reshape(-1)
+        return (self.torch.view_as_real(self.bufs[self.cur]).reshape(-1),
+                self.torch.view_as_real(self.bufs[1 - self.cur]).reshape(-1))
 
     def commit_exchange(self):
-        """The receive buffer becomes the state."""
-        self.torch.cuda.current_stream(self.device).synchronize()
-        self.buf, self.spare = self.spare, self.buf
-        self.close()
-        self._wrap()
+        """The receive buffer becomes the state (no synchronisation: later
+        work is ordered by the transport's stream waits)."""
+        self.cur = 1 - self.cur
 
     def norm_sq(self) -> float:
         out = C.c_double()
@@ -141,10 +202,171 @@ class CudaShard:
         return out.value
 
 
+# ---------------------------------------------------------------------------
+# transports
+# ---------------------------------------------------------------------------
+
+
+class AllToAllTransport:
+    """One `all_to_all_single` per chunk: NCCL over NVLink for device buffers,
+    gloo for CPU buffers (tests), or gloo staged through host memory."""
+
+    def __init__(self, dist, group=None):
+        self.dist = dist
+        self.group = group
+        self.gloo = dist.get_backend(group) == "gloo"
+
+    def exchange(self, sim, G, chunk_log2, on_chunk):
+        import torch
+
+        shard = sim.shard
+        s = len(G)
+        nl = sim.n_local
+        chunk = 2 << (nl - chunk_log2)  # float64 per chunk
+        blk = chunk >> s
+        gmask = sum(1 << (p - nl) for p in G)
+        splits = [blk if (r & ~gmask) == (sim.rank & ~gmask) else 0 for r in range(sim.world)]
+        send, recv = shard.exchange_buffers()
+        stream = getattr(shard, "stream", None)
+        on_device = send.device.type != "cpu"
+        works = []
+        for i in range(1 << chunk_log2):
+            sl = slice(i * chunk, (i + 1) * chunk)
+            if self.gloo and on_device:
+                hs, hr = send[sl].cpu(), torch.empty(chunk, dtype=send.dtype)
+                self.dist.all_to_all_single(hr, hs, output_split_sizes=splits, input_split_sizes=splits,
+                                            group=self.group)
+                recv[sl].copy_(hr)
+                works.append(None)
+            else:
+                works.append(self.dist.all_to_all_single(recv[sl], send[sl], output_split_sizes=splits,
+                                                         input_split_sizes=splits, group=self.group,
+                                                         async_op=True))
+        shard.commit_exchange()
+        for i, w in enumerate(works):
+            if w is not None:
+                if on_device and stream is not None:
+                    with torch.cuda.stream(stream):
+                        w.wait()  # the compute stream waits for chunk i
+                else:
+                    w.wait()
+            elif on_device and stream is not None:
+                stream.wait_stream(torch.cuda.current_stream(send.device))
+            on_chunk(i)
+
+
+class P2PTransport:
+    """Copy-engine pushes into CUDA-IPC-mapped peer buffers (NVLink P2P).
+
+    Setup shares both buffers of every rank (qsv_ipc_mem_handle) and one
+    interprocess event per chunk (torch.cuda.Event(interprocess=True)).  An
+    exchange: wait until every rank's previous pushes completed (host
+    barrier) so every receive buffer is free; push chunk by chunk on the copy
+    stream, recording chunk i's event after its blocks; host barrier (every
+    rank has ENQUEUED its records); the compute stream then waits for chunk i's
+    events of all partner ranks before running the prefix on chunk i."""
+
+    def __init__(self, dist, shard, group=None, max_chunk_log2: int = 3):
+        import torch
+
+        from . import _native as N
+
+        self.dist, self.group, self.shard, self.N = dist, group, shard, N
+        self.torch = torch
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.copy_stream = torch.cuda.Stream(device=shard.device)
+        L = N.lib()
+        mine = []
+        for b in shard.bufs:
+            hbuf = C.create_string_buffer(64)
+            off = C.c_uint64()
+            N.check(L.qsv_ipc_mem_handle(C.c_void_p(b.data_ptr()), hbuf, C.byref(off)))
+            mine.append((hbuf.raw, off.value))
+        self.events = [torch.cuda.Event(interprocess=True) for _ in range(1 << max_chunk_log2)]
+        ev_handles = [e.ipc_handle() for e in self.events]
+        allh = [None] * self.world
+        dist.all_gather_object(allh, (mine, ev_handles), group=group)
+        self.peer_ptr = []  # [rank][buffer] -> device pointer (own buffers: local pointers)
+        self.peer_events = []
+        self._opened = []
+        for r, (bufs, evh) in enumerate(allh):
+            if r == self.rank:
+                self.peer_ptr.append([b.data_ptr() for b in shard.bufs])
+                self.peer_events.append(self.events)
+                continue
+            ptrs = []
+            for raw, off in bufs:
+                p = C.c_void_p()
+                N.check(L.qsv_ipc_mem_open(raw, off, shard.device, C.byref(p)))
+                self._opened.append(p)
+                ptrs.append(p.value)
+            self.peer_ptr.append(ptrs)
+            self.peer_events.append([torch.cuda.Event.from_ipc_handle(shard.device, h) for h in evh])
+        self.max_chunk_log2 = max_chunk_log2
+        self.last_exchange_ms = 0.0
+        self._t0 = torch.cuda.Event(enable_timing=True)
+        self._t1 = torch.cuda.Event(enable_timing=True)
+
+    def close(self):
+        for p in self._opened:
+            self.N.lib().qsv_ipc_mem_close(p)
+        self._opened.clear()
+
+    def exchange(self, sim, G, chunk_log2, on_chunk):
+        torch, L = self.torch, self.N.lib()
+        shard = self.shard
+        assert chunk_log2 <= self.max_chunk_log2
+        s, nl = len(G), sim.n_local
+        gbits = [p - nl for p in G]
+        gmask = sum(1 << b for b in gbits)
+        my_g = sum(((self.rank >> b) & 1) << i for i, b in enumerate(gbits))
+        chunk = 1 << (nl - chunk_log2)  # amplitudes
+        blk = chunk >> s
+        src_base = shard.bufs[shard.cur].data_ptr()
+        spare = 1 - shard.cur
+        # every rank's previous pushes are complete -> every receive buffer is free
+        self.copy_stream.synchronize()
+        self.dist.barrier(group=self.group)
+        self.copy_stream.wait_stream(shard.stream)  # this rank's send data is final
+        partners = []
+        for j in range(1 << s):
+            peer = self.rank & ~gmask
+            for i, b in enumerate(gbits):
+                peer |= ((j >> i) & 1) << b
+            partners.append(peer)
+        self._t0.record(self.copy_stream)
+        for i in range(1 << chunk_log2):
+            for j, peer in enumerate(partners):
+                src = src_base + (i * chunk + j * blk) * 16
+                dst = self.peer_ptr[peer][spare] + (i * chunk + my_g * blk) * 16
+                self.N.check(L.qsv_copy_async(C.c_void_p(dst), C.c_void_p(src), blk * 16,
+                                              C.c_void_p(self.copy_stream.cuda_stream)))
+            self.events[i].record(self.copy_stream)
+        self._t1.record(self.copy_stream)
+        self.dist.barrier(group=self.group)  # every partner has enqueued its chunk events
+        shard.commit_exchange()
+        for i in range(1 << chunk_log2):
+            for peer in partners:
+                shard.stream.wait_event(self.peer_events[peer][i])
+            on_chunk(i)
+
+    def exchange_ms(self) -> float:
+        """Copy-stream time of the last exchange (this rank's pushes)."""
+        self._t1.synchronize()
+        return self._t0.elapsed_time(self._t1)
+
+
+# ---------------------------------------------------------------------------
+# the sharded simulator
+# ---------------------------------------------------------------------------
+
+
 class ShardedSimulator:
     """Runs expanded gate streams on a state sharded over a process group."""
 
-    def __init__(self, n: int, shard, group=None, rank: int | None = None, world: int | None = None):
+    def __init__(self, n: int, shard, group=None, rank: int | None = None, world: int | None = None,
+                 chunk_log2: int | None = None, transport=None):
         import torch.distributed as dist
 
         self.dist = dist
@@ -158,131 +380,202 @@ class ShardedSimulator:
             raise ValueError(f"{n} qubits cannot be sharded over {self.world} ranks")
         self.n, self.g, self.n_local = n, g, n - g
         self.shard = shard
-        # gloo cannot exchange device tensors: stage the blocks through host memory
-        self.stage_host = dist.get_backend(group) == "gloo"
-        self.perm = list(range(n))  # logical qubit -> physical position
+        if chunk_log2 is None:
+            chunk_log2 = int(os.environ.get("QSV_SWAP_CHUNKS_LOG2", "2" if self.n_local >= 16 else "0"))
+        self.chunk_log2 = chunk_log2
+        self.transport = transport or AllToAllTransport(dist, group)
+        self.dq = list(range(n))    # logical -> data qubit
+        self.perm = list(range(n))  # data qubit -> physical position
+        self._basis = None          # pending basis index (layout still free)
         self.stats = ShardStats()
 
     # -- bookkeeping ----------------------------------------------------------
     def _rank_bit(self, phys: int) -> int:
         return (self.rank >> (phys - self.n_local)) & 1
 
-    def _logical_at(self, phys: int) -> int:
+    def _occupant(self, phys: int) -> int:
         return self.perm.index(phys)
 
+    def _local_mask(self) -> int:
+        return sum(1 << q for q in range(self.n) if self.perm[q] < self.n_local)
+
     def set_basis(self, index: int = 0):
-        """|index> (logical basis index) with the identity layout."""
+        """|index> (logical basis index).  Materialised lazily: a basis state
+        fits any layout, so the first segment picks its local qubits freely."""
+        self.dq = list(range(self.n))
         self.perm = list(range(self.n))
-        local = index & ((1 << self.n_local) - 1)
-        self.shard.set_basis(local if (index >> self.n_local) == self.rank else None)
+        self._basis = index
 
-    # -- the global <-> local qubit swap ------------------------------------------
-    def swap_in(self, need_global: list[int], keep: set[int] = frozenset()):
-        """Exchange global physical positions `need_global` with the top local
-        positions (all-to-all of contiguous blocks within each 2^s-rank group)."""
-        import time
+    def upload_local(self, host_slice: np.ndarray):
+        """This rank's slice of a logical-order state (identity layout)."""
+        self.dq = list(range(self.n))
+        self.perm = list(range(self.n))
+        self._basis = None
+        self.shard.upload(host_slice)
 
-        G = sorted(need_global)
-        s = len(G)
-        top = list(range(self.n_local - s, self.n_local))
-        # a top local position holding a qubit the current gate needs locally is
-        # first moved down with a local SWAP gate
-        for p in top:
-            lq = self._logical_at(p)
-            if lq in keep:
-                free = next(q for q in range(self.n_local - s - 1, -1, -1)
-                            if self._logical_at(q) not in keep)
-                self.shard.run([(gates.SWAP, (p, free), ())])
-                lf = self._logical_at(free)
-                self.perm[lq], self.perm[lf] = free, p
-        chunk = 1 << (self.n_local - s)
-        send, recv = self.shard.exchange_buffers()
-        gbits = [q - self.n_local for q in G]
-        mask = sum(1 << b for b in gbits)
-        splits = []
-        for r in range(self.world):
-            splits.append(2 * chunk if (r & ~mask) == (self.rank & ~mask) else 0)
-        t0 = time.perf_counter()
-        if self.stage_host and send.device.type != "cpu":
-            hs, hr = send.cpu(), send.new_empty(send.shape, device="cpu")
-            self.dist.all_to_all_single(hr, hs, output_split_sizes=splits, input_split_sizes=splits,
-                                        group=self.group)
-            recv.copy_(hr)
-        else:
-            self.dist.all_to_all_single(recv, send, output_split_sizes=splits, input_split_sizes=splits,
-                                        group=self.group)
-        self.shard.commit_exchange()
-        dt = time.perf_counter() - t0
-        # physical positions G[i] <-> top[i] exchange their logical qubits
-        for gp, lp in zip(G, top):
-            a, b = self._logical_at(gp), self._logical_at(lp)
-            self.perm[a], self.perm[b] = lp, gp
-        self.stats.swaps.append(SwapRecord(tuple(G), tuple(top), 16 * chunk * ((1 << s) - 1), dt))
+    def _materialize(self):
+        if self._basis is None:
+            return
+        phys = 0
+        for q in range(self.n):  # logical q = data q right after set_basis
+            if (self._basis >> q) & 1:
+                phys |= 1 << self.perm[q]
+        nl = self.n_local
+        self.shard.set_basis(phys & ((1 << nl) - 1) if (phys >> nl) == self.rank else None)
+        self._basis = None
 
-    # -- gate stream ------------------------------------------------------------
-    def _localise(self, u, targets, controls):
-        """Map one controlled-form gate onto this shard, or None when it is a
-        no-op here.  Targets must already be local when the gate is not diagonal."""
-        u = np.asarray(u, dtype=np.complex128)
+    # -- localisation -----------------------------------------------------------
+    def _localise(self, item, chunk=None):
+        """Map one gate on physical positions onto this shard (or onto chunk
+        `chunk` = (c, i) of it), or None when it is a no-op here.  Positions at or
+        above the view's size are fixed bits: chunk bits, then rank bits."""
+        u, pt, pc = item
+        nv = self.n_local - (chunk[0] if chunk else 0)
+
+        def fixed(p):
+            if p >= self.n_local:
+                return self._rank_bit(p)
+            return (chunk[1] >> (p - nv)) & 1
+
         ctl = []
-        for c in controls:
-            pc = self.perm[c]
-            if pc >= self.n_local:
-                if not self._rank_bit(pc):
-                    return None  # a global control is 0 on this rank
+        for p in pc:
+            if p >= nv:
+                if not fixed(p):
+                    return None  # a fixed control is 0 here
             else:
-                ctl.append(pc)
-        pt = [self.perm[t] for t in targets]
-        glob = [i for i, p in enumerate(pt) if p >= self.n_local]
+                ctl.append(p)
+        glob = [i for i, p in enumerate(pt) if p >= nv]
         if not glob:
             return (u, tuple(pt), tuple(ctl))
         if not _is_diag(u):
-            raise AssertionError("non-diagonal gate on a global qubit must be swapped in first")
+            raise AssertionError("non-diagonal gate on a fixed qubit must be exchanged in first")
         d = np.diag(u)
-        anchor = next(q for q in range(self.n_local) if q not in ctl)
+        anchor = next(q for q in range(nv) if q not in ctl)
         if len(pt) == 1:
-            f = d[self._rank_bit(pt[0])]
+            f = d[fixed(pt[0])]
             return None if f == 1 else (np.diag([f, f]), (anchor,), tuple(ctl))
-        b = [self._rank_bit(p) if p >= self.n_local else None for p in pt]
+        b = [fixed(p) if p >= nv else None for p in pt]
         if len(glob) == 2:
             f = d[2 * b[0] + b[1]]
             return None if f == 1 else (np.diag([f, f]), (anchor,), tuple(ctl))
-        if glob == [0]:  # first target (matrix MSB) global
+        if glob == [0]:  # first target (matrix MSB) fixed
             return (np.diag([d[2 * b[0]], d[2 * b[0] + 1]]), (pt[1],), tuple(ctl))
         return (np.diag([d[b[1]], d[2 + b[1]]]), (pt[0],), tuple(ctl))
 
+    def _physical(self, item):
+        u, t, c = item
+        return (u, tuple(self.perm[q] for q in t), tuple(self.perm[q] for q in c))
+
+    def _flush(self, run, stats):
+        self.shard.run(run, stats)
+        self.stats.gate_runs += bool(run)
+
+    # -- the global <-> local qubit swap ------------------------------------------
+    def _transition(self, new_local: int, seg_items, run, stats):
+        """Exchange into local set `new_local`; returns the segment's gates not
+        already run on the chunks (the part after its prefix)."""
+        nl = self.n_local
+        E = [q for q in range(self.n) if (new_local >> q) & 1 and self.perm[q] >= nl]
+        V = [q for q in range(self.n) if not (new_local >> q) & 1 and self.perm[q] < nl]
+        s = len(E)
+        c = max(0, min(self.chunk_log2, nl - s - 2))
+        X = list(range(nl - c - s, nl - c))
+        # leaving qubits onto the exchange positions (SWAPs fused into the run)
+        for v in V:
+            if self.perm[v] in X:
+                continue
+            x = next(p for p in X if self._occupant(p) not in V)
+            w = self._occupant(x)
+            run.append((gates.SWAP, (self.perm[v], x), ()))
+            self.perm[v], self.perm[w] = x, self.perm[v]
+            self.stats.placement_swaps += 1
+        self._flush(run, stats)
+        G = sorted(self.perm[e] for e in E)
+        Xs = sorted(self.perm[v] for v in V)
+        assert Xs == X
+        for gp, xp in zip(G, X):  # bit i of the block index <-> bit i of the partner's global index
+            a, b = self._occupant(gp), self._occupant(xp)
+            self.perm[a], self.perm[b] = xp, gp
+        # prefix: gates of the segment that never act non-diagonally on chunk positions
+        nv = nl - c
+        prefix, rest = [], []
+        bN = bD = 0
+        for it in seg_items:
+            u, pt, pc = self._physical(it)
+            diag = _is_diag(u)
+            nmask = 0 if diag else sum(1 << p for p in pt)
+            dmask = sum(1 << p for p in pc) | (sum(1 << p for p in pt) if diag else 0)
+            blocked = ((nmask | dmask) & bN) or (nmask & bD)
+            if c and not blocked and not any(p >= nv for p in (pt if not diag else ())):
+                prefix.append((u, pt, pc))
+            else:
+                rest.append(it)
+                bN |= nmask
+                bD |= dmask
+
+        def on_chunk(i):
+            items = [x for x in (self._localise(p, (c, i)) for p in prefix) if x is not None]
+            self.shard.run(items, stats, chunk=(c, i))
+
+        self.transport.exchange(self, G, c, on_chunk)
+        self.stats.swaps.append(SwapRecord(tuple(G), tuple(X), 16 * (1 << nl) * ((1 << s) - 1) >> s, 1 << c,
+                                           len(prefix)))
+        return rest
+
+    # -- gate stream ------------------------------------------------------------
     def run(self, program, stats: dict | None = None):
         """Apply every gate of an expanded Program (MEASURE / PMEASURE are
         not supported on the sharded path)."""
-        batch = []
+        items = []
         for inst in program.instructions:
             if not inst.is_gate:
                 raise UnsupportedGate(f"{inst.name} is not supported on a sharded state", inst.line)
             u, targets, controls = gates.controlled_form(inst)
             if len(targets) > 2:
                 raise UnsupportedGate(f"{inst.name} targets {targets}", inst.line)
-            if not _is_diag(u):
-                need = [self.perm[t] for t in targets if self.perm[t] >= self.n_local]
-                if need:
-                    self.shard.run(batch, stats)
-                    self.stats.gate_runs += bool(batch)
-                    batch = []
-                    self.swap_in(need, keep={t for t in targets})
-            item = self._localise(u, targets, controls)
-            if item is None:
-                self.stats.skipped_gates += 1
+            u = np.asarray(u, dtype=np.complex128)
+            if _is_plain_swap(u, controls):
+                a, b = targets
+                self.dq[a], self.dq[b] = self.dq[b], self.dq[a]
+                self.stats.relabelled_swaps += 1
                 continue
-            batch.append(item)
-            self.stats.local_gates += 1
-        self.shard.run(batch, stats)
-        self.stats.gate_runs += bool(batch)
+            items.append((u, tuple(self.dq[t] for t in targets), tuple(self.dq[c] for c in controls)))
+        if not items:
+            self._materialize()
+            return
+        free = self._basis is not None
+        seg, seg_local = plan_segments(items, self.n, self.n_local, self._local_mask(), free)
+        if free:
+            loc = [q for q in range(self.n) if (seg_local[0] >> q) & 1]
+            glo = [q for q in range(self.n) if not (seg_local[0] >> q) & 1]
+            for p, q in enumerate(loc + glo):
+                self.perm[q] = p
+        self._materialize()
+        by_seg = [[] for _ in seg_local]
+        for it, k in zip(items, seg):
+            by_seg[k].append(it)
+        self.stats.segments += len(seg_local)
+        run = []
+        for k, seg_items in enumerate(by_seg):
+            if seg_local[k] != self._local_mask():
+                seg_items = self._transition(seg_local[k], seg_items, run, stats)
+                run = []
+            for it in seg_items:
+                loc_it = self._localise(self._physical(it))
+                if loc_it is None:
+                    self.stats.skipped_gates += 1
+                    continue
+                run.append(loc_it)
+                self.stats.local_gates += 1
+        self._flush(run, stats)
 
     # -- readout ----------------------------------------------------------------
     def norm_sq(self) -> float:
         import torch
 
+        self._materialize()
         v = torch.tensor([self.shard.norm_sq()], dtype=torch.float64,
-                         device="cpu" if self.stage_host else getattr(self.shard, "reduce_device", "cpu"))
+                         device=getattr(self.shard, "reduce_device", "cpu"))
         self.dist.all_reduce(v, group=self.group)
         return float(v.item())
 
@@ -290,9 +583,10 @@ class ShardedSimulator:
         """All 2^n amplitudes in LOGICAL order on rank 0 (None elsewhere)."""
         import torch
 
+        self._materialize()
         # complex128 travels as float64 pairs (gloo/NCCL reductions are real)
         local = torch.from_numpy(self.shard.download().copy().view(np.float64))
-        dev = "cpu" if self.stage_host else getattr(self.shard, "reduce_device", "cpu")
+        dev = getattr(self.shard, "reduce_device", "cpu")
         local = local.to(dev)
         parts = [torch.empty_like(local) for _ in range(self.world)] if self.rank == 0 else None
         self.dist.gather(local, parts, dst=0, group=self.group)
@@ -301,15 +595,21 @@ class ShardedSimulator:
         phys = torch.cat(parts).cpu().numpy().view(np.complex128)  # index = rank << n_local | local
         idx = np.arange(1 << self.n, dtype=np.int64)
         src = np.zeros_like(idx)
-        for q in range(self.n):  # logical bit q lives at physical position perm[q]
-            src |= ((idx >> q) & 1) << self.perm[q]
+        for q in range(self.n):  # logical bit q lives at physical position perm[dq[q]]
+            src |= ((idx >> q) & 1) << self.perm[self.dq[q]]
         return phys[src]
 
 
+def make_transport(kind: str, dist, shard, group=None):
+    if kind == "p2p":
+        return P2PTransport(dist, shard, group)
+    return AllToAllTransport(dist, group)
+
+
 def bench_main(args) -> None:
-    """`bench.py --gpus N` under torchrun: weak-scaled RQC, n = 30 + log2(N)."""
+    """`bench.py --gpus N` under torchrun: C3 weak scaling, RQC with
+    n = 32 + log2(N) qubits (2^32 local amplitudes = 64 GiB per GPU)."""
     import json
-    import time
 
     import torch
     import torch.distributed as dist
@@ -323,13 +623,15 @@ def bench_main(args) -> None:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     g = int(round(math.log2(world)))
-    n = (args.qubits or 30) + g
+    n = (args.qubits or 32) + g
     prog = parse_program(workloads.rqc_for_qubits(n, 24, 0))
     G = len(prog.gate_instructions())
     shard = CudaShard(n - g, local, options=N.options(tile_qubits=args.tile, reg_qubits=args.regs,
                                                       low_qubits=args.low))
     shard.reduce_device = f"cuda:{local}"
-    sim = ShardedSimulator(n, shard)
+    kind = os.environ.get("QSV_TRANSPORT", "p2p")
+    transport = make_transport(kind, dist, shard)
+    sim = ShardedSimulator(n, shard, transport=transport)
 
     def step():
         sim.set_basis(0)
@@ -341,27 +643,36 @@ def bench_main(args) -> None:
     dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sim.stats.swaps.clear()
-    ev0.record()
+    ev0.record(shard.stream)
     for _ in range(args.steps):
         step()
-    ev1.record()
+    ev1.record(shard.stream)
     torch.cuda.synchronize()
     ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms_step = float(ms.item())
     swaps = sim.stats.swaps
     swap_bytes = sum(s.bytes_sent for s in swaps) / max(1, args.steps)
+    xfer = {}
+    if kind == "p2p" and swaps:
+        t = torch.tensor([transport.exchange_ms()], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        last = swaps[-1].bytes_sent
+        xfer = {"last_exchange_ms": float(t.item()), "last_exchange_bytes_per_rank": last,
+                "nvlink_gbs_per_rank": last / (float(t.item()) / 1e3) / 1e9, "nvlink_peak_gbs": 900.0}
     if rank == 0:
         line = {
             "metric": "amplitude-gate updates/s", "value": G * float(1 << n) / (ms_step / 1e3),
             "unit": "amp-gate/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128 (f64)", "data": "synthetic",
-            "config": {"workload": f"C3-style weak scaling: RQC n={n} on grid {workloads.grid_shape(n)}, 24 cycles",
+            "config": {"workload": f"C3 weak scaling: RQC n={n} on grid {workloads.grid_shape(n)}, 24 cycles",
                        "n_qubits": n, "n_local": n - g, "gates": G, "parallelism": f"sharded x{world}",
+                       "transport": kind, "chunks": 1 << sim.chunk_log2,
                        "swaps_per_step": len(swaps) / max(1, args.steps),
-                       "swap_bytes_per_rank_per_step": swap_bytes},
+                       "swap_bytes_per_rank_per_step": swap_bytes, **xfer},
             "gpu_launches": None,
         }
         print(json.dumps(line), flush=True)
+    transport.close() if hasattr(transport, "close") else None
     dist.destroy_process_group()

@@ -245,13 +245,13 @@ def test_trajectories_full_size_c5():
         assert_parity(rep.kept[t], ref.state.amplitudes)
 
 
-def _sharded_gpu_worker(rank, world, port, out):
+def _sharded_gpu_worker(rank, world, port, out, transport):
     import os
 
     import torch
     import torch.distributed as dist
 
-    from paper_2008_07140_b200.distributed import CudaShard, ShardedSimulator
+    from paper_2008_07140_b200.distributed import CudaShard, ShardedSimulator, make_transport
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -260,12 +260,18 @@ def _sharded_gpu_worker(rank, world, port, out):
         for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
             prog = parse_program(text)
             g = world.bit_length() - 1
-            sim = ShardedSimulator(prog.qubit_count, CudaShard(prog.qubit_count - g, 0))
-            sim.set_basis(1)
-            sim.run(prog)
+            shard = CudaShard(prog.qubit_count - g, 0)
+            tr = make_transport(transport, dist, shard)
+            sim = ShardedSimulator(prog.qubit_count, shard, chunk_log2=2, transport=tr)
+            for _ in range(2):  # twice: the second run reuses buffers, handles and plans
+                sim.set_basis(1)
+                sim.run(prog)
             amps = sim.gather_amplitudes()
             if rank == 0:
                 res[name] = (amps, len(sim.stats.swaps))
+            if hasattr(tr, "close"):
+                tr.close()
+            dist.barrier()
             sim.shard.close()
         if rank == 0:
             np.save(out, np.array([res], dtype=object), allow_pickle=True)
@@ -273,11 +279,13 @@ def _sharded_gpu_worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_sharded_path_on_gpu(world, tmp_path):
-    """CudaShard (libqsv on the GPU) + global<->local qubit swaps, P ranks sharing
-    the one GPU of this box; blocks are exchanged over gloo through host memory
-    (no kernel ever waits on another rank)."""
+@pytest.mark.parametrize("world,transport", [(2, "gloo"), (4, "gloo"), (2, "p2p"), (4, "p2p")])
+def test_sharded_path_on_gpu(world, transport, tmp_path):
+    """CudaShard (libqsv on the GPU) + chunked global<->local qubit swaps, P ranks
+    sharing the one GPU of this box.  Blocks travel over gloo through host
+    memory, or as copy-engine pushes into CUDA-IPC-mapped peer buffers ordered
+    by interprocess events (the P2PTransport used over NVLink on a multi-GPU
+    box); no kernel ever waits on another rank."""
     import socket
 
     import torch.multiprocessing as mp
@@ -286,7 +294,7 @@ def test_sharded_path_on_gpu(world, tmp_path):
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     out = str(tmp_path / "sharded.npy")
-    mp.spawn(_sharded_gpu_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_sharded_gpu_worker, args=(world, port, out, transport), nprocs=world, join=True)
     res = np.load(out, allow_pickle=True)[0]
     for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
         prog = parse_program(text)
