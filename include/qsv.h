@@ -188,6 +188,29 @@ int qsv_ipc_mem_close(void *mapped);
 /* asynchronous copy between any two device pointers (UVA; peer pointers go over NVLink) */
 int qsv_copy_async(void *dst, const void *src, uint64_t bytes, void *stream);
 
+/* ---- noisy trajectories on a compiled plan ----
+ * One Pauli error (1 = X, 2 = Y, 3 = Z) on `qubit` acting right BEFORE gate record `gate` of the
+ * plan's gate list (gate == n_gates: after the last gate): the explicit X/Y/Z insertion of a
+ * pre-sampled depolarising trajectory (noise.py:188-222 semantics, workloads.py).  The reference
+ * re-runs every trajectory gate by gate (statevector.py:343-357). */
+typedef struct qsv_pauli {
+    int64_t gate;
+    int32_t qubit;
+    int32_t kind;
+} qsv_pauli;
+/* Runs `plan` with Pauli errors inserted, reusing the plan's compiled pass kernels: every error
+ * is moved to a pass boundary (gates on its qubit that it crosses are replaced by their Pauli
+ * conjugates; the boundary chosen crosses as few passes' gates as possible), applied there as a
+ * Pauli-string kernel, and only passes holding conjugated gates run through the interpreted
+ * kernel.  QSV_E_UNSUPPORTED when the plan relabelled SWAPs or uses super-passes. */
+int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
+                            const qsv_options *opt, qsv_run_stats *stats);
+/* host only (tests): the gate stream such an execution applies, in execution order - boundary
+ * strings as Z, X gates and a phase, then each pass's (conjugated) gates.  *n_out = records
+ * written (at most cap), *n_modified = passes that would run interpreted. */
+int qsv_plan_pauli_stream(const qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis, qsv_gate *out,
+                          int64_t cap, int64_t *n_out, int64_t *n_modified);
+
 /* ---- readout (synchronous) ---- */
 int qsv_norm_sq(qsv_state *st, double *out);
 int qsv_prob_bit0(qsv_state *st, int k, double *out);

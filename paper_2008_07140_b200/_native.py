@@ -17,11 +17,16 @@ from .errors import NativeLibraryMissing, raise_for_status
 LIB_PATH = Path(__file__).resolve().parent / "libqsv.so"
 
 QSV_OP_MAT1, QSV_OP_MAT2, QSV_OP_DIAG1, QSV_OP_DIAG2 = 1, 2, 3, 4
+QSV_E_UNSUPPORTED = -6  # qsv.h
 
 # numpy mirror of `qsv_gate` (C layout: int32 n_targets, int32 targets[2],
 # uint64 control_mask, double u[32]) - built in bulk from a Program
 GATE_DTYPE = np.dtype([("n_targets", "<i4"), ("targets", "<i4", (2,)),
                        ("control_mask", "<u8"), ("u", "<f8", (32,))], align=True)
+
+
+# one Pauli error before gate record `gate` (qsv.h qsv_pauli): kind 1 X, 2 Y, 3 Z
+PAULI_DTYPE = np.dtype([("gate", "<i8"), ("qubit", "<i4"), ("kind", "<i4")], align=True)
 
 
 class qsv_options(C.Structure):
@@ -96,6 +101,9 @@ _SIGNATURES = {
     "qsv_ipc_mem_open": ([_P, C.c_uint64, C.c_int, C.POINTER(_P)], C.c_int),
     "qsv_ipc_mem_close": ([_P], C.c_int),
     "qsv_copy_async": ([_P, _P, C.c_uint64, _P], C.c_int),
+    "qsv_plan_execute_paulis": ([_P, _P, _P, C.c_int64, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),
+    "qsv_plan_pauli_stream": ([_P, _P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
+                              C.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)

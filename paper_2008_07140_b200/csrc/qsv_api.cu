@@ -772,6 +772,265 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     return execute_plan(st, P, dp, ds, dop, opt, stats);
 }
 
+// ---- noisy trajectories on a compiled plan -----------------------------------
+struct PauliString {
+    cd phase{1.0, 0.0};
+    uint64_t x = 0, z = 0;
+    bool any = false;
+    // left-multiply by a Pauli on q (it acts after the current string)
+    void push(int q, int kind) {
+        const uint64_t b = 1ull << q;
+        any = true;
+        if (kind == 3 || kind == 2) {  // Z_q X^x Z^z = (-1)^{x_q} X^x Z_q Z^z
+            if (x & b) phase = -phase;
+            z ^= b;
+        }
+        if (kind == 1 || kind == 2) x ^= b;       // X_q X^x = X^{x^q}
+        if (kind == 2) phase *= cd(0.0, 1.0);     // Y = i X Z
+    }
+};
+
+struct PauliPlacement {
+    std::vector<GateRec> recs;
+    std::vector<char> modified;
+    std::vector<PauliString> bnd;  // one per pass boundary (+ the end)
+};
+
+int place_paulis(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &out, std::string &msg) {
+    const int np = (int)P.passes.size();
+    if (P.relabelled || (int)P.pass_gates.size() != np || use_supers(P)) {
+        msg = "plan relabels SWAPs or uses super-passes";
+        return QSV_E_UNSUPPORTED;
+    }
+    const int64_t G = (int64_t)P.recs.size();
+    out.recs = P.recs;
+    out.modified.assign(np, 0);
+    out.bnd.assign(np + 1, PauliString{});
+    std::vector<int> gpass(G, -1);
+    for (int j = 0; j < np; ++j)
+        for (int gi : P.pass_gates[j]) gpass[gi] = j;
+    std::vector<std::vector<int>> onq(P.n);
+    for (int64_t k = 0; k < G; ++k)
+        for (int q = 0; q < P.n; ++q)
+            if (((P.recs[k].nmask | P.recs[k].dmask) >> q) & 1) onq[q].push_back((int)k);
+    std::vector<int64_t> order(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (pa[i].gate < 0 || pa[i].gate > G || pa[i].qubit < 0 || pa[i].qubit >= P.n || pa[i].kind < 1 ||
+            pa[i].kind > 3) {
+            msg = "Pauli error " + std::to_string(i) + " out of range";
+            return QSV_E_PARSE;
+        }
+        order[i] = i;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return pa[a].gate < pa[b].gate; });
+    std::vector<int> chosen(n, 0);
+    std::vector<char> seen(np);
+    for (int64_t idx : order) {
+        const int q = pa[idx].qubit, kind = pa[idx].kind;
+        const int64_t g = pa[idx].gate;
+        const int home = g < G ? gpass[g] : np;
+        int best = -1;
+        long best_key[3] = {0, 0, 0};
+        for (int b = 0; b <= np; ++b) {
+            std::fill(seen.begin(), seen.end(), 0);
+            long new_mod = 0, crossed = 0;
+            bool ok = true;
+            for (int k : onq[q]) {
+                if ((k >= g) == (gpass[k] >= b)) continue;
+                ++crossed;
+                if (!can_conjugate_pauli(out.recs[k], q, kind)) ok = false;
+                if (!out.modified[gpass[k]] && !seen[gpass[k]]) {
+                    seen[gpass[k]] = 1;
+                    ++new_mod;
+                }
+            }
+            if (!ok) continue;
+            const long key[3] = {new_mod, crossed, std::labs((long)(b - home))};
+            if (best < 0 || std::lexicographical_compare(key, key + 3, best_key, best_key + 3)) {
+                best = b;
+                std::copy(key, key + 3, best_key);
+            }
+        }
+        if (best < 0) {
+            msg = "Pauli error cannot be moved to a pass boundary (crosses a gate controlled by its qubit)";
+            return QSV_E_UNSUPPORTED;
+        }
+        for (int k : onq[q])
+            if ((k >= g) != (gpass[k] >= best)) {
+                conjugate_pauli(out.recs[k], q, kind);
+                out.modified[gpass[k]] = 1;
+            }
+        out.bnd[best].push(q, kind);
+        chosen[idx] = best;
+    }
+    // two errors on one qubit whose order flipped: X, Y, Z anticommute pairwise
+    bool neg = false;
+    for (int64_t a = 0; a < n; ++a)
+        for (int64_t b = a + 1; b < n; ++b) {
+            const int64_t i = order[a], j = order[b];
+            if (pa[i].qubit == pa[j].qubit && pa[i].kind != pa[j].kind && chosen[i] > chosen[j]) neg = !neg;
+        }
+    if (neg) {
+        out.bnd[np].phase = -out.bnd[np].phase;
+        out.bnd[np].any = true;
+    }
+    return QSV_OK;
+}
+
+int launch_pauli(qsv_state *st, const PauliString &ps) {
+    if (!ps.any) return QSV_OK;
+    const int rc = materialize(st);
+    if (rc) return rc;
+    pauli_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(st->amps, st->size(), ps.x, ps.z,
+                                                                                ps.phase.real(), ps.phase.imag());
+    CUDA_TRY(cudaGetLastError());
+    return QSV_OK;
+}
+
+int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
+                            const qsv_options *opt, qsv_run_stats *stats) {
+    if (n_paulis <= 0) return qsv_plan_execute(st, plan, opt, stats);
+    Plan &P = plan->p;
+    if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    PauliPlacement pl;
+    std::string msg;
+    rc = place_paulis(P, paulis, n_paulis, pl, msg);
+    if (rc) return fail(rc, msg);
+    rc = jit_prepare(P, st->device, msg);
+    if (rc) return fail(rc, msg);
+    const std::vector<double> &sc = pass_scales(P);
+    const int np = (int)P.passes.size();
+    LaunchTimer tm;
+    tm.on = opt && opt->profile;
+    tm.s = st->stream;
+    int64_t launches = 0, interpreted = 0;
+    for (int j = 0; j <= np; ++j) {
+        if (pl.bnd[j].any) {
+            tm.begin();
+            rc = launch_pauli(st, pl.bnd[j]);
+            tm.end();
+            if (rc) return rc;
+            ++launches;
+        }
+        if (j == np) break;
+        tm.begin();
+        if (!pl.modified[j]) {
+            const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+            rc = jit_launch(P, j, st->amps, st->n, st->stream, msg, basis);
+            if (rc) return fail(rc, msg);
+            st->pending_basis = -1;
+        } else {
+            rc = materialize(st);
+            if (rc) return rc;
+            // the interpreted pass sees the state as the compiled pass j would
+            // (stored = true / sc[j]) and must leave it as pass j+1 expects
+            std::vector<GateRec> recs = pl.recs;
+            std::vector<int32_t> taken = P.pass_gates[j];
+            const double f = sc[j] / sc[j + 1];
+            if (f != 1.0) {
+                GateRec s;
+                s.nt = 1;
+                s.t[0] = P.passes[j].tq[0];
+                for (int k = 0; k < 16; ++k) s.u[k] = 0;
+                s.u[0] = s.u[3] = f;
+                s.diag = true;
+                s.dmask = 1ull << s.t[0];
+                recs.push_back(s);
+                taken.push_back((int32_t)recs.size() - 1);
+            }
+            Plan Q = build_single_pass(recs, taken, P.passes[j].tile_mask, P.n, P.m, std::min(P.r, 4), P.L);
+            const size_t bytes = plan_bytes(Q);
+            if (st->plan_buf_bytes < bytes) {
+                if (st->plan_buf) {
+                    CUDA_TRY(cudaStreamSynchronize(st->stream));
+                    cudaFree(st->plan_buf);
+                }
+                st->plan_buf = nullptr;
+                st->plan_buf_bytes = 0;
+                CUDA_TRY(cudaMalloc(&st->plan_buf, bytes));
+                st->plan_buf_bytes = bytes;
+            }
+            DevPass *dp;
+            DevStage *ds;
+            DevOp *dop;
+            rc = upload_plan(st, Q, st->plan_buf, &dp, &ds, &dop);
+            if (!rc) rc = launch_pass(st, Q, 0, dp, ds, dop);
+            if (rc) return rc;
+            ++interpreted;
+        }
+        tm.end();
+        ++launches;
+    }
+    tm.collect(stats);
+    if (stats) {
+        stats->gates += P.gates + n_paulis;
+        stats->passes += launches;
+        stats->inner_passes += np;
+        stats->stages += (int64_t)P.stages.size();
+        stats->launches += launches;
+        stats->algorithmic_bytes += (double)launches * 32.0 * (double)st->size();
+    }
+    (void)interpreted;
+    return QSV_OK;
+}
+
+int qsv_plan_pauli_stream(const qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis, qsv_gate *out,
+                          int64_t cap, int64_t *n_out, int64_t *n_modified) {
+    const Plan &P = plan->p;
+    PauliPlacement pl;
+    std::string msg;
+    const int rc = place_paulis(P, paulis, n_paulis, pl, msg);
+    if (rc) return fail(rc, msg);
+    int64_t w = 0;
+    auto put = [&](const GateRec &g) {
+        if (w < cap) {
+            qsv_gate &o = out[w];
+            std::memset(&o, 0, sizeof(o));
+            o.n_targets = g.nt;
+            o.targets[0] = g.t[0];
+            o.targets[1] = g.nt == 2 ? g.t[1] : 0;
+            o.control_mask = g.cmask;
+            const int d = 1 << g.nt;
+            for (int k = 0; k < d * d; ++k) {
+                o.u[2 * k] = g.u[k].real();
+                o.u[2 * k + 1] = g.u[k].imag();
+            }
+        }
+        ++w;
+    };
+    auto one = [&](int q, cd a, cd b, cd c, cd d) {
+        GateRec g;
+        g.nt = 1;
+        g.t[0] = q;
+        for (int k = 0; k < 16; ++k) g.u[k] = 0;
+        g.u[0] = a;
+        g.u[1] = b;
+        g.u[2] = c;
+        g.u[3] = d;
+        put(g);
+    };
+    const int np = (int)P.passes.size();
+    for (int j = 0; j <= np; ++j) {
+        const PauliString &ps = pl.bnd[j];
+        if (ps.any) {
+            for (int q = 0; q < P.n; ++q)
+                if ((ps.z >> q) & 1) one(q, 1, 0, 0, -1);
+            for (int q = 0; q < P.n; ++q)
+                if ((ps.x >> q) & 1) one(q, 0, 1, 1, 0);
+            if (ps.phase != cd(1, 0)) one(0, ps.phase, 0, 0, ps.phase);
+        }
+        if (j < np)
+            for (int gi : P.pass_gates[j]) put(pl.recs[gi]);
+    }
+    *n_out = w;
+    int64_t mods = 0;
+    for (char m : pl.modified) mods += m;
+    *n_modified = mods;
+    return QSV_OK;
+}
+
 int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *buf, int64_t buf_size, int64_t *needed) {
     const Plan &P = plan->p;
     if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
@@ -889,7 +1148,18 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
     CUDA_TRY(cudaMallocAsync(&d_q, sizeof(int) * m, st->stream));
     CUDA_TRY(cudaMemcpyAsync(d_q, qubits, sizeof(int) * m, cudaMemcpyHostToDevice, st->stream));
     CUDA_TRY(cudaMallocAsync(&d_table, sizeof(double) * bins, st->stream));
-    if (m <= kPmeasureSmallBits) {
+    if (m <= 4) {
+        const int blocks = 148 * 4;
+        rc = ensure_work(st, sizeof(double) * bins * blocks);
+        if (rc) return rc;
+        switch (m) {
+            case 1: pmeasure_small_kernel<1><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
+            case 2: pmeasure_small_kernel<2><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
+            case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
+            default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
+        }
+        pmeasure_finish<<<1, 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
+    } else if (m <= kPmeasureSmallBits) {
         const int blocks = 148 * 2;
         rc = ensure_work(st, sizeof(double) * bins * blocks);
         if (rc) return rc;

@@ -53,6 +53,10 @@ bool jit_double_buffer();
 // true when the plan's super-passes run as L2-resident persistent kernels
 bool use_supers(const Plan &P);
 
+// The uniform scale every pass's specialised kernel expects the stored state
+// to carry (stored = true / scale); entry passes.size() is the plan's output (1).
+const std::vector<double> &pass_scales(const Plan &P);
+
 // Launches pass `pass` of a prepared plan over the whole state.  `basis` !=
 // ~0 means the state is the basis state |basis> and is not read (single-buffer
 // kernels synthesise the tiles; see jit_basis_fusable).

@@ -544,6 +544,62 @@ __global__ void __launch_bounds__(256) pmeasure_kernel(const double2 *__restrict
     for (int b = threadIdx.x; b < bins; b += blockDim.x) partial[(size_t)blockIdx.x * bins + b] = hist[b];
 }
 
+// small tables (<= 16 bins): per-thread register bins (no shared-memory
+// atomics on a handful of addresses), fixed-order block and grid sums
+template <int M>
+__global__ void __launch_bounds__(256) pmeasure_small_kernel(const double2 *__restrict__ psi, uint64_t size,
+                                                             const int *__restrict__ qubits, double *partial) {
+    constexpr int B = 1 << M;
+    double acc[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) acc[b] = 0.0;
+    int q[M];
+#pragma unroll
+    for (int p = 0; p < M; ++p) q[p] = qubits[p];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        const double2 x = psi[i];
+        const double pr = fma(x.x, x.x, x.y * x.y);
+        uint32_t key = 0;
+#pragma unroll
+        for (int p = 0; p < M; ++p) key |= (uint32_t)((i >> q[p]) & 1) << (M - 1 - p);
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] += key == (uint32_t)b ? pr : 0.0;
+    }
+    __shared__ double red[B][256 / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        double v = acc[b];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) red[b][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < B) {
+        double s = 0.0;
+        for (int w = 0; w < 256 / 32; ++w) s += red[threadIdx.x][w];
+        partial[(size_t)blockIdx.x * B + threadIdx.x] = s;
+    }
+}
+
+// Pauli string phase * X^x Z^z (Z first): out[i] = phase * (-1)^popc((i^x)&z) * in[i^x],
+// in place over pairs {i, i^x} (noisy trajectories: errors moved to pass boundaries)
+__global__ void pauli_kernel(double2 *__restrict__ psi, uint64_t size, uint64_t x, uint64_t z, double pre,
+                             double pim) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t hi = x ? (1ull << (63 - __clzll((long long)x))) : 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        if (x && (i & hi)) continue;  // the partner handles the pair
+        const uint64_t j = i ^ x;
+        const double2 a = psi[i], b = psi[j];
+        const double si = (__popcll(i & z) & 1) ? -1.0 : 1.0, sj = (__popcll(j & z) & 1) ? -1.0 : 1.0;
+        // out[i] = phase * s(j) * in[j]; out[j] = phase * s(i) * in[i]
+        const double2 bi = make_double2(sj * b.x, sj * b.y), aj = make_double2(si * a.x, si * a.y);
+        psi[i] = make_double2(pre * bi.x - pim * bi.y, pre * bi.y + pim * bi.x);
+        if (x) psi[j] = make_double2(pre * aj.x - pim * aj.y, pre * aj.y + pim * aj.x);
+    }
+}
+
 __global__ void pmeasure_finish(const double *partial, int n_blocks, int bins, double *table) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= bins) return;

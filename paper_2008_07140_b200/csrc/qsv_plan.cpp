@@ -675,6 +675,101 @@ int plan_segments(const std::vector<GateRec> &recs, int n, int capacity, uint64_
     return QSV_OK;
 }
 
+Plan build_single_pass(const std::vector<GateRec> &recs, const std::vector<int32_t> &taken, uint64_t tile_mask, int n,
+                       int m, int r, int L) {
+    Plan Q;
+    Q.recs = recs;
+    Q.n = n;
+    Q.m = m;
+    Q.r = r;
+    Q.L = L;
+    Q.s = m;
+    Q.gates = (int64_t)taken.size();
+    const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
+    SuperPass sp;
+    sp.mask = tile_mask;
+    sp.pass_begin = 0;
+    emit_pass(Q, recs, std::vector<int>(taken.begin(), taken.end()), tile_mask, all);
+    sp.pass_end = 1;
+    Q.supers.push_back(sp);
+    Q.pass_gates.push_back(taken);
+    Q.pass_op_begin.push_back((int64_t)Q.ops.size());
+    return Q;
+}
+
+namespace {
+void pauli2(int kind, cd *p) {
+    const cd z(0, 0), one(1, 0), I(0, 1);
+    if (kind == 1) { p[0] = z; p[1] = one; p[2] = one; p[3] = z; }
+    else if (kind == 2) { p[0] = z; p[1] = -I; p[2] = I; p[3] = z; }
+    else { p[0] = one; p[1] = z; p[2] = z; p[3] = -one; }
+}
+}  // namespace
+
+bool can_conjugate_pauli(const GateRec &g, int q, int kind) {
+    if (!((g.cmask >> q) & 1) || kind == 3) return true;  // targets always; Z commutes with a control
+    return g.diag && g.nt == 1 && popc(g.cmask) == 1;    // C-diag(d0,d1) -> diag over (q, t) with q flipped
+}
+
+void conjugate_pauli(GateRec &g, int q, int kind) {
+    if ((g.cmask >> q) & 1) {
+        if (kind == 3) return;
+        // X_q C_q-D X_q = D applied where q = 0: a 2-qubit diagonal over (q, t)
+        const cd d0 = g.u[0], d1 = g.u[3];
+        GateRec h;
+        h.nt = 2;
+        h.t[0] = q;
+        h.t[1] = g.t[0];
+        for (int k = 0; k < 16; ++k) h.u[k] = 0;
+        h.u[0] = d0;
+        h.u[5] = d1;
+        h.u[10] = h.u[15] = 1;
+        h.cmask = 0;
+        h.diag = true;
+        h.nmask = 0;
+        h.dmask = (1ull << q) | (1ull << g.t[0]);
+        g = h;
+        return;
+    }
+    int pos = -1;
+    for (int k = 0; k < g.nt; ++k)
+        if (g.t[k] == q) pos = k;
+    if (pos < 0) return;
+    cd p[4];
+    pauli2(kind, p);
+    const int d = 1 << g.nt;
+    // full Pauli on the gate's index space: bit (nt-1-pos) of the row/column index
+    const int bit = g.nt - 1 - pos;
+    auto P = [&](int r, int c) -> cd {
+        if ((r & ~(1 << bit)) != (c & ~(1 << bit))) return cd(0, 0);
+        return p[2 * ((r >> bit) & 1) + ((c >> bit) & 1)];
+    };
+    cd t[16], u2[16];
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            cd s(0, 0);
+            for (int k = 0; k < d; ++k) s += g.u[r * d + k] * P(k, c);
+            t[r * d + c] = s;
+        }
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            cd s(0, 0);
+            for (int k = 0; k < d; ++k) s += P(r, k) * t[k * d + c];
+            u2[r * d + c] = s;
+        }
+    bool diag = true;
+    for (int r = 0; r < d; ++r)
+        for (int c = 0; c < d; ++c) {
+            g.u[r * d + c] = u2[r * d + c];
+            if (r != c && u2[r * d + c] != cd(0, 0)) diag = false;
+        }
+    uint64_t tmask = 0;
+    for (int k = 0; k < g.nt; ++k) tmask |= 1ull << g.t[k];
+    g.diag = diag;
+    g.nmask = diag ? 0 : tmask;
+    g.dmask = g.cmask | (diag ? tmask : 0);
+}
+
 // Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy
 // absorption with capacity s); its gates are then split into ordinary passes
 // whose tiles lie inside S.  The executor runs all inner passes of a
@@ -694,6 +789,7 @@ Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L,
     P.s = std::max(m, std::min(s, n));
     P.gates = (int64_t)recs_in.size();
     const std::vector<GateRec> recs = relabel_swaps(recs_in, n);
+    P.relabelled = recs.size() != recs_in.size();
     const uint64_t low = L > 0 ? ((1ull << L) - 1) : 0;
     const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
 
@@ -730,6 +826,7 @@ Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L,
             spp.mask = padded_tile(pass_res[k], all, n, m);
             spp.pass_begin = (int32_t)P.passes.size();
             emit_pass(P, recs, pass_gates[k], pass_res[k], all);
+            P.pass_gates.emplace_back(pass_gates[k].begin(), pass_gates[k].end());
             spp.pass_end = (int32_t)P.passes.size();
             P.supers.push_back(spp);
         }
@@ -764,7 +861,10 @@ Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L,
         }
         balance_passes(recs, pass_gates, pass_res, smask, n, m);
         for (size_t k = 0; k < pass_gates.size(); ++k)
-            if (!pass_gates[k].empty()) emit_pass(P, recs, pass_gates[k], pass_res[k], smask);
+            if (!pass_gates[k].empty()) {
+                emit_pass(P, recs, pass_gates[k], pass_res[k], smask);
+                P.pass_gates.emplace_back(pass_gates[k].begin(), pass_gates[k].end());
+            }
         spp.pass_end = (int32_t)P.passes.size();
         P.supers.push_back(spp);
         remaining.swap(s_def);

@@ -114,6 +114,8 @@ struct Plan {
     std::vector<GlobalOp> gops;           // every op in global-qubit terms
     std::vector<uint64_t> stage_regs;     // global register-qubit mask per stage
     std::vector<int64_t> pass_op_begin;   // first op of every pass (+ sentinel)
+    std::vector<std::vector<int32_t>> pass_gates;  // gate records (indices into recs) of every pass, in order
+    bool relabelled = false;              // SWAPs were folded into a qubit relabelling (indices shifted)
     // device copies (owned by the launcher, lazily uploaded)
     void *d_passes = nullptr, *d_stages = nullptr, *d_ops = nullptr;
     int device = -1;
@@ -136,6 +138,18 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector
 
 // Builds the fused schedule.  m, r, L already clamped to the state size.
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s);
+
+// One pass over `tile_mask` applying recs[taken] (program order) with r
+// register qubits: the interpreted kernel's tables for a pass whose gates
+// differ from a compiled plan's (noisy trajectories, qsv_plan_execute_paulis).
+Plan build_single_pass(const std::vector<GateRec> &recs, const std::vector<int32_t> &taken, uint64_t tile_mask, int n,
+                       int m, int r, int L);
+
+// P U P for a Pauli (1 X, 2 Y, 3 Z) on qubit q: gate g as seen when the Pauli is
+// moved across it.  False when the result is no gate record (a non-diagonal
+// gate, or a multi-controlled one, controlled by q, conjugated by X or Y).
+bool can_conjugate_pauli(const GateRec &g, int q, int kind);
+void conjugate_pauli(GateRec &g, int q, int kind);
 
 // SWAP gates folded into a logical->physical qubit map (see qsv_plan.cpp).
 std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &recs, int n);

@@ -7,11 +7,16 @@ statevector.py:343-357 + noise.py:188-222) with the Pauli branch of every
 and inserted as explicit X/Y/Z gates before that gate, so each trajectory is a
 noiseless program run by the fused engine.
 
-Execution on one GPU: one device state is reused for all trajectories;
-trajectories without an error share one program, hence one plan whose
-specialised kernels are compiled once (cache by source); trajectories with
-errors each have a distinct gate list and run through the interpreted fused
-kernel (no per-trajectory NVRTC compile).  With `dedup=True` the error-free
+Execution on one GPU: one device state is reused for all trajectories, and
+ALL of them run on the clean circuit's plan, whose specialised kernels are
+compiled once: a trajectory's errors go to libqsv as (gate, qubit, Pauli)
+triples (`qsv_plan_execute_paulis`), which moves each error to a pass
+boundary (conjugating the gates on its qubit that it crosses), applies it
+there as a Pauli-string kernel, and runs only the (typically one) pass holding
+conjugated gates through the interpreted kernel - no per-trajectory NVRTC
+compile, no per-trajectory re-planning.  Plans the Pauli path cannot take
+(SWAP relabelling, super-passes, errors that would cross a gate controlled by
+their qubit) fall back to running the noisy program itself.  With `dedup=True` the error-free
 trajectories are simulated once and the result reused - reported separately
 (`TrajectoryReport.unique_runs`).  Across GPUs trajectories are independent
 replicas: rank r takes t = r, r+P, ... and results are gathered on rank 0.
@@ -58,6 +63,10 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     opts_noisy = N.options(fuse=True, jit=-1, tile_qubits=opts_clean.tile_qubits,
                            reg_qubits=opts_clean.reg_qubits, low_qubits=opts_clean.low_qubits)
     clean_gates = [i for i in program.instructions if i.is_gate]
+    gate_index = {}
+    for j, inst in enumerate(program.instructions):
+        if inst.is_gate:
+            gate_index[j] = len(gate_index)
     clean_rec = SV.compile_gates(clean_gates)
     clean_plan = C.c_void_p()
     N.check(L.qsv_plan_create(clean_rec.ctypes.data, len(clean_rec), n, C.byref(opts_clean),
@@ -85,9 +94,19 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             if n_err == 0:
                 N.check(L.qsv_plan_execute(state.handle, clean_plan, C.byref(opts_clean), C.byref(stats)))
             else:
-                noisy = noisy_trajectory_program(program, p, seed)
-                rec = SV.compile_gates([i for i in noisy.instructions if i.is_gate])
-                N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats)))
+                pa = np.zeros(n_err, dtype=N.PAULI_DTYPE)
+                k2 = 0
+                for idx, picks in ins.items():
+                    for q, g in picks:
+                        pa[k2] = (gate_index[idx], q, "IXYZ".index(g))
+                        k2 += 1
+                rc = L.qsv_plan_execute_paulis(state.handle, clean_plan, pa.ctypes.data, n_err, C.byref(opts_clean),
+                                               C.byref(stats))
+                if rc == N.QSV_E_UNSUPPORTED:
+                    noisy = noisy_trajectory_program(program, p, seed)
+                    rec = SV.compile_gates([i for i in noisy.instructions if i.is_gate])
+                    rc = L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats))
+                N.check(rc)
             unique += 1
             tables[k] = SV.pmeasure(state, pq)
             norms[k] = state.norm_sq()

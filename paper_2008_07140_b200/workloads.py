@@ -95,6 +95,35 @@ def _depolarizing_weights(p: float) -> list[float]:
     return [x * x for x in c]
 
 
+_DRAW_PLANS: dict = {}
+
+
+def _draw_plan(program):
+    """Per program (cached): for every random draw of a trajectory, the
+    instruction index and its qubits (controls + targets), None for MEASURE."""
+    key = id(program)
+    hit = _DRAW_PLANS.get(key)
+    if hit is not None and hit[0] is program:
+        return hit[1]
+    from . import gates
+
+    plan = []
+    for idx, inst in enumerate(program.instructions):
+        if inst.name == "MEASURE":
+            plan.append((idx, None))
+            continue
+        if not inst.is_gate:
+            continue
+        _, targets, controls = gates.controlled_form(inst)
+        qubits = tuple(controls) + tuple(targets)
+        if len(qubits) <= 2:
+            plan.append((idx, qubits))
+    if len(_DRAW_PLANS) > 64:
+        _DRAW_PLANS.clear()
+    _DRAW_PLANS[key] = (program, plan)
+    return plan
+
+
 def sample_pauli_insertions(program, p: float, seed: int):
     """Replay the reference trajectory draw rule on the host.
 
@@ -104,40 +133,35 @@ def sample_pauli_insertions(program, p: float, seed: int):
     set K_a (x) M_b with index a*4+b, K_a acting on the first qubit of
     controls+targets (`noise.py:77-79`, `statevector.py:347-356`).  MEASURE
     consumes one draw too (`statevector.py:304`).  Returns {instruction index:
-    [(qubit, pauli), ...]} for non-identity branches.
+    [(qubit, pauli), ...]} for non-identity branches.  All draws of a
+    trajectory come from one `rng.random(k)` call (the same stream as k
+    scalar calls); the cumulative weights are summed left to right as the
+    reference loop does.
     """
-    from . import gates
-
     w1 = _depolarizing_weights(p)
     w2 = [a * b for a in w1 for b in w1]
-    rng = np.random.default_rng(seed)
+    plan = _draw_plan(program)
+    draws = np.random.default_rng(seed).random(len(plan))
     out = {}
-    for idx, inst in enumerate(program.instructions):
-        if inst.name == "MEASURE":
-            rng.random()
+    for w, nq in ((w1, 1), (w2, 2)):
+        acc, run = [], 0.0
+        for wi in w:
+            run += wi
+            acc.append(run)
+        sel = [k for k, (_, qs) in enumerate(plan) if qs is not None and len(qs) == nq]
+        if not sel:
             continue
-        if not inst.is_gate:
-            continue
-        _, targets, controls = gates.controlled_form(inst)
-        qubits = tuple(controls) + tuple(targets)
-        if len(qubits) > 2:
-            continue
-        w = w1 if len(qubits) == 1 else w2
-        r = rng.random() * sum(w)
-        acc, choice = 0.0, len(w) - 1
-        for i, wi in enumerate(w):
-            acc += wi
-            if r < acc:
-                choice = i
-                break
-        if len(qubits) == 1:
-            picks = [(qubits[0], _PAULI[choice])]
-        else:
-            picks = [(qubits[0], _PAULI[choice // 4]), (qubits[1], _PAULI[choice % 4])]
-        picks = [(q, g) for q, g in picks if g != "I"]
-        if picks:
-            out[idx] = picks
-    return out
+        r = draws[sel] * sum(w)
+        # first branch with r < acc[i] (the last one if none)
+        choice = np.minimum(np.searchsorted(np.asarray(acc), r, side="right"), len(w) - 1)
+        for k in np.nonzero(choice)[0]:
+            idx, qs = plan[sel[k]]
+            c = int(choice[k])
+            picks = [(qs[0], _PAULI[c])] if nq == 1 else [(qs[0], _PAULI[c // 4]), (qs[1], _PAULI[c % 4])]
+            picks = [(q, g) for q, g in picks if g != "I"]
+            if picks:
+                out[idx] = picks
+    return dict(sorted(out.items()))
 
 
 def noisy_trajectory_program(program, p: float, seed: int):
