@@ -218,6 +218,10 @@ int qsv_collapse(qsv_state *st, int k, int outcome, double scale);
 int qsv_scale(qsv_state *st, double scale);
 int qsv_pmeasure(qsv_state *st, const int32_t *qubits_msb_first, int m, double *table);
 int qsv_inner(qsv_state *st, const void *other_device_c128, double *re, double *im);
+/* asynchronous probe table (1..4 qubits, first listed = MSB) written to DEVICE memory on the
+ * state's stream: batched trajectories read their tables once at the end (noise.py:173-185 /
+ * statevector.py:311-328 semantics) */
+int qsv_pmeasure_async(qsv_state *st, const int32_t *qubits_msb_first, int m, double *device_table);
 int qsv_max_abs_diff(qsv_state *st, const void *other_device_c128, double *out);
 /* reduced density matrix of 1 or 2 qubits (first listed = MSB), row-major complex
  * 2^nq x 2^nq; branch weights ||K psi||^2 = tr(K rho K^dag) (noise.py:173-185) */

@@ -88,6 +88,7 @@ _SIGNATURES = {
     "qsv_collapse": ([_P, C.c_int, C.c_int, C.c_double], C.c_int),
     "qsv_scale": ([_P, C.c_double], C.c_int),
     "qsv_pmeasure": ([_P, _P, C.c_int, _P], C.c_int),
+    "qsv_pmeasure_async": ([_P, _P, C.c_int, _P], C.c_int),
     "qsv_inner": ([_P, _P, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "qsv_max_abs_diff": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),

@@ -1143,26 +1143,27 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
     rc = materialize(st);
     if (rc) return rc;
     const size_t bins = (size_t)1 << m;
-    int *d_q = nullptr;
-    double *d_table = nullptr;
-    CUDA_TRY(cudaMallocAsync(&d_q, sizeof(int) * m, st->stream));
+    // one persistent scratch (no per-call stream-ordered allocation: the
+    // default pool releases memory at every synchronisation):
+    // [partials (blocks x bins) | table (bins) | qubit list]
+    const int blocks = m <= 4 ? 148 * 4 : 148 * 2;
+    const size_t n_part = m <= kPmeasureSmallBits ? bins * blocks : 0;
+    rc = ensure_work(st, sizeof(double) * (n_part + bins) + sizeof(int) * 64);
+    if (rc) return rc;
+    double *d_table = st->work + n_part;
+    int *d_q = (int *)(d_table + bins);
     CUDA_TRY(cudaMemcpyAsync(d_q, qubits, sizeof(int) * m, cudaMemcpyHostToDevice, st->stream));
-    CUDA_TRY(cudaMallocAsync(&d_table, sizeof(double) * bins, st->stream));
     if (m <= 4) {
-        const int blocks = 148 * 4;
-        rc = ensure_work(st, sizeof(double) * bins * blocks);
-        if (rc) return rc;
+        QubitList ql;
+        for (int p = 0; p < m; ++p) ql.q[p] = qubits[p];
         switch (m) {
-            case 1: pmeasure_small_kernel<1><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
-            case 2: pmeasure_small_kernel<2><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
-            case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
-            default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), d_q, st->work); break;
+            case 1: pmeasure_small_kernel<1><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+            case 2: pmeasure_small_kernel<2><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+            case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+            default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
         }
         pmeasure_finish<<<1, 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
     } else if (m <= kPmeasureSmallBits) {
-        const int blocks = 148 * 2;
-        rc = ensure_work(st, sizeof(double) * bins * blocks);
-        if (rc) return rc;
         pmeasure_kernel<<<blocks, 256, sizeof(double) * bins, st->stream>>>(st->amps, st->size(), m, d_q, st->work);
         pmeasure_finish<<<(unsigned)((bins + 255) / 256), 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
     } else {
@@ -1172,9 +1173,34 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
     }
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(table, d_table, sizeof(double) * bins, cudaMemcpyDeviceToHost, st->stream));
-    CUDA_TRY(cudaFreeAsync(d_q, st->stream));
-    CUDA_TRY(cudaFreeAsync(d_table, st->stream));
     CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_pmeasure_async(qsv_state *st, const int32_t *qubits, int m, double *device_table) {
+    if (m < 1 || m > 4) return fail(QSV_E_UNSUPPORTED, "asynchronous pmeasure takes 1..4 qubits");
+    for (int p = 0; p < m; ++p)
+        if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "pmeasure qubit out of range");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
+    // one scratch per state: the partials stay valid until the finish kernel
+    // of the same stream consumed them (stream order)
+    const int blocks = 148 * 4;
+    const size_t bins = (size_t)1 << m;
+    rc = ensure_work(st, sizeof(double) * bins * blocks + sizeof(int) * 64);
+    if (rc) return rc;
+    QubitList ql;
+    for (int p = 0; p < m; ++p) ql.q[p] = qubits[p];
+    switch (m) {
+        case 1: pmeasure_small_kernel<1><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+        case 2: pmeasure_small_kernel<2><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+        case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+        default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
+    }
+    pmeasure_finish<<<1, 256, 0, st->stream>>>(st->work, blocks, (int)bins, device_table);
+    CUDA_TRY(cudaGetLastError());
     return QSV_OK;
 }
 

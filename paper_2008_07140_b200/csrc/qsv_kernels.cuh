@@ -546,16 +546,20 @@ __global__ void __launch_bounds__(256) pmeasure_kernel(const double2 *__restrict
 
 // small tables (<= 16 bins): per-thread register bins (no shared-memory
 // atomics on a handful of addresses), fixed-order block and grid sums
+struct QubitList {
+    int q[16];
+};
+
 template <int M>
 __global__ void __launch_bounds__(256) pmeasure_small_kernel(const double2 *__restrict__ psi, uint64_t size,
-                                                             const int *__restrict__ qubits, double *partial) {
+                                                             QubitList qubits, double *partial) {
     constexpr int B = 1 << M;
     double acc[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) acc[b] = 0.0;
     int q[M];
 #pragma unroll
-    for (int p = 0; p < M; ++p) q[p] = qubits[p];
+    for (int p = 0; p < M; ++p) q[p] = qubits.q[p];
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
         const double2 x = psi[i];

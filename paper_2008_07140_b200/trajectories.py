@@ -75,7 +75,15 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     tables = np.zeros((len(mine), 1 << len(pq)))
     norms = np.zeros(len(mine))
     errors, kept = [], {}
-    clean_cache = None
+    clean_cache = None  # (slot of the first simulated clean trajectory)
+    dedup_from = {}     # slot -> slot whose table it reuses
+    # probe tables land in device memory, one row per trajectory, read once at
+    # the end: the host runs ahead of the GPU (no per-trajectory synchronisation)
+    async_tables = len(pq) <= 4
+    if async_tables:
+        import torch
+
+        dev_tables = torch.zeros((max(1, len(mine)), 1 << len(pq)), dtype=torch.float64, device=f"cuda:{device}")
     updates = 0
     unique = 0
     t0 = time.perf_counter()
@@ -87,7 +95,7 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             errors.append(n_err)
             updates += (len(clean_gates) + n_err) << n
             if n_err == 0 and dedup and clean_cache is not None and t not in keep:
-                tables[k], norms[k] = clean_cache
+                dedup_from[k] = clean_cache
                 continue
             state.set_basis(0)
             stats = N.qsv_run_stats()
@@ -108,12 +116,21 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
                     rc = L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats))
                 N.check(rc)
             unique += 1
-            tables[k] = SV.pmeasure(state, pq)
-            norms[k] = state.norm_sq()
+            if async_tables:
+                N.check(L.qsv_pmeasure_async(state.handle, pq.ctypes.data, len(pq),
+                                             C.c_void_p(dev_tables[k].data_ptr())))
+            else:
+                tables[k] = SV.pmeasure(state, pq)
             if t in keep:
                 kept[t] = state.amplitudes
-            if n_err == 0:
-                clean_cache = (tables[k].copy(), norms[k])
+            if n_err == 0 and clean_cache is None:
+                clean_cache = k
+        if async_tables and mine:
+            N.check(L.qsv_synchronize(state.handle))
+            tables[:] = dev_tables.cpu().numpy()[: len(mine)]
+        for k, src in dedup_from.items():
+            tables[k] = tables[src]
+        norms[:] = tables.sum(axis=1)  # the probe table sums to ||psi||^2
     finally:
         L.qsv_plan_destroy(clean_plan)
     return TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
