@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <functional>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -41,6 +44,7 @@ struct Nvrtc {
     nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t *) = nullptr;
     nvrtcResult (*GetCUBIN)(nvrtcProgram, char *) = nullptr;
     nvrtcResult (*DestroyProgram)(nvrtcProgram *) = nullptr;
+    nvrtcResult (*Version)(int *, int *) = nullptr;
 };
 
 struct Driver {
@@ -79,6 +83,7 @@ Nvrtc &nvrtc() {
                  sym(h, "nvrtcGetProgramLog", api.GetProgramLog) && sym(h, "nvrtcGetCUBINSize", api.GetCUBINSize) &&
                  sym(h, "nvrtcGetCUBIN", api.GetCUBIN) && sym(h, "nvrtcDestroyProgram", api.DestroyProgram);
         if (!api.ok) api.why = "libnvrtc lacks a required symbol";
+        sym(h, "nvrtcVersion", api.Version);
     });
     return api;
 }
@@ -1300,6 +1305,72 @@ std::string jit_compile_cubin(const std::string &src, std::string &log) {
 
 namespace {
 
+// On-disk cubin cache: a fresh process (the CLI, a new job) loads the
+// specialised kernels of a circuit it has seen before instead of recompiling
+// them with NVRTC (C2: ~1.4 s of first-call latency).  Key: FNV-1a of the
+// kernel source (which embeds the whole pass) + compile options + NVRTC
+// version.  $QSV_CACHE_DIR (empty or "0": off), else $XDG_CACHE_HOME/qsv,
+// else $HOME/.cache/qsv.  Files are written to a temporary name and renamed.
+std::string disk_cache_path(const std::string &src) {
+    static const std::string dir = [] {
+        const char *e = std::getenv("QSV_CACHE_DIR");
+        if (e) return (std::string(e) == "0") ? std::string() : std::string(e);
+        if (const char *x = std::getenv("XDG_CACHE_HOME")) return std::string(x) + "/qsv";
+        if (const char *h = std::getenv("HOME")) return std::string(h) + "/.cache/qsv";
+        return std::string();
+    }();
+    if (dir.empty()) return {};
+    static const std::string salt = [] {
+        int major = 0, minor = 0;
+        Nvrtc &api = nvrtc();
+        if (api.ok && api.Version) api.Version(&major, &minor);
+        return "sm_100a|lineinfo|xdv|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+    }();
+    uint64_t h = 1469598103934665603ull;
+    for (const std::string *part : {&salt, &src})
+        for (unsigned char c : *part) {
+            h ^= c;
+            h *= 1099511628211ull;
+        }
+    char name[64];
+    std::snprintf(name, sizeof(name), "/%016" PRIx64 "-%zu.cubin", h, src.size());
+    return dir + name;
+}
+
+bool disk_cache_load(const std::string &path, std::string &cubin) {
+    if (path.empty()) return false;
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return false;
+    std::string data((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    if (data.size() < 16) return false;
+    cubin.swap(data);
+    return true;
+}
+
+void disk_cache_store(const std::string &path, const std::string &cubin) {
+    if (path.empty() || cubin.empty()) return;
+    const size_t slash = path.rfind('/');
+    std::string cmd_dir = path.substr(0, slash);
+    // mkdir -p
+    for (size_t at = 1; at <= cmd_dir.size(); ++at)
+        if (at == cmd_dir.size() || cmd_dir[at] == '/') {
+            const std::string d = cmd_dir.substr(0, at);
+            mkdir(d.c_str(), 0755);
+        }
+    const std::string tmp = path + ".tmp" + std::to_string((long)getpid());
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (!f) return;
+        f.write(cubin.data(), (std::streamsize)cubin.size());
+        if (!f) return;
+    }
+    std::rename(tmp.c_str(), path.c_str());
+}
+
+}  // namespace
+
+namespace {
+
 struct CacheEntry {
     CUfunction fn = nullptr;
     int grid = 0;  // persistent grid: resident CTAs per SM x SMs
@@ -1383,6 +1454,8 @@ int jit_prepare(Plan &P, int device, std::string &err) {
             pool.emplace_back([&] {
                 for (size_t k; (k = next.fetch_add(1)) < todo.size();) {
                     Unit &u = units[todo[k]];
+                    const std::string path = disk_cache_path(u.src);
+                    if (disk_cache_load(path, u.cubin)) continue;
                     u.cubin = jit_compile_cubin(u.src, u.log);
                     // a three-CTA register cap that spills (accumulator-heavy
                     // passes, e.g. QFT: 1.2 KB of local memory, +20 % time) is
@@ -1396,6 +1469,7 @@ int jit_prepare(Plan &P, int device, std::string &err) {
                         std::string cubin2 = jit_compile_cubin(src2, log2);
                         if (!cubin2.empty()) u.cubin.swap(cubin2);
                     }
+                    disk_cache_store(path, u.cubin);
                 }
             });
         for (auto &th : pool) th.join();
