@@ -159,6 +159,10 @@ int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_
  * same pass as plain C++ (used by the CPU tests to check the generator) */
 int qsv_plan_kernel_source(const qsv_plan *plan, int64_t pass, int host, char *buf, int64_t buf_size,
                            int64_t *needed);
+/* source of the exchange-out variant of one pass (qsv_run_exchange); host=1 renders it as C++
+ * with signature (double2 *psi, u64 n_tiles, XDst xd) */
+int qsv_plan_exchange_source(const qsv_plan *plan, int64_t pass, int host, uint64_t positions, char *buf,
+                             int64_t buf_size, int64_t *needed);
 /* source of the persistent kernel of one super-pass (all its inner passes on L2-resident
  * super-tiles, grid barrier in between); host=1 renders it as plain C++ */
 int qsv_plan_super_source(const qsv_plan *plan, int64_t super_pass, int host, char *buf, int64_t buf_size,
@@ -185,6 +189,24 @@ int qsv_ipc_mem_handle(void *device_ptr, void *handle64, uint64_t *offset);
 /* maps a peer allocation into this process on `device`; *out = base + offset */
 int qsv_ipc_mem_open(const void *handle64, uint64_t offset, int device, void **out);
 int qsv_ipc_mem_close(void *mapped);
+/* Global<->local qubit swap FUSED into the last pass of a gate run: the run's fused passes execute
+ * as in qsv_run, except that the last one stores every output amplitude straight into the
+ * receive buffer of the rank selected by its bits at `positions` (dst[value], a peer allocation
+ * mapped with qsv_ipc_mem_open, or this rank's own), at the same offset with those bits replaced
+ * by `self_bits` (this rank's global bits deposited at `positions`).  The state buffer itself is
+ * left stale.  QSV_E_UNSUPPORTED when the last pass holds an exchanged position in its tile (the
+ * caller then runs qsv_run and copies). */
+typedef struct qsv_exchange {
+    uint64_t positions;
+    uint64_t self_bits;
+    uint64_t dst[8];
+} qsv_exchange;
+int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
+                     const qsv_exchange *ex, qsv_run_stats *stats);
+/* *out = 1 when qsv_run_exchange can fuse an exchange at `positions` into this run (plans it; the
+ * plan is cached for the following qsv_run_exchange).  Ranks agree collectively before fusing. */
+int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
+                         uint64_t positions, int *out);
 /* asynchronous copy between any two device pointers (UVA; peer pointers go over NVLink) */
 int qsv_copy_async(void *dst, const void *src, uint64_t bytes, void *stream);
 

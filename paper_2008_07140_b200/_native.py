@@ -29,6 +29,10 @@ GATE_DTYPE = np.dtype([("n_targets", "<i4"), ("targets", "<i4", (2,)),
 PAULI_DTYPE = np.dtype([("gate", "<i8"), ("qubit", "<i4"), ("kind", "<i4")], align=True)
 
 
+class qsv_exchange(C.Structure):
+    _fields_ = [("positions", C.c_uint64), ("self_bits", C.c_uint64), ("dst", C.c_uint64 * 8)]
+
+
 class qsv_options(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
@@ -93,6 +97,8 @@ _SIGNATURES = {
     "qsv_max_abs_diff": ([_P, _P, C.POINTER(C.c_double)], C.c_int),
     "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),
     "qsv_plan_kernel_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_plan_exchange_source": ([_P, C.c_int64, C.c_int, C.c_uint64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)],
+                                 C.c_int),
     "qsv_plan_super_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_plan_pass_cost": ([_P, C.c_int64, C.POINTER(C.c_double)], C.c_int),
     "qsv_jit_compile": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int),
@@ -102,6 +108,8 @@ _SIGNATURES = {
     "qsv_ipc_mem_open": ([_P, C.c_uint64, C.c_int, C.POINTER(_P)], C.c_int),
     "qsv_ipc_mem_close": ([_P], C.c_int),
     "qsv_copy_async": ([_P, _P, C.c_uint64, _P], C.c_int),
+    "qsv_exchange_fusable": ([_P, _P, C.c_int64, C.POINTER(qsv_options), C.c_uint64, C.POINTER(C.c_int)], C.c_int),
+    "qsv_run_exchange": ([_P, _P, C.c_int64, C.POINTER(qsv_options), _P, C.POINTER(qsv_run_stats)], C.c_int),
     "qsv_plan_execute_paulis": ([_P, _P, _P, C.c_int64, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),
     "qsv_plan_pauli_stream": ([_P, _P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
                               C.c_int),

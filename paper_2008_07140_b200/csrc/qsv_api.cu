@@ -6,6 +6,7 @@
 #include <map>
 
 #include <algorithm>
+#include <bit>
 #include <cstdio>
 #include <cstring>
 #include <list>
@@ -1028,6 +1029,94 @@ int qsv_plan_pauli_stream(const qsv_plan *plan, const qsv_pauli *paulis, int64_t
     int64_t mods = 0;
     for (char m : pl.modified) mods += m;
     *n_modified = mods;
+    return QSV_OK;
+}
+
+int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
+                         uint64_t positions, int *out) {
+    *out = 0;
+    std::vector<GateRec> recs;
+    std::string msg;
+    int rc = to_records(gates, n_gates, st->n, recs, msg);
+    if (rc) return fail(rc, msg);
+    if (recs.empty() || (opt && !opt->fuse)) return QSV_OK;
+    const int jm = opt ? opt->jit : 0;
+    if (jm < 0 || (jm == 0 && st->n < kJitAutoQubits)) return QSV_OK;
+    std::string why;
+    if (!jit_available(why)) return QSV_OK;
+    int m, r, L, sq;
+    resolve_options(opt, st->n, m, r, L, sq);
+    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, jm, st->device);
+    const Plan &P = cp->plan;
+    *out = !use_supers(P) && !P.passes.empty() && !(P.passes.back().tile_mask & positions);
+    return QSV_OK;
+}
+
+int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
+                     const qsv_exchange *ex, qsv_run_stats *stats) {
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    const int s = std::popcount(ex->positions);
+    if (s < 1 || s > 3 || (ex->positions >> st->n)) return fail(QSV_E_PARSE, "exchange positions: 1..3 local qubits");
+    std::vector<GateRec> recs;
+    std::string msg;
+    rc = to_records(gates, n_gates, st->n, recs, msg);
+    if (rc) return fail(rc, msg);
+    if (recs.empty() || (opt && !opt->fuse)) return fail(QSV_E_UNSUPPORTED, "no fused pass to carry the exchange");
+    int m, r, L, sq;
+    resolve_options(opt, st->n, m, r, L, sq);
+    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, opt ? opt->jit : 0,
+                                                 st->device);
+    Plan &P = cp->plan;
+    const int last = (int)P.passes.size() - 1;
+    if (use_supers(P) || last < 0) return fail(QSV_E_UNSUPPORTED, "plan uses super-passes");
+    if (P.passes[last].tile_mask & ex->positions)
+        return fail(QSV_E_UNSUPPORTED, "exchanged qubits are tile qubits of the last pass");
+    void *xfn = nullptr;
+    int xgrid = 0;
+    {
+        std::lock_guard<std::mutex> lk(cp->mu);
+        rc = jit_prepare(P, st->device, msg);
+        if (!rc) rc = jit_exchange_prepare(P, last, ex->positions, st->device, &xfn, &xgrid, msg);
+    }
+    if (rc) return fail(QSV_E_UNSUPPORTED, msg);
+    LaunchTimer tm;
+    tm.on = opt && opt->profile;
+    tm.s = st->stream;
+    for (int i = 0; i <= last; ++i) {
+        const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+        tm.begin();
+        if (i < last) rc = jit_launch(P, i, st->amps, st->n, st->stream, msg, basis);
+        else rc = jit_launch_exchange(P, i, xfn, xgrid, st->amps, st->n, st->stream, msg, basis,
+                                      (const unsigned long long *)ex->dst, ex->self_bits);
+        tm.end();
+        if (rc) return fail(rc, msg);
+        st->pending_basis = -1;
+    }
+    tm.collect(stats);
+    if (stats) {
+        stats->gates += P.gates;
+        stats->passes += last + 1;
+        stats->inner_passes += last + 1;
+        stats->stages += (int64_t)P.stages.size();
+        stats->launches += last + 1;
+        stats->algorithmic_bytes += (double)(last + 1) * 32.0 * (double)st->size();
+    }
+    return QSV_OK;
+}
+
+int qsv_plan_exchange_source(const qsv_plan *plan, int64_t pass, int host, uint64_t positions, char *buf,
+                             int64_t buf_size, int64_t *needed) {
+    const Plan &P = plan->p;
+    if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
+    if (!positions || (P.passes[pass].tile_mask & positions)) return fail(QSV_E_UNSUPPORTED, "positions overlap the tile");
+    const std::string src = jit_source(P, (int)pass, host != 0, nullptr, positions);
+    if (needed) *needed = (int64_t)src.size() + 1;
+    if (buf && buf_size > 0) {
+        const size_t k = std::min<size_t>(src.size(), (size_t)buf_size - 1);
+        std::memcpy(buf, src.data(), k);
+        buf[k] = 0;
+    }
     return QSV_OK;
 }
 

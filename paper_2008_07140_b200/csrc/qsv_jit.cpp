@@ -910,7 +910,7 @@ namespace {
 double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
                       const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
                       bool basis_param = false, bool prefetch = true, double scale_in = 1.0,
-                      bool final_pass = true, double *scale_out = nullptr, int gang = 1) {
+                      bool final_pass = true, double *scale_out = nullptr, int gang = 1, uint64_t xmask = 0) {
     double fp64 = 0;
     double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
@@ -935,6 +935,20 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     // first tile, so the kernel runs out of L2 and its time is compute + smem + barriers
     static const bool diag_l2 = std::getenv("QSV_JIT_DIAG_L2") != nullptr;
     o << "    const u64 base = " << (diag_l2 && !host ? base_of("(u64)blockIdx.x") : base_of("t")) << ";\n";
+    // exchange-out pass (sharded layout): the outputs of this tile go to the
+    // rank selected by its bits at the exchanged positions `xmask` (tile-base
+    // bits), at the same offset with those bits replaced by this rank's own
+    // global bits - the global<->local qubit swap fused into the pass's stores
+    // (remote stores over NVLink into the peer's receive buffer)
+    std::string out_base = "psi + base";
+    if (xmask) {
+        o << "    double2 *const xo = (double2 *)xd.p[";
+        int i = 0;
+        for (int q = 0; q < 64; ++q)
+            if ((xmask >> q) & 1) o << (i ? " | " : "") << "(((base >> " << q << ") & 1ull) << " << i++ << ")";
+        o << "] + ((base & ~" << xmask << "ull) | xd.self);\n";
+        out_base = "xo";
+    }
     SmemMap smap;
     {
         std::vector<std::vector<int>> lane_sets;
@@ -1085,7 +1099,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
             o << thread_end << barrier << thread_loop << "    " << guard << "{\n";
             o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
-            o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
+            o << "    double2 *gpc = " << out_base << " + (" << deposit_expr("tid", lowq, true) << ");\n";
             for (int k = 0; k < (1 << R); ++k)
                 o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gpc + " << goffc[k] << "ull, tile[tsc ^ " << cc[k]
                   << "u]);\n";
@@ -1094,8 +1108,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             // evict-first stores when the data leaves for HBM; write-back (L2
             // resident) stores between the inner passes of a super-pass
             o << "    " << guard << "{\n";
+            if (xmask) o << "    double2 *gq = xo + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
             for (int rho = 0; rho < (1 << R); ++rho)
-                o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gp + " << goff[rho] << "ull, v" << rho << ");\n";
+                o << "    " << (stream_out ? "stcs2" : "stwb2") << (xmask ? "(gq + " : "(gp + ") << goff[rho] << "ull, v"
+                  << rho << ");\n";
             o << "    }\n";
             o << thread_end << "    }\n";
         } else {
@@ -1171,7 +1187,7 @@ const std::vector<double> &pass_scales(const Plan &P) {
     return P.jit_scale_in;
 }
 
-std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
+std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, uint64_t xmask) {
     const DevPass &dp = P.passes[pi];
     std::ostringstream o;
     o << "// libqsv specialised pass kernel: n=" << P.n << " m=" << dp.m << " R=" << P.r << " pass=" << pi << "\n";
@@ -1200,16 +1216,20 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp) {
             ((size_t)env_gang << (dp.m + 4)) <= ((size_t)227 << 10))
             gang = env_gang;
     }
-    o << kernel_head(P, dp.m, host, "qsv_pass",
-                     host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis",
-                     cost, gang);
+    if (xmask) {
+        gang = 1;
+        o << "struct XDst { unsigned long long p[8]; unsigned long long self; };\n";
+    }
+    std::string params = host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis";
+    if (xmask) params += ", XDst xd";
+    o << kernel_head(P, dp.m, host, "qsv_pass", params.c_str(), cost, gang);
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
     const char *e = std::getenv("QSV_JIT_PREFETCH");
     const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
-                                    sc, final_pass, nullptr, gang);
+                                    sc, final_pass, nullptr, gang, xmask);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
     o << "}\n";
     return o.str();
@@ -1520,6 +1540,79 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         }
     }
     P.jit_device = device;
+    return QSV_OK;
+}
+
+// Exchange-out variant of one pass (compiled on demand, cached by source).
+int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, void **fn, int *grid, std::string &err) {
+    if (!jit_available(err)) return QSV_E_DEVICE;
+    Driver &drv = driver();
+    const std::string src = jit_source(P, pass, false, nullptr, xmask);
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_cache.find({device, src});
+        if (it != g_cache.end()) {
+            *fn = it->second.fn;
+            *grid = it->second.grid;
+            return QSV_OK;
+        }
+    }
+    std::string cubin;
+    const std::string path = disk_cache_path(src);
+    if (!disk_cache_load(path, cubin)) {
+        std::string log;
+        cubin = jit_compile_cubin(src, log);
+        if (cubin.empty()) {
+            err = "NVRTC failed for the exchange-out pass: " + log;
+            return QSV_E_DEVICE;
+        }
+        disk_cache_store(path, cubin);
+    }
+    cudaSetDevice(device);
+    cudaFree(nullptr);
+    const int m = P.passes[pass].m;
+    CUmodule mod;
+    CUfunction f;
+    CUresult r = drv.ModuleLoadData(&mod, cubin.data());
+    if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&f, mod, "qsv_pass");
+    const int smem = (int)((size_t)16 << m);
+    if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+    int per_sm = 0;
+    if (r == CUDA_SUCCESS) r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 1 << (m - P.r), (size_t)smem);
+    if (r != CUDA_SUCCESS || per_sm < 1) {
+        err = "loading the exchange-out pass kernel failed";
+        return QSV_E_DEVICE;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[{device, src}] = CacheEntry{f, per_sm * sms, 1};
+    *fn = f;
+    *grid = per_sm * sms;
+    return QSV_OK;
+}
+
+int jit_launch_exchange(const Plan &P, int pass, void *fn, int grid_cap, void *psi, int n, cudaStream_t stream,
+                        std::string &err, unsigned long long basis, const unsigned long long *dst8,
+                        unsigned long long self_bits) {
+    const int m = P.passes[pass].m, T = 1 << (m - P.r);
+    unsigned long long n_tiles = 1ull << (n - m);
+    const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, (unsigned long long)grid_cap);
+    struct XDst {
+        unsigned long long p[8];
+        unsigned long long self;
+    } xd;
+    for (int i = 0; i < 8; ++i) xd.p[i] = dst8[i];
+    xd.self = self_bits;
+    void *args[] = {&psi, &n_tiles, &basis, &xd};
+    const CUresult r = driver().LaunchKernel((CUfunction)fn, grid, 1, 1, T, 1, 1, (unsigned)((size_t)16 << m),
+                                             (CUstream)stream, args, nullptr);
+    if (r != CUDA_SUCCESS) {
+        const char *s2 = nullptr;
+        driver().GetErrorString(r, &s2);
+        err = std::string("cuLaunchKernel (exchange-out): ") + (s2 ? s2 : "?");
+        return QSV_E_DEVICE;
+    }
     return QSV_OK;
 }
 

@@ -24,7 +24,16 @@ bool jit_available(std::string &why);
 
 // CUDA source of the specialised kernel for pass `pass` of plan P (extern "C"
 // entry point `qsv_pass`).  Pure host code (testable without a GPU).
-std::string jit_source(const Plan &P, int pass, bool host = false, double *fp64_per_amp = nullptr);
+std::string jit_source(const Plan &P, int pass, bool host = false, double *fp64_per_amp = nullptr,
+                       uint64_t xmask = 0);
+
+// Exchange-out variant of pass `pass` (xmask = exchanged positions, all tile-base
+// bits of that pass): stores go to dst8[bits at xmask] + (index with those bits
+// replaced by self_bits).  Compiled on demand and cached like the pass kernels.
+int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, void **fn, int *grid, std::string &err);
+int jit_launch_exchange(const Plan &P, int pass, void *fn, int grid_cap, void *psi, int n, cudaStream_t stream,
+                        std::string &err, unsigned long long basis, const unsigned long long *dst8,
+                        unsigned long long self_bits);
 
 // Cost model: decides for every super-pass whether its inner passes run as one
 // L2-resident persistent kernel (one HBM pass) or as flat passes (one HBM pass

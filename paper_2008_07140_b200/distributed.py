@@ -26,7 +26,16 @@ g qubits per circuit).  Within a segment:
   statevector.py:128-132);
 * runs of local gates go to the native fused scheduler (`qsv_run`).
 
-Exchange (global <-> local qubit swap).  Leaving qubits V are first moved
+Exchange (global <-> local qubit swap), preferred form - FUSED into the
+previous run's last pass (`P2PTransport.fused_exchange`, `qsv_run_exchange`):
+that pass's kernel stores every output amplitude straight into the receive
+buffer of the rank selected by its bits at the leaving qubits' positions
+(remote stores over NVLink to CUDA-IPC-mapped peer memory), so the exchange
+costs no extra HBM pass and overlaps the pass's math tile by tile; the
+entering qubits take the leaving qubits' positions.  All ranks agree first
+(it needs those positions outside the last pass's tile on every rank).
+
+Otherwise (copy form): leaving qubits V are first moved
 (SWAP gates appended to the previous run - the fused planner turns them into
 relabellings materialised by its last pass) onto the exchange positions
 X = [n_local - c - s, n_local - c) just below the c CHUNK positions at the
@@ -76,6 +85,7 @@ class SwapRecord:
     bytes_sent: int
     chunks: int = 1
     prefix_gates: int = 0
+    fused: bool = False  # carried by the last pass's stores (qsv_run_exchange)
 
 
 @dataclass
@@ -351,6 +361,57 @@ class P2PTransport:
                 shard.stream.wait_event(self.peer_events[peer][i])
             on_chunk(i)
 
+    def fused_exchange(self, sim, run, vpos, G, stats=None) -> bool:
+        """The global<->local swap FUSED into the run's last pass: its kernel
+        stores every output amplitude straight into the partner rank's receive
+        buffer over NVLink (qsv_run_exchange).  All ranks decide together (a
+        rank whose last pass holds an exchanged position in its tile cannot
+        fuse); False = nothing was run, the caller exchanges by copies."""
+        torch, L, N = self.torch, self.N.lib(), self.N
+        shard = self.shard
+        rec = N.gate_records(run) if run else None
+        ok = C.c_int(0)
+        vmask = sum(1 << p for p in vpos)
+        if run:
+            N.check(L.qsv_exchange_fusable(shard.handle(), rec.ctypes.data, len(rec), C.byref(shard.options),
+                                           C.c_uint64(vmask), C.byref(ok)))
+        flag = torch.tensor([int(ok.value)], dtype=torch.int32,
+                            device="cpu" if self.dist.get_backend(self.group) == "gloo" else f"cuda:{shard.device}")
+        self.dist.all_reduce(flag, op=self.dist.ReduceOp.MIN, group=self.group)
+        if not int(flag.item()):
+            return False
+        nl = sim.n_local
+        gbits = [p - nl for p in G]
+        gmask = sum(1 << b for b in gbits)
+        my_g = sum(((self.rank >> b) & 1) << i for i, b in enumerate(gbits))
+        spare = 1 - shard.cur
+        ex = N.qsv_exchange()
+        ex.positions = vmask
+        ex.self_bits = sum(((my_g >> i) & 1) << p for i, p in enumerate(vpos))
+        partners = []
+        for j in range(1 << len(G)):
+            peer = self.rank & ~gmask
+            for i, b in enumerate(gbits):
+                peer |= ((j >> i) & 1) << b
+            partners.append(peer)
+            ex.dst[j] = self.peer_ptr[peer][spare]
+        # every rank's previous exchange is complete -> every receive buffer is free
+        self.copy_stream.synchronize()
+        shard.stream.synchronize()
+        self.dist.barrier(group=self.group)
+        st = N.qsv_run_stats()
+        N.check(L.qsv_run_exchange(shard.handle(), rec.ctypes.data, len(rec), C.byref(shard.options), C.byref(ex),
+                                   C.byref(st)))
+        if stats is not None:
+            for k, v in st.as_dict().items():
+                stats[k] = stats.get(k, 0) + v
+        self.events[0].record(shard.stream)
+        self.dist.barrier(group=self.group)  # every partner has enqueued its event
+        shard.commit_exchange()
+        for peer in partners:
+            shard.stream.wait_event(self.peer_events[peer][0])
+        return True
+
     def exchange_ms(self) -> float:
         """Copy-stream time of the last exchange (this rank's pushes)."""
         self._t1.synchronize()
@@ -384,6 +445,7 @@ class ShardedSimulator:
             chunk_log2 = int(os.environ.get("QSV_SWAP_CHUNKS_LOG2", "2" if self.n_local >= 16 else "0"))
         self.chunk_log2 = chunk_log2
         self.transport = transport or AllToAllTransport(dist, group)
+        self.fuse_exchange = os.environ.get("QSV_FUSED_EXCHANGE", "1") != "0"
         self.dq = list(range(n))    # logical -> data qubit
         self.perm = list(range(n))  # data qubit -> physical position
         self._basis = None          # pending basis index (layout still free)
@@ -478,6 +540,17 @@ class ShardedSimulator:
         E = [q for q in range(self.n) if (new_local >> q) & 1 and self.perm[q] >= nl]
         V = [q for q in range(self.n) if not (new_local >> q) & 1 and self.perm[q] < nl]
         s = len(E)
+        if hasattr(self.transport, "fused_exchange") and self.fuse_exchange:
+            vpos = sorted(self.perm[v] for v in V)
+            G = sorted(self.perm[e] for e in E)
+            if self.transport.fused_exchange(self, run, vpos, G, stats):
+                self.stats.gate_runs += bool(run)
+                for gp, vp in zip(G, vpos):  # bit i at vpos[i] <-> the partner's global bit G[i]
+                    a, b = self._occupant(gp), self._occupant(vp)
+                    self.perm[a], self.perm[b] = vp, gp
+                self.stats.swaps.append(SwapRecord(tuple(G), tuple(vpos), 16 * (1 << nl) * ((1 << s) - 1) >> s, 0,
+                                                   0, True))
+                return seg_items
         c = max(0, min(self.chunk_log2, nl - s - 2))
         X = list(range(nl - c - s, nl - c))
         # leaving qubits onto the exchange positions (SWAPs fused into the run)

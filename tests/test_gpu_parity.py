@@ -252,6 +252,7 @@ def _sharded_gpu_worker(rank, world, port, out, transport):
     import torch.distributed as dist
 
     from paper_2008_07140_b200.distributed import CudaShard, ShardedSimulator, make_transport
+    from paper_2008_07140_b200 import _native as N
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -260,15 +261,20 @@ def _sharded_gpu_worker(rank, world, port, out, transport):
         for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
             prog = parse_program(text)
             g = world.bit_length() - 1
-            shard = CudaShard(prog.qubit_count - g, 0)
-            tr = make_transport(transport, dist, shard)
+            kind, _, variant = transport.partition("-")
+            # specialised kernels at this small size (the fused exchange needs them); 8-qubit tiles
+            # leave the leaving qubits outside the last pass's tile often enough to fuse
+            opts = N.options(jit=1, tile_qubits=8, reg_qubits=4) if kind == "p2p" else None
+            shard = CudaShard(prog.qubit_count - g, 0, options=opts)
+            tr = make_transport(kind, dist, shard)
             sim = ShardedSimulator(prog.qubit_count, shard, chunk_log2=2, transport=tr)
+            sim.fuse_exchange = variant == "fused"
             for _ in range(2):  # twice: the second run reuses buffers, handles and plans
                 sim.set_basis(1)
                 sim.run(prog)
             amps = sim.gather_amplitudes()
             if rank == 0:
-                res[name] = (amps, len(sim.stats.swaps))
+                res[name] = (amps, len(sim.stats.swaps), sum(x.fused for x in sim.stats.swaps))
             if hasattr(tr, "close"):
                 tr.close()
             dist.barrier()
@@ -279,7 +285,8 @@ def _sharded_gpu_worker(rank, world, port, out, transport):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,transport", [(2, "gloo"), (4, "gloo"), (2, "p2p"), (4, "p2p")])
+@pytest.mark.parametrize("world,transport", [(2, "gloo"), (4, "gloo"), (2, "p2p-copy"), (4, "p2p-copy"),
+                                             (2, "p2p-fused"), (4, "p2p-fused")])
 def test_sharded_path_on_gpu(world, transport, tmp_path):
     """CudaShard (libqsv on the GPU) + chunked global<->local qubit swaps, P ranks
     sharing the one GPU of this box.  Blocks travel over gloo through host
@@ -301,6 +308,8 @@ def test_sharded_path_on_gpu(world, transport, tmp_path):
         init = np.zeros(1 << prog.qubit_count, complex)
         init[1] = 1
         ref = O.run_full(prog, initial=init).state.amplitudes
-        amps, swaps = res[name]
+        amps, swaps, fused = res[name]
         assert swaps > 0
         assert_parity(amps, ref)
+    if transport.endswith("fused"):
+        assert sum(res[k][2] for k in res) > 0  # at least one exchange rode on a pass's stores

@@ -147,3 +147,62 @@ def test_generated_qft_runtime_diagonals(cfg):
     rt = parse_program(workloads.qft_text(n, round_trip=True))
     out = run_plan_host_super(compile_gates(rt.gate_instructions()), n, psi, **cfg)
     assert np.abs(out - psi).max() <= 1e-12
+
+
+@pytest.mark.parametrize("seed,n_pos", [(0, 2), (1, 1), (2, 3), (3, 2)])
+def test_exchange_out_pass_host(seed, n_pos):
+    """Exchange-out variant of a run's last pass (qsv_run_exchange): every output
+    amplitude lands in dst[bits at `positions`] at its index with those bits
+    replaced by this rank's own bits - the global<->local qubit swap fused into
+    the pass's stores.  Host rendering of the generated kernel vs the oracle."""
+    import ctypes as C2
+
+    from jit_host import _compile, kernel_source, plan_handle
+
+    n = 12
+    prog = parse_program(workloads.rqc_for_qubits(n, 8, seed))
+    recs = compile_gates(prog.gate_instructions())
+    psi = workloads.gaussian_state(n, seed)
+    ref = O.run_full(prog, initial=psi).state.amplitudes
+    h = plan_handle(recs, n, tile_qubits=6, reg_qubits=3, low_qubits=2)
+    try:
+        info = N.qsv_plan_info()
+        N.check(N.lib().qsv_plan_summary(h, C2.byref(info)))
+        last = info.passes - 1
+        pi = N.qsv_pass_info()
+        N.check(N.lib().qsv_plan_pass(h, last, C2.byref(pi)))
+        free = [q for q in range(n) if not (pi.tile_mask >> q) & 1]
+        positions = tuple(sorted(free[-n_pos:] if seed % 2 else free[:n_pos]))
+        vmask = sum(1 << p for p in positions)
+        out = psi.copy()
+        for p in range(last):
+            q = N.qsv_pass_info()
+            N.check(N.lib().qsv_plan_pass(h, p, C2.byref(q)))
+            _compile(kernel_source(h, p, True)).qsv_pass_host(out.ctypes.data, 1 << (n - q.m))
+        need = C2.c_int64()
+        N.check(N.lib().qsv_plan_exchange_source(h, last, 1, vmask, None, 0, C2.byref(need)))
+        buf = C2.create_string_buffer(need.value)
+        N.check(N.lib().qsv_plan_exchange_source(h, last, 1, vmask, buf, need.value, C2.byref(need)))
+        lib = _compile(buf.value.decode())
+
+        class XDst(C2.Structure):
+            _fields_ = [("p", C2.c_uint64 * 8), ("self", C2.c_uint64)]
+
+        dsts = [np.zeros(1 << n, complex) for _ in range(1 << len(positions))]
+        self_val = (1 << len(positions)) - 2 if len(positions) > 1 else 1
+        self_bits = sum(((self_val >> i) & 1) << p for i, p in enumerate(positions))
+        xd = XDst()
+        for j, d in enumerate(dsts):
+            xd.p[j] = d.ctypes.data
+        xd.self = self_bits
+        lib.qsv_pass_host.argtypes = [C2.c_void_p, C2.c_ulonglong, XDst]
+        lib.qsv_pass_host(out.ctypes.data, 1 << (n - pi.m), xd)
+    finally:
+        N.lib().qsv_plan_destroy(h)
+    idx = np.arange(1 << n)
+    j = sum(((idx >> p) & 1) << i for i, p in enumerate(positions))
+    dest = (idx & ~vmask) | self_bits
+    got = np.array([dsts[a][b] for a, b in zip(j, dest)])
+    assert np.abs(got - ref).max() <= 1e-12
+    written = sum(int(np.count_nonzero(d)) for d in dsts)
+    assert written == np.count_nonzero(ref)
