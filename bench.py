@@ -321,7 +321,8 @@ def run_gpu(args) -> None:
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"],
-                "traffic": args.traffic if args.traffic is not None else measured_traffic(),
+                "traffic": args.traffic if args.traffic is not None else (
+                    measured_traffic() if (n == N_BASE and args.workload == "rqc") else None),
                 "peak_src": pk["src"],
                 "kernel": "qsv_pass (specialised fused pass)" if not args.unfused else "gate_kernel",
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
@@ -374,7 +375,7 @@ def run_gpu(args) -> None:
                    "stages": int(info.stages), "tile_qubits": int(info.tile_qubits),
                    "super_passes": int(info.super_passes), "super_qubits": int(info.super_qubits),
                    "reg_qubits": int(info.reg_qubits), "low_qubits": int(info.low_qubits),
-                   "l2": "state (16 GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
+                   "l2": f"state ({16 << n >> 30} GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(launches),  # fused pass kernels (|0..0> is synthesised by the first pass)
         "clocks": clocks,

@@ -194,8 +194,8 @@ int qsv_ipc_mem_close(void *mapped);
  * receive buffer of the rank selected by its bits at `positions` (dst[value], a peer allocation
  * mapped with qsv_ipc_mem_open, or this rank's own), at the same offset with those bits replaced
  * by `self_bits` (this rank's global bits deposited at `positions`).  The state buffer itself is
- * left stale.  QSV_E_UNSUPPORTED when the last pass holds an exchanged position in its tile (the
- * caller then runs qsv_run and copies). */
+ * left stale.  QSV_E_UNSUPPORTED without specialised kernels or with super-passes (the caller then
+ * runs qsv_run and copies). */
 typedef struct qsv_exchange {
     uint64_t positions;
     uint64_t self_bits;

@@ -1048,7 +1048,7 @@ int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, 
     resolve_options(opt, st->n, m, r, L, sq);
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, jm, st->device);
     const Plan &P = cp->plan;
-    *out = !use_supers(P) && !P.passes.empty() && !(P.passes.back().tile_mask & positions);
+    *out = !use_supers(P) && !P.passes.empty() && positions && !(positions >> st->n);
     return QSV_OK;
 }
 
@@ -1070,8 +1070,6 @@ int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, cons
     Plan &P = cp->plan;
     const int last = (int)P.passes.size() - 1;
     if (use_supers(P) || last < 0) return fail(QSV_E_UNSUPPORTED, "plan uses super-passes");
-    if (P.passes[last].tile_mask & ex->positions)
-        return fail(QSV_E_UNSUPPORTED, "exchanged qubits are tile qubits of the last pass");
     void *xfn = nullptr;
     int xgrid = 0;
     {
@@ -1109,7 +1107,7 @@ int qsv_plan_exchange_source(const qsv_plan *plan, int64_t pass, int host, uint6
                              int64_t buf_size, int64_t *needed) {
     const Plan &P = plan->p;
     if (pass < 0 || pass >= (int64_t)P.passes.size()) return fail(QSV_E_PARSE, "pass index out of range");
-    if (!positions || (P.passes[pass].tile_mask & positions)) return fail(QSV_E_UNSUPPORTED, "positions overlap the tile");
+    if (!positions || (positions >> P.n)) return fail(QSV_E_PARSE, "exchange positions out of range");
     const std::string src = jit_source(P, (int)pass, host != 0, nullptr, positions);
     if (needed) *needed = (int64_t)src.size() + 1;
     if (buf && buf_size > 0) {

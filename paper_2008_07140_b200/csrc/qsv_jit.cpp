@@ -935,20 +935,11 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     // first tile, so the kernel runs out of L2 and its time is compute + smem + barriers
     static const bool diag_l2 = std::getenv("QSV_JIT_DIAG_L2") != nullptr;
     o << "    const u64 base = " << (diag_l2 && !host ? base_of("(u64)blockIdx.x") : base_of("t")) << ";\n";
-    // exchange-out pass (sharded layout): the outputs of this tile go to the
-    // rank selected by its bits at the exchanged positions `xmask` (tile-base
-    // bits), at the same offset with those bits replaced by this rank's own
-    // global bits - the global<->local qubit swap fused into the pass's stores
+    // exchange-out pass (sharded layout): every output amplitude goes to the
+    // rank selected by its index bits at the exchanged positions `xmask`, at
+    // its index with those bits replaced by this rank's own global bits
+    // (QSV_XDST) - the global<->local qubit swap fused into the pass's stores
     // (remote stores over NVLink into the peer's receive buffer)
-    std::string out_base = "psi + base";
-    if (xmask) {
-        o << "    double2 *const xo = (double2 *)xd.p[";
-        int i = 0;
-        for (int q = 0; q < 64; ++q)
-            if ((xmask >> q) & 1) o << (i ? " | " : "") << "(((base >> " << q << ") & 1ull) << " << i++ << ")";
-        o << "] + ((base & ~" << xmask << "ull) | xd.self);\n";
-        out_base = "xo";
-    }
     SmemMap smap;
     {
         std::vector<std::vector<int>> lane_sets;
@@ -1099,19 +1090,26 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             for (int rho = 0; rho < (1 << R); ++rho) o << "    tile[tsw ^ " << c[rho] << "u] = v" << rho << ";\n";
             o << thread_end << barrier << thread_loop << "    " << guard << "{\n";
             o << "    const unsigned tsc = " << smap.tid_expr(natural) << ";\n";
-            o << "    double2 *gpc = " << out_base << " + (" << deposit_expr("tid", lowq, true) << ");\n";
+            if (xmask) {
+                o << "    const u64 xib = base + (" << deposit_expr("tid", lowq, true) << ");\n";
+                for (int k = 0; k < (1 << R); ++k)
+                    o << "    " << (stream_out ? "stcs2" : "stwb2") << "(QSV_XDST(xib + " << goffc[k] << "ull), tile[tsc ^ "
+                      << cc[k] << "u]);\n";
+            } else {
+            o << "    double2 *gpc = psi + base + (" << deposit_expr("tid", lowq, true) << ");\n";
             for (int k = 0; k < (1 << R); ++k)
                 o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gpc + " << goffc[k] << "ull, tile[tsc ^ " << cc[k]
                   << "u]);\n";
+            }
             o << "    }\n" << thread_end << "    }\n";
         } else if (last) {
             // evict-first stores when the data leaves for HBM; write-back (L2
             // resident) stores between the inner passes of a super-pass
             o << "    " << guard << "{\n";
-            if (xmask) o << "    double2 *gq = xo + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+            if (xmask) o << "    const u64 xib = base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
             for (int rho = 0; rho < (1 << R); ++rho)
-                o << "    " << (stream_out ? "stcs2" : "stwb2") << (xmask ? "(gq + " : "(gp + ") << goff[rho] << "ull, v"
-                  << rho << ");\n";
+                o << "    " << (stream_out ? "stcs2" : "stwb2") << (xmask ? "(QSV_XDST(xib + " : "(gp + ") << goff[rho]
+                  << (xmask ? "ull), v" : "ull, v") << rho << ");\n";
             o << "    }\n";
             o << thread_end << "    }\n";
         } else {
@@ -1219,6 +1217,11 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     if (xmask) {
         gang = 1;
         o << "struct XDst { unsigned long long p[8]; unsigned long long self; };\n";
+        o << "#define QSV_XDST(ix) ((double2 *)xd.p[";
+        int i = 0;
+        for (int q = 0; q < 64; ++q)
+            if ((xmask >> q) & 1) o << (i ? " | " : "") << "((((ix) >> " << q << ") & 1ull) << " << i++ << ")";
+        o << "] + (((ix) & ~" << xmask << "ull) | xd.self))\n";
     }
     std::string params = host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis";
     if (xmask) params += ", XDst xd";

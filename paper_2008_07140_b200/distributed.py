@@ -33,7 +33,7 @@ buffer of the rank selected by its bits at the leaving qubits' positions
 (remote stores over NVLink to CUDA-IPC-mapped peer memory), so the exchange
 costs no extra HBM pass and overlaps the pass's math tile by tile; the
 entering qubits take the leaving qubits' positions.  All ranks agree first
-(it needs those positions outside the last pass's tile on every rank).
+(it needs the specialised kernels on every rank).
 
 Otherwise (copy form): leaving qubits V are first moved
 (SWAP gates appended to the previous run - the fused planner turns them into
@@ -619,7 +619,12 @@ class ShardedSimulator:
         free = self._basis is not None
         seg, seg_local = plan_segments(items, self.n, self.n_local, self._local_mask(), free)
         if free:
-            loc = [q for q in range(self.n) if (seg_local[0] >> q) & 1]
+            # qubits leaving at the first exchange sit at the TOP local positions:
+            # outside the forced low tile qubits, so the exchange can ride on the
+            # last pass's stores (fused exchange)
+            nxt = seg_local[1] if len(seg_local) > 1 else seg_local[0]
+            loc = [q for q in range(self.n) if (seg_local[0] >> q) & 1 and (nxt >> q) & 1]
+            loc += [q for q in range(self.n) if (seg_local[0] >> q) & 1 and not (nxt >> q) & 1]
             glo = [q for q in range(self.n) if not (seg_local[0] >> q) & 1]
             for p, q in enumerate(loc + glo):
                 self.perm[q] = p
@@ -726,12 +731,12 @@ def bench_main(args) -> None:
     ms_step = float(ms.item())
     swaps = sim.stats.swaps
     swap_bytes = sum(s.bytes_sent for s in swaps) / max(1, args.steps)
-    xfer = {}
-    if kind == "p2p" and swaps:
+    xfer = {"fused_exchanges_per_step": sum(s.fused for s in swaps) / max(1, args.steps)}
+    if kind == "p2p" and swaps and not all(s.fused for s in swaps):
         t = torch.tensor([transport.exchange_ms()], device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         last = swaps[-1].bytes_sent
-        xfer = {"last_exchange_ms": float(t.item()), "last_exchange_bytes_per_rank": last,
+        xfer |= {"last_exchange_ms": float(t.item()), "last_exchange_bytes_per_rank": last,
                 "nvlink_gbs_per_rank": last / (float(t.item()) / 1e3) / 1e9, "nvlink_peak_gbs": 900.0}
     if rank == 0:
         line = {

@@ -171,8 +171,9 @@ def test_exchange_out_pass_host(seed, n_pos):
         last = info.passes - 1
         pi = N.qsv_pass_info()
         N.check(N.lib().qsv_plan_pass(h, last, C2.byref(pi)))
-        free = [q for q in range(n) if not (pi.tile_mask >> q) & 1]
-        positions = tuple(sorted(free[-n_pos:] if seed % 2 else free[:n_pos]))
+        # outside the tile (per-tile destination) or inside it (per-store destination)
+        pool = [q for q in range(n) if bool((pi.tile_mask >> q) & 1) == bool(seed % 2)]
+        positions = tuple(sorted(pool[-n_pos:]))
         vmask = sum(1 << p for p in positions)
         out = psi.copy()
         for p in range(last):
