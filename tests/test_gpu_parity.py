@@ -313,3 +313,40 @@ def test_sharded_path_on_gpu(world, transport, tmp_path):
         assert_parity(amps, ref)
     if transport.endswith("fused"):
         assert sum(res[k][2] for k in res) > 0  # at least one exchange rode on a pass's stores
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("positions", [(17,), (3, 12), (0, 9, 17)])
+def test_exchange_out_pass_single_process(positions):
+    """qsv_run_exchange on one GPU with local destinations: the last pass's stores
+    land at dst[bits at positions] + (index with those bits replaced by self_bits);
+    here dst[j] = receive buffer + j-th slot so the receive buffer must equal the
+    plain run's state exactly (layout identity when self_bits = 0)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2008_07140_b200 import _native as N
+
+    n = 18
+    prog = parse_program(workloads.rqc_for_qubits(n, 12, 5))
+    rec = SV.compile_gates(prog.gate_instructions())
+    L = N.lib()
+    st = SV.init_state(n, max_qubits=n, device=0)
+    recv = torch.zeros(1 << n, dtype=torch.complex128, device="cuda:0")
+    o = N.options(jit=1)
+    ex = N.qsv_exchange()
+    ex.positions = sum(1 << p for p in positions)
+    ex.self_bits = 0
+    for j in range(1 << len(positions)):
+        off = sum(((j >> i) & 1) << p for i, p in enumerate(positions))
+        ex.dst[j] = recv.data_ptr() + off * 16
+    ok = C.c_int()
+    N.check(L.qsv_exchange_fusable(st.handle, rec.ctypes.data, len(rec), C.byref(o), ex.positions, C.byref(ok)))
+    assert ok.value == 1
+    st.set_basis(0)
+    N.check(L.qsv_run_exchange(st.handle, rec.ctypes.data, len(rec), C.byref(o), C.byref(ex), C.byref(N.qsv_run_stats())))
+    torch.cuda.synchronize()
+    ref = O.run_full(prog).state.amplitudes
+    assert_parity(recv.cpu().numpy(), ref)
+    st.close()
