@@ -317,7 +317,9 @@ def run_gpu(args) -> None:
     launches = stats.launches
     avg_launch_ms = stats.kernel_ms / max(1, launches)
     pk = peaks()
-    bytes_per_launch = 32.0 * float(1 << n)
+    # fused passes: every pass reads + writes all 2^n amplitudes; unfused: each
+    # gate touches the amplitudes whose controls are set (libqsv counts them)
+    bytes_per_launch = (stats.algorithmic_bytes / max(1, launches)) if args.unfused else 32.0 * float(1 << n)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"],

@@ -729,7 +729,10 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
             stats->gates += (int64_t)recs.size();
             stats->passes += (int64_t)recs.size();
             stats->launches += (int64_t)recs.size();
-            stats->algorithmic_bytes += (double)recs.size() * 32.0 * (double)st->size();
+            // a gate touches the amplitudes whose controls are set (gate_kernel /
+            // diag_kernel visit only those): read + write 16 B each
+            for (const GateRec &g : recs)
+                stats->algorithmic_bytes += 32.0 * std::ldexp(1.0, st->n - std::popcount(g.cmask));
         }
         return QSV_OK;
     }
