@@ -225,6 +225,7 @@ def run_traj(args) -> None:
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
+                           streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")),
                            dedup=args.dedup)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0

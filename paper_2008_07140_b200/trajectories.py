@@ -53,11 +53,16 @@ class TrajectoryReport:
 def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0, *,
                      probe_qubits=(0, 1, 2), keep=(), dedup: bool = False, device: int = 0,
                      stream=None, rank: int = 0, world: int = 1, state: SV.StateVector | None = None,
-                     options=None) -> TrajectoryReport:
+                     options=None, streams: int = 2) -> TrajectoryReport:
     n = program.qubit_count
     mine = list(range(rank, n_traj, world))
     if state is None:
         state = SV.init_state(n, max_qubits=max(n, SV.DEFAULT_MAX_QUBITS), device=device, stream=stream)
+    # consecutive trajectories alternate between `streams` device states, each
+    # with its own stream: one trajectory's pass tails and launch gaps overlap
+    # the next one's passes
+    states = [state] + [SV.init_state(n, max_qubits=max(n, SV.DEFAULT_MAX_QUBITS), device=device)
+                        for _ in range(max(0, streams - 1))]
     L = N.lib()
     opts_clean = options or N.options()
     opts_noisy = N.options(fuse=True, jit=-1, tile_qubits=opts_clean.tile_qubits,
@@ -83,7 +88,9 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     if async_tables:
         import torch
 
-        dev_tables = torch.zeros((max(1, len(mine)), 1 << len(pq)), dtype=torch.float64, device=f"cuda:{device}")
+        # no fill kernel: the libqsv streams are not ordered after torch's; every
+        # simulated row is written by its pmeasure, deduplicated rows are copied below
+        dev_tables = torch.empty((max(1, len(mine)), 1 << len(pq)), dtype=torch.float64, device=f"cuda:{device}")
     updates = 0
     unique = 0
     t0 = time.perf_counter()
@@ -97,6 +104,7 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             if n_err == 0 and dedup and clean_cache is not None and t not in keep:
                 dedup_from[k] = clean_cache
                 continue
+            state = states[unique % len(states)]
             state.set_basis(0)
             stats = N.qsv_run_stats()
             if n_err == 0:
@@ -126,12 +134,15 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             if n_err == 0 and clean_cache is None:
                 clean_cache = k
         if async_tables and mine:
-            N.check(L.qsv_synchronize(state.handle))
+            for st_ in states:
+                N.check(L.qsv_synchronize(st_.handle))
             tables[:] = dev_tables.cpu().numpy()[: len(mine)]
         for k, src in dedup_from.items():
             tables[k] = tables[src]
         norms[:] = tables.sum(axis=1)  # the probe table sums to ||psi||^2
     finally:
         L.qsv_plan_destroy(clean_plan)
+        for st_ in states[1:]:
+            st_.close()
     return TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
                             time.perf_counter() - t0)
