@@ -843,6 +843,7 @@ int place_paulis(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &
                 if ((k >= g) == (gpass[k] >= b)) continue;
                 ++crossed;
                 if (!can_conjugate_pauli(out.recs[k], q, kind)) ok = false;
+                else if (pauli_commutes(out.recs[k], q, kind)) continue;  // P G P = G: the pass is unchanged
                 if (!out.modified[gpass[k]] && !seen[gpass[k]]) {
                     seen[gpass[k]] = 1;
                     ++new_mod;
@@ -860,7 +861,7 @@ int place_paulis(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &
             return QSV_E_UNSUPPORTED;
         }
         for (int k : onq[q])
-            if ((k >= g) != (gpass[k] >= best)) {
+            if ((k >= g) != (gpass[k] >= best) && !pauli_commutes(out.recs[k], q, kind)) {
                 conjugate_pauli(out.recs[k], q, kind);
                 out.modified[gpass[k]] = 1;
             }

@@ -135,6 +135,31 @@ __device__ __forceinline__ void prefetch_l2(const void *g, unsigned bytes) {
 __device__ __forceinline__ void cp_async16(unsigned saddr, const void *g) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned spins = 0;
+    while (!mbar_try(bar, parity))
+        if (++spins > (1u << 26)) __trap();  // never hang the GPU: fail loudly
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
@@ -910,7 +935,8 @@ namespace {
 double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, const std::string &ntiles,
                       const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
                       bool basis_param = false, bool prefetch = true, double scale_in = 1.0,
-                      bool final_pass = true, double *scale_out = nullptr, int gang = 1, uint64_t xmask = 0) {
+                      bool final_pass = true, double *scale_out = nullptr, int gang = 1, uint64_t xmask = 0,
+                      bool tma = false) {
     double fp64 = 0;
     double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
@@ -926,6 +952,33 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     // warps run every stage in lock step (one code region in flight per SM);
     // a sub-tile past the end recomputes the last tile without storing it
     const std::string guard = (!host && gang > 1) ? "if (act) " : "";
+    tma = tma && !host;
+    // TMA-fed tiles (QSV_JIT_TMA): the next tile (group) is brought into the
+    // shared tile by bulk copies (one 2^lr-amplitude run per copy, completion
+    // on an mbarrier) as soon as this tile's last shared-memory read is done,
+    // so the load overlaps the last stage's math and no LDG is issued
+    int tma_lr = 0;
+    while (tma_lr < m && dp.tq[tma_lr] == tma_lr) ++tma_lr;
+    std::vector<int> tma_runq(dp.tq + tma_lr, dp.tq + m);
+    const std::string step = gang > 1 ? "(u64)gridDim.x * " + std::to_string(gang) + "u" : "(u64)gridDim.x";
+    auto tma_issue = [&](const std::string &tgx) {
+        // tgx: first tile of the group to load; every thread issues its runs
+        o << "    if (tma_on && " << tgx << " < ntiles) {\n";
+        o << "      const u64 tn = " << (gang > 1 ? "min(" + tgx + " + sub, ntiles - 1)" : tgx) << ";\n";
+        o << "      const u64 bn = " << base_of("tn") << ";\n";
+        o << "      if (threadIdx.x == 0) mbar_expect_tx(mbar, " << gang * (16u << m) << "u);\n";
+        o << "      for (unsigned j = tid; j < " << (1u << (m - tma_lr)) << "u; j += " << (1 << (m - R)) << "u)\n";
+        o << "        bulk_g2s(smem_u32(tile) + (j << " << (tma_lr + 4) << "), psi + bn + ("
+          << deposit_expr("j", tma_runq, true) << "), " << (16u << tma_lr) << "u, mbar);\n";
+        o << "    }\n";
+    };
+    if (tma) {
+        o << "  __shared__ __align__(8) unsigned long long qsv_mbar;\n";
+        o << "  const unsigned mbar = smem_u32(&qsv_mbar);\n  unsigned ph = 0;\n";
+        o << "  const bool tma_on = " << (basis_param ? "basis == ~0ull" : "true") << ";\n";
+        o << "  if (threadIdx.x == 0) mbar_init(mbar, 1);\n  __syncthreads();\n";
+        tma_issue(gang > 1 ? "((u64)blockIdx.x * " + std::to_string(gang) + "u)" : "(u64)blockIdx.x");
+    }
     if (host) o << "  for (u64 t = 0; t < ntiles; ++t) {\n";
     else if (gang == 1) o << "  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {\n";
     else
@@ -989,7 +1042,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         int run = 0;
         while (run < (int)nonreg.size() && nonreg[run] == run && tq[run] == run) ++run;
         static const int stage_min = std::getenv("QSV_JIT_STAGE_MIN") ? std::atoi(std::getenv("QSV_JIT_STAGE_MIN")) : 1;
-        const bool staged_in = first && run < stage_min, staged_out = last && run < stage_min;
+        const bool staged_in = !tma && first && run < stage_min, staged_out = last && run < stage_min;
         const int T = 1 << (m - R);
         std::vector<int> lowq(tq.begin(), tq.begin() + (m - R));
         std::vector<uint64_t> goffc(1u << R);
@@ -1048,6 +1101,24 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         if (staged_basis) {
         } else if (staged_in) {
             for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
+        } else if (first && tma) {
+            // the tile arrived by TMA in the raw layout (slot = local index)
+            std::vector<uint32_t> raw(1u << R);
+            for (int rho = 0; rho < (1 << R); ++rho) {
+                uint32_t off = 0;
+                for (int k = 0; k < R; ++k)
+                    if ((rho >> k) & 1) off |= 1u << st.rb[k];
+                raw[rho] = off;
+            }
+            o << "    if (tma_on) { mbar_wait(mbar, ph); ph ^= 1u; }\n";
+            o << "    const unsigned tr = (unsigned)(" << deposit_expr("tid", nonreg, true) << ");\n";
+            if (basis_param) o << "    const u64 gb = (u64)(gp - psi);\n";
+            for (int rho = 0; rho < (1 << R); ++rho) {
+                o << "    double2 v" << rho << " = ";
+                if (basis_param)
+                    o << "!tma_on ? make_double2(gb + " << goff[rho] << "ull == basis ? 1.0 : 0.0, 0.0) : ";
+                o << "tile[tr + " << raw[rho] << "u];\n";
+            }
         } else if (first) {
             if (basis_param) {
                 // the state is |basis>: synthesise the registers instead of
@@ -1078,6 +1149,14 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
               << "u) prefetch_l2(psi + (" << base_of("nt")
               << ") + (" << deposit_expr("j", runq, true) << "), " << (16u << lr) << "u); }\n";
         }
+        const std::string next_group = gang > 1 ? "(tg + " + step + ")" : "(t + " + step + ")";
+        if (tma && last && !staged_out) {
+            // every thread has read this tile's registers: the shared tile is
+            // free for the next tile (group) while this stage computes
+            o << barrier;
+            o << "    fence_proxy_async();\n";
+            tma_issue(next_group);
+        }
         g.declare_accumulators();
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all(sigma, final_pass && last);
@@ -1101,7 +1180,12 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
                 o << "    " << (stream_out ? "stcs2" : "stwb2") << "(gpc + " << goffc[k] << "ull, tile[tsc ^ " << cc[k]
                   << "u]);\n";
             }
-            o << "    }\n" << thread_end << "    }\n";
+            o << "    }\n" << thread_end;
+            if (tma) {
+                o << barrier << "    fence_proxy_async();\n";
+                tma_issue(next_group);
+            }
+            o << "    }\n";
         } else if (last) {
             // evict-first stores when the data leaves for HBM; write-back (L2
             // resident) stores between the inner passes of a super-pass
@@ -1203,8 +1287,10 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
                (double)(1 << P.r);
     }
     // QSV_JIT_GANG=G: compute-bound passes run G tiles per CTA in lock step
-    // (one CTA per SM) instead of independent CTAs
+    // (one CTA per SM) instead of independent CTAs; QSV_JIT_TMA=1: their
+    // tiles arrive by TMA bulk copies during the previous tile's last stage
     int gang = 1;
+    bool tma = false;
     if (!host) {
         static const int env_gang = std::getenv("QSV_JIT_GANG") ? std::atoi(std::getenv("QSV_JIT_GANG")) : 1;
         const int T = 1 << (dp.m - P.r);
@@ -1213,6 +1299,8 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
         if (env_gang > 1 && cost >= gang_min && env_gang * T <= 1024 &&
             ((size_t)env_gang << (dp.m + 4)) <= ((size_t)227 << 10))
             gang = env_gang;
+        static const bool env_tma = std::getenv("QSV_JIT_TMA") && std::atoi(std::getenv("QSV_JIT_TMA")) != 0;
+        tma = env_tma && cost >= gang_min;
     }
     if (xmask) {
         gang = 1;
@@ -1232,7 +1320,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     const char *e = std::getenv("QSV_JIT_PREFETCH");
     const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
-                                    sc, final_pass, nullptr, gang, xmask);
+                                    sc, final_pass, nullptr, gang, xmask, tma && !xmask);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
     o << "}\n";
     return o.str();

@@ -706,6 +706,18 @@ void pauli2(int kind, cd *p) {
 }
 }  // namespace
 
+bool pauli_commutes(const GateRec &g, int q, int kind) {
+    if (!(((g.nmask | g.dmask) >> q) & 1)) return true;
+    if (!can_conjugate_pauli(g, q, kind)) return false;
+    GateRec h = g;
+    conjugate_pauli(h, q, kind);
+    if (h.nt != g.nt || h.cmask != g.cmask || h.t[0] != g.t[0] || (g.nt == 2 && h.t[1] != g.t[1])) return false;
+    const int d = 1 << g.nt;
+    for (int k = 0; k < d * d; ++k)
+        if (h.u[k] != g.u[k]) return false;  // Pauli entries are 0, +-1, +-i: exact
+    return true;
+}
+
 bool can_conjugate_pauli(const GateRec &g, int q, int kind) {
     if (!((g.cmask >> q) & 1) || kind == 3) return true;  // targets always; Z commutes with a control
     return g.diag && g.nt == 1 && popc(g.cmask) == 1;    // C-diag(d0,d1) -> diag over (q, t) with q flipped

@@ -150,6 +150,8 @@ Plan build_single_pass(const std::vector<GateRec> &recs, const std::vector<int32
 // gate, or a multi-controlled one, controlled by q, conjugated by X or Y).
 bool can_conjugate_pauli(const GateRec &g, int q, int kind);
 void conjugate_pauli(GateRec &g, int q, int kind);
+// P G P == G exactly (the Pauli moves across G without changing it)
+bool pauli_commutes(const GateRec &g, int q, int kind);
 
 // SWAP gates folded into a logical->physical qubit map (see qsv_plan.cpp).
 std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &recs, int n);
