@@ -55,4 +55,11 @@ n = bench["config"]["n_qubits"]
     "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
     "algorithmic_bytes_per_launch": 32 * 2 ** n, "round": int(sys.argv[1][1:])}, indent=1) + "\n")
 (out / "bench.json").write_text(json.dumps(bench, indent=1) + "\n")
+# the other configs' bench lines (scripts/round_measure.sh)
+for name in ("bench_qft", "bench_traj", "bench_traj_dedup", "bench_n32"):
+    f = src / f"{name}.json"
+    if f.exists() and f.read_text().strip():
+        (out / f"{name}.json").write_text(json.dumps(json.loads(f.read_text().strip().splitlines()[-1]), indent=1) + "\n")
+if (src / "exchange_pass.log").exists():
+    shutil.copy(src / "exchange_pass.log", out / "exchange_pass.log")
 print("wrote", out)
