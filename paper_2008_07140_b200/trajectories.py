@@ -61,8 +61,9 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     # consecutive trajectories alternate between `streams` device states, each
     # with its own stream: one trajectory's pass tails and launch gaps overlap
     # the next one's passes
+    # (only while a second state is small: at n > 28 it would cost >= 8 GiB)
     states = [state] + [SV.init_state(n, max_qubits=max(n, SV.DEFAULT_MAX_QUBITS), device=device)
-                        for _ in range(max(0, streams - 1))]
+                        for _ in range(max(0, streams - 1) if n <= 28 else 0)]
     L = N.lib()
     opts_clean = options or N.options()
     opts_noisy = N.options(fuse=True, jit=-1, tile_qubits=opts_clean.tile_qubits,
