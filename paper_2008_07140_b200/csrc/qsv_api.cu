@@ -1253,7 +1253,7 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
             case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
             default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
         }
-        pmeasure_finish<<<1, 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
+        pmeasure_finish_small<<<(unsigned)bins, 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
     } else if (m <= kPmeasureSmallBits) {
         pmeasure_kernel<<<blocks, 256, sizeof(double) * bins, st->stream>>>(st->amps, st->size(), m, d_q, st->work);
         pmeasure_finish<<<(unsigned)((bins + 255) / 256), 256, 0, st->stream>>>(st->work, blocks, (int)bins, d_table);
@@ -1290,7 +1290,7 @@ int qsv_pmeasure_async(qsv_state *st, const int32_t *qubits, int m, double *devi
         case 3: pmeasure_small_kernel<3><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
         default: pmeasure_small_kernel<4><<<blocks, 256, 0, st->stream>>>(st->amps, st->size(), ql, st->work); break;
     }
-    pmeasure_finish<<<1, 256, 0, st->stream>>>(st->work, blocks, (int)bins, device_table);
+    pmeasure_finish_small<<<(unsigned)bins, 256, 0, st->stream>>>(st->work, blocks, (int)bins, device_table);
     CUDA_TRY(cudaGetLastError());
     return QSV_OK;
 }

@@ -604,6 +604,23 @@ __global__ void pauli_kernel(double2 *__restrict__ psi, uint64_t size, uint64_t 
     }
 }
 
+// small tables: one 256-thread block per bin sums the per-block partials in a
+// fixed order (strided per thread, then a fixed tree) - deterministic
+__global__ void __launch_bounds__(256) pmeasure_finish_small(const double *partial, int n_blocks, int bins,
+                                                             double *table) {
+    __shared__ double red[256];
+    const int b = blockIdx.x;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n_blocks; i += 256) s += partial[(size_t)i * bins + b];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) table[b] = red[0];
+}
+
 __global__ void pmeasure_finish(const double *partial, int n_blocks, int bins, double *table) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= bins) return;
