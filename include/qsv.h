@@ -227,6 +227,13 @@ typedef struct qsv_pauli {
  * kernel.  QSV_E_UNSUPPORTED when the plan relabelled SWAPs or uses super-passes. */
 int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
                             const qsv_options *opt, qsv_run_stats *stats);
+/* qsv_plan_execute_paulis (n_paulis may be 0) followed by the probe table (1..4 qubits, first listed =
+ * MSB, statevector.py:311-328 semantics) of the final state, written to DEVICE memory on the state's
+ * stream.  When the plan's last pass runs compiled with nothing after it, that pass accumulates the
+ * table while it stores (no extra read of the state); otherwise pmeasure runs after it. */
+int qsv_plan_execute_probe(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
+                           const int32_t *probe_qubits_msb_first, int m, double *device_table, const qsv_options *opt,
+                           qsv_run_stats *stats);
 /* host only (tests): the gate stream such an execution applies, in execution order - boundary
  * strings as Z, X gates and a phase, then each pass's (conjugated) gates.  *n_out = records
  * written (at most cap), *n_modified = passes that would run interpreted. */

@@ -111,6 +111,8 @@ _SIGNATURES = {
     "qsv_exchange_fusable": ([_P, _P, C.c_int64, C.POINTER(qsv_options), C.c_uint64, C.POINTER(C.c_int)], C.c_int),
     "qsv_run_exchange": ([_P, _P, C.c_int64, C.POINTER(qsv_options), _P, C.POINTER(qsv_run_stats)], C.c_int),
     "qsv_plan_execute_paulis": ([_P, _P, _P, C.c_int64, C.POINTER(qsv_options), C.POINTER(qsv_run_stats)], C.c_int),
+    "qsv_plan_execute_probe": ([_P, _P, _P, C.c_int64, _P, C.c_int, _P, C.POINTER(qsv_options),
+                                C.POINTER(qsv_run_stats)], C.c_int),
     "qsv_plan_pauli_stream": ([_P, _P, C.c_int64, _P, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int64)],
                               C.c_int),
 }

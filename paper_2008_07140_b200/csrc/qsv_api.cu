@@ -892,27 +892,35 @@ int launch_pauli(qsv_state *st, const PauliString &ps) {
     return QSV_OK;
 }
 
-int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
-                            const qsv_options *opt, qsv_run_stats *stats) {
-    if (n_paulis <= 0) return qsv_plan_execute(st, plan, opt, stats);
-    Plan &P = plan->p;
-    if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
-    int rc = set_device(st->device);
-    if (rc) return rc;
-    PauliPlacement pl;
+// Runs plan P with the placed Pauli errors `pl` (no errors: pl empty).  With
+// `probe` (1..4 qubits, first = MSB) the probe table of the final state is
+// written to device memory: by the last pass itself when it is a compiled pass
+// with nothing after it (a probe-out variant accumulating |amp|^2 per key as
+// it stores, per-CTA partials + a fixed-order finish), else by pmeasure.
+int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_t n_paulis, const qsv_options *opt,
+                        qsv_run_stats *stats, const int32_t *probe, int probe_m, double *probe_table) {
     std::string msg;
-    rc = place_paulis(P, paulis, n_paulis, pl, msg);
-    if (rc) return fail(rc, msg);
-    rc = jit_prepare(P, st->device, msg);
+    int rc = jit_prepare(P, st->device, msg);
     if (rc) return fail(rc, msg);
     const std::vector<double> &sc = pass_scales(P);
     const int np = (int)P.passes.size();
+    const bool has_pl = !pl.modified.empty();
+    const bool fused_probe = probe && np > 0 && !(has_pl && (pl.modified[np - 1] || pl.bnd[np].any));
+    void *pfn = nullptr;
+    int pgrid = 0;
+    if (fused_probe) {
+        rc = jit_probe_prepare(P, np - 1, std::vector<int>(probe, probe + probe_m), st->device, &pfn, &pgrid, msg);
+        if (rc) return fail(rc, msg);
+        pgrid = (int)std::min<uint64_t>((uint64_t)pgrid, 1ull << (st->n - P.passes[np - 1].m));
+        rc = ensure_work(st, sizeof(double) * ((size_t)pgrid << probe_m) + sizeof(int) * 64);
+        if (rc) return rc;
+    }
     LaunchTimer tm;
     tm.on = opt && opt->profile;
     tm.s = st->stream;
-    int64_t launches = 0, interpreted = 0;
+    int64_t launches = 0;
     for (int j = 0; j <= np; ++j) {
-        if (pl.bnd[j].any) {
+        if (has_pl && pl.bnd[j].any) {
             tm.begin();
             rc = launch_pauli(st, pl.bnd[j]);
             tm.end();
@@ -921,9 +929,12 @@ int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paul
         }
         if (j == np) break;
         tm.begin();
-        if (!pl.modified[j]) {
+        if (!has_pl || !pl.modified[j]) {
             const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
-            rc = jit_launch(P, j, st->amps, st->n, st->stream, msg, basis);
+            if (fused_probe && j == np - 1)
+                rc = jit_launch_probe(P, j, pfn, pgrid, st->amps, st->n, st->stream, msg, basis, st->work);
+            else
+                rc = jit_launch(P, j, st->amps, st->n, st->stream, msg, basis);
             if (rc) return fail(rc, msg);
             st->pending_basis = -1;
         } else {
@@ -963,7 +974,6 @@ int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paul
             rc = upload_plan(st, Q, st->plan_buf, &dp, &ds, &dop);
             if (!rc) rc = launch_pass(st, Q, 0, dp, ds, dop);
             if (rc) return rc;
-            ++interpreted;
         }
         tm.end();
         ++launches;
@@ -977,8 +987,50 @@ int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paul
         stats->launches += launches;
         stats->algorithmic_bytes += (double)launches * 32.0 * (double)st->size();
     }
-    (void)interpreted;
+    if (probe) {
+        if (fused_probe) {
+            pmeasure_finish_small<<<1u << probe_m, 256, 0, st->stream>>>(st->work, pgrid, 1 << probe_m, probe_table);
+            CUDA_TRY(cudaGetLastError());
+        } else {
+            return qsv_pmeasure_async(st, probe, probe_m, probe_table);
+        }
+    }
     return QSV_OK;
+}
+
+int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
+                            const qsv_options *opt, qsv_run_stats *stats) {
+    if (n_paulis <= 0) return qsv_plan_execute(st, plan, opt, stats);
+    Plan &P = plan->p;
+    if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    PauliPlacement pl;
+    std::string msg;
+    rc = place_paulis(P, paulis, n_paulis, pl, msg);
+    if (rc) return fail(rc, msg);
+    return execute_with_paulis(st, P, pl, n_paulis, opt, stats, nullptr, 0, nullptr);
+}
+
+int qsv_plan_execute_probe(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
+                           const int32_t *probe_qubits_msb_first, int m, double *device_table, const qsv_options *opt,
+                           qsv_run_stats *stats) {
+    Plan &P = plan->p;
+    if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
+    if (m < 1 || m > 4) return fail(QSV_E_UNSUPPORTED, "probe tables take 1..4 qubits");
+    for (int p = 0; p < m; ++p)
+        if (probe_qubits_msb_first[p] < 0 || probe_qubits_msb_first[p] >= st->n)
+            return fail(QSV_E_PARSE, "probe qubit out of range");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    if (use_supers(P)) return fail(QSV_E_UNSUPPORTED, "plan uses super-passes");
+    PauliPlacement pl;
+    std::string msg;
+    if (n_paulis > 0) {
+        rc = place_paulis(P, paulis, n_paulis, pl, msg);
+        if (rc) return fail(rc, msg);
+    }
+    return execute_with_paulis(st, P, pl, n_paulis, opt, stats, probe_qubits_msb_first, m, device_table);
 }
 
 int qsv_plan_pauli_stream(const qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis, qsv_gate *out,

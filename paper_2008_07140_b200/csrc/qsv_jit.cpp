@@ -936,7 +936,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
                       const std::function<std::string(const std::string &)> &base_of, bool stream_out = true,
                       bool basis_param = false, bool prefetch = true, double scale_in = 1.0,
                       bool final_pass = true, double *scale_out = nullptr, int gang = 1, uint64_t xmask = 0,
-                      bool tma = false) {
+                      bool tma = false, const std::vector<int> *probe = nullptr) {
     double fp64 = 0;
     double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
@@ -1161,6 +1161,43 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
         g.flush_all(sigma, final_pass && last);
         fp64 += g.fp64;
+        if (probe && last && !host) {
+            // probe-out pass: |amp|^2 of the final amplitudes accumulated per
+            // probe key (first probe qubit = MSB) while they are stored; the
+            // register-qubit part of the key is compile-time per amplitude
+            const int M = (int)probe->size(), B = 1 << M;
+            std::vector<std::pair<int, int>> regbits;  // (probe index, register position)
+            for (int i = 0; i < M; ++i)
+                for (int k = 0; k < R; ++k)
+                    if (g.regq[k] == (*probe)[i]) regbits.push_back({i, k});
+            const int K = 1 << regbits.size();
+            unsigned regmask = 0;
+            for (auto &e : regbits) regmask |= 1u << (M - 1 - e.first);
+            o << "    " << guard << "{\n    double pk0 = 0.0";
+            for (int kr = 1; kr < K; ++kr) o << ", pk" << kr << " = 0.0";
+            o << ";\n";
+            for (int rho = 0; rho < (1 << R); ++rho) {
+                int kr = 0;
+                for (size_t e = 0; e < regbits.size(); ++e) kr |= ((rho >> regbits[e].second) & 1) << e;
+                o << "    pk" << kr << " = fma(v" << rho << ".x, v" << rho << ".x, fma(v" << rho << ".y, v" << rho
+                  << ".y, pk" << kr << "));\n";
+            }
+            o << "    const u64 pib = base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+            o << "    const unsigned kt = 0u";
+            for (int i = 0; i < M; ++i)
+                if (!((regmask >> (M - 1 - i)) & 1))
+                    o << " | ((unsigned)((pib >> " << (*probe)[i] << ") & 1ull) << " << (M - 1 - i) << ")";
+            o << ";\n";
+            for (int kr = 0; kr < K; ++kr) {
+                unsigned KR = 0;
+                for (size_t e = 0; e < regbits.size(); ++e)
+                    if ((kr >> e) & 1) KR |= 1u << (M - 1 - regbits[e].first);
+                for (int b = 0; b < B; ++b)
+                    if (((unsigned)b & regmask) == KR)
+                        o << "    pb" << b << " += kt == " << ((unsigned)b & ~regmask) << "u ? pk" << kr << " : 0.0;\n";
+            }
+            o << "    }\n";
+        }
         if (last && staged_out) {
             // each thread overwrites only the slots it read this stage; a
             // first stage read global memory, and the previous tile's last
@@ -1269,7 +1306,9 @@ const std::vector<double> &pass_scales(const Plan &P) {
     return P.jit_scale_in;
 }
 
-std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, uint64_t xmask) {
+std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, uint64_t xmask,
+                       const std::vector<int> *probe) {
+    if (host) probe = nullptr;
     const DevPass &dp = P.passes[pi];
     std::ostringstream o;
     o << "// libqsv specialised pass kernel: n=" << P.n << " m=" << dp.m << " R=" << P.r << " pass=" << pi << "\n";
@@ -1313,15 +1352,39 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     }
     std::string params = host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis";
     if (xmask) params += ", XDst xd";
+    if (probe) {
+        gang = 1;
+        params += ", double *__restrict__ probe_out";
+    }
     o << kernel_head(P, dp.m, host, "qsv_pass", params.c_str(), cost, gang);
+    const int PB = probe ? 1 << probe->size() : 0;
+    if (probe) {
+        o << "  // probe-out pass: qubits";
+        for (int q : *probe) o << " " << q;
+        o << "\n  double pb0 = 0.0";
+        for (int b = 1; b < PB; ++b) o << ", pb" << b << " = 0.0";
+        o << ";\n";
+    }
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
     const char *e = std::getenv("QSV_JIT_PREFETCH");
     const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
-                                    sc, final_pass, nullptr, gang, xmask, tma && !xmask);
+                                    sc, final_pass, nullptr, gang, xmask, tma && !xmask && !probe, probe);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
+    if (probe) {
+        // per-CTA partials in a fixed order (warp tree, then warps in order)
+        o << "  {\n  __shared__ double qsv_pred[" << PB << "][32];\n";
+        o << "  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;\n";
+        for (int b = 0; b < PB; ++b)
+            o << "  { double s = pb" << b << "; for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);"
+              << " if (lane == 0) qsv_pred[" << b << "][wid] = s; }\n";
+        o << "  __syncthreads();\n";
+        o << "  if (threadIdx.x < " << PB << "u) { double s = 0.0;"
+          << " for (unsigned w = 0; w < (blockDim.x + 31u) / 32u; ++w) s += qsv_pred[threadIdx.x][w];"
+          << " probe_out[(size_t)blockIdx.x * " << PB << "u + threadIdx.x] = s; }\n  }\n";
+    }
     o << "}\n";
     return o.str();
 }
@@ -1635,10 +1698,39 @@ int jit_prepare(Plan &P, int device, std::string &err) {
 }
 
 // Exchange-out variant of one pass (compiled on demand, cached by source).
+int jit_variant_prepare(const Plan &P, int pass, const std::string &src, int device, void **fn, int *grid,
+                        std::string &err);
+
 int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, void **fn, int *grid, std::string &err) {
+    return jit_variant_prepare(P, pass, jit_source(P, pass, false, nullptr, xmask), device, fn, grid, err);
+}
+
+int jit_probe_prepare(const Plan &P, int pass, const std::vector<int> &probe, int device, void **fn, int *grid,
+                      std::string &err) {
+    return jit_variant_prepare(P, pass, jit_source(P, pass, false, nullptr, 0, &probe), device, fn, grid, err);
+}
+
+int jit_launch_probe(const Plan &P, int pass, void *fn, int grid, void *psi, int n, cudaStream_t stream,
+                     std::string &err, unsigned long long basis, double *probe_out) {
+    const int m = P.passes[pass].m, T = 1 << (m - P.r);
+    unsigned long long n_tiles = 1ull << (n - m);
+    void *args[] = {&psi, &n_tiles, &basis, &probe_out};
+    const CUresult r = driver().LaunchKernel((CUfunction)fn, (unsigned)grid, 1, 1, T, 1, 1, (unsigned)((size_t)16 << m),
+                                             (CUstream)stream, args, nullptr);
+    if (r != CUDA_SUCCESS) {
+        const char *s2 = nullptr;
+        driver().GetErrorString(r, &s2);
+        err = std::string("cuLaunchKernel (probe-out): ") + (s2 ? s2 : "?");
+        return QSV_E_DEVICE;
+    }
+    return QSV_OK;
+}
+
+// Compiles (disk cache, NVRTC) and loads a variant of one pass kernel; cached by source.
+int jit_variant_prepare(const Plan &P, int pass, const std::string &src, int device, void **fn, int *grid,
+                        std::string &err) {
     if (!jit_available(err)) return QSV_E_DEVICE;
     Driver &drv = driver();
-    const std::string src = jit_source(P, pass, false, nullptr, xmask);
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
         auto it = g_cache.find({device, src});
@@ -1654,7 +1746,7 @@ int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, vo
         std::string log;
         cubin = jit_compile_cubin(src, log);
         if (cubin.empty()) {
-            err = "NVRTC failed for the exchange-out pass: " + log;
+            err = "NVRTC failed for a pass-kernel variant: " + log;
             return QSV_E_DEVICE;
         }
         disk_cache_store(path, cubin);
@@ -1671,7 +1763,7 @@ int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, vo
     int per_sm = 0;
     if (r == CUDA_SUCCESS) r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 1 << (m - P.r), (size_t)smem);
     if (r != CUDA_SUCCESS || per_sm < 1) {
-        err = "loading the exchange-out pass kernel failed";
+        err = "loading a pass-kernel variant failed";
         return QSV_E_DEVICE;
     }
     int sms = 148;

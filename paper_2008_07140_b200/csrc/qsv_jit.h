@@ -25,7 +25,15 @@ bool jit_available(std::string &why);
 // CUDA source of the specialised kernel for pass `pass` of plan P (extern "C"
 // entry point `qsv_pass`).  Pure host code (testable without a GPU).
 std::string jit_source(const Plan &P, int pass, bool host = false, double *fp64_per_amp = nullptr,
-                       uint64_t xmask = 0);
+                       uint64_t xmask = 0, const std::vector<int> *probe = nullptr);
+
+// Probe-out variant of pass `pass`: the |amp|^2 of its outputs accumulated per key
+// over `probe` (first = MSB) into per-CTA partials probe_out[grid][2^|probe|]; the
+// launch uses exactly `grid` CTAs (the caller sizes the partials and the finish).
+int jit_probe_prepare(const Plan &P, int pass, const std::vector<int> &probe, int device, void **fn, int *grid,
+                      std::string &err);
+int jit_launch_probe(const Plan &P, int pass, void *fn, int grid, void *psi, int n, cudaStream_t stream,
+                     std::string &err, unsigned long long basis, double *probe_out);
 
 // Exchange-out variant of pass `pass` (xmask = exchanged positions, all tile-base
 // bits of that pass): stores go to dst8[bits at xmask] + (index with those bits

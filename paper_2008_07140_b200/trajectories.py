@@ -108,27 +108,31 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             state = states[unique % len(states)]
             state.set_basis(0)
             stats = N.qsv_run_stats()
-            if n_err == 0:
-                N.check(L.qsv_plan_execute(state.handle, clean_plan, C.byref(opts_clean), C.byref(stats)))
+            pa = np.zeros(n_err, dtype=N.PAULI_DTYPE)
+            k2 = 0
+            for idx, picks in ins.items():
+                for q, g in picks:
+                    pa[k2] = (gate_index[idx], q, "IXYZ".index(g))
+                    k2 += 1
+            if async_tables:
+                # the plan's last pass accumulates the probe table while it
+                # stores (no extra read of the state)
+                rc = L.qsv_plan_execute_probe(state.handle, clean_plan, pa.ctypes.data, n_err, pq.ctypes.data,
+                                              len(pq), C.c_void_p(dev_tables[k].data_ptr()), C.byref(opts_clean),
+                                              C.byref(stats))
             else:
-                pa = np.zeros(n_err, dtype=N.PAULI_DTYPE)
-                k2 = 0
-                for idx, picks in ins.items():
-                    for q, g in picks:
-                        pa[k2] = (gate_index[idx], q, "IXYZ".index(g))
-                        k2 += 1
                 rc = L.qsv_plan_execute_paulis(state.handle, clean_plan, pa.ctypes.data, n_err, C.byref(opts_clean),
                                                C.byref(stats))
-                if rc == N.QSV_E_UNSUPPORTED:
-                    noisy = noisy_trajectory_program(program, p, seed)
-                    rec = SV.compile_gates([i for i in noisy.instructions if i.is_gate])
-                    rc = L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats))
-                N.check(rc)
+            if rc == N.QSV_E_UNSUPPORTED:
+                noisy = noisy_trajectory_program(program, p, seed)
+                rec = SV.compile_gates([i for i in noisy.instructions if i.is_gate])
+                rc = L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts_noisy), C.byref(stats))
+                if rc == 0 and async_tables:
+                    rc = L.qsv_pmeasure_async(state.handle, pq.ctypes.data, len(pq),
+                                              C.c_void_p(dev_tables[k].data_ptr()))
+            N.check(rc)
             unique += 1
-            if async_tables:
-                N.check(L.qsv_pmeasure_async(state.handle, pq.ctypes.data, len(pq),
-                                             C.c_void_p(dev_tables[k].data_ptr())))
-            else:
+            if not async_tables:
                 tables[k] = SV.pmeasure(state, pq)
             if t in keep:
                 kept[t] = state.amplitudes

@@ -350,3 +350,59 @@ def test_exchange_out_pass_single_process(positions):
     ref = O.run_full(prog).state.amplitudes
     assert_parity(recv.cpu().numpy(), ref)
     st.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("probe", [(0, 1, 2), (5,), (19, 3), (7, 0, 12, 18)])
+def test_probe_out_last_pass(probe):
+    """qsv_plan_execute_probe: the probe table accumulated by the last pass while
+    it stores (clean run and runs with Pauli errors) equals pmeasure of the
+    oracle's final state; the stored state is untouched by the probe."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2008_07140_b200 import _native as N
+
+    n = 20
+    prog = parse_program(workloads.rqc_for_qubits(n, 14, 8))
+    gl = prog.gate_instructions()
+    rec = SV.compile_gates(gl)
+    L = N.lib()
+    o = N.options()
+    plan = C.c_void_p()
+    N.check(L.qsv_plan_create(rec.ctypes.data, len(rec), n, C.byref(o), C.byref(plan)))
+    st = SV.init_state(n, max_qubits=n, device=0)
+    pq = np.asarray(probe, dtype=np.int32)
+    table = torch.zeros(1 << len(probe), dtype=torch.float64, device="cuda:0")
+    try:
+        for errs in ([], [(10, 3, 1)], [(len(gl) - 1, 0, 2), (40, 7, 3)]):
+            pa = np.zeros(len(errs), dtype=N.PAULI_DTYPE)
+            for i, e in enumerate(errs):
+                pa[i] = e
+            st.set_basis(0)
+            N.check(L.qsv_plan_execute_probe(st.handle, plan, pa.ctypes.data, len(pa), pq.ctypes.data, len(pq),
+                                             C.c_void_p(table.data_ptr()), C.byref(o), C.byref(N.qsv_run_stats())))
+            st.synchronize()
+            got = table.cpu().numpy()
+            by = {}
+            for g, q, k in errs:
+                by.setdefault(g, []).append(gates_mod_instruction("_XYZ"[k], q))
+            insts = []
+            for i, inst in enumerate(gl):
+                insts += by.get(i, [])
+                insts.append(inst)
+            from paper_2008_07140_b200.program import Program
+
+            ref = O.run_full(Program(n, prog.creg_count, tuple(insts))).state
+            assert np.abs(got - O.pmeasure(ref, probe)).max() <= 1e-12, (probe, errs)
+            assert_parity(st.amplitudes, ref.amplitudes)
+    finally:
+        L.qsv_plan_destroy(plan)
+        st.close()
+
+
+def gates_mod_instruction(name, q):
+    from paper_2008_07140_b200.program import Instruction
+
+    return Instruction(name, (q,))
