@@ -211,6 +211,23 @@ class CudaShard:
         self.N.check(self.N.lib().qsv_norm_sq(self.h, C.byref(out)))
         return out.value
 
+    def pmeasure_local(self, positions) -> np.ndarray:
+        q = np.asarray(positions, dtype=np.int32)
+        table = np.empty(1 << q.size)
+        self.N.check(self.N.lib().qsv_pmeasure(self.h, q.ctypes.data, int(q.size), table.ctypes.data))
+        return table
+
+    def prob_bit0(self, position: int) -> float:
+        out = C.c_double()
+        self.N.check(self.N.lib().qsv_prob_bit0(self.h, int(position), C.byref(out)))
+        return out.value
+
+    def collapse(self, position: int, outcome: int, scale: float):
+        self.N.check(self.N.lib().qsv_collapse(self.h, int(position), int(outcome), float(scale)))
+
+    def scale(self, s: float):
+        self.N.check(self.N.lib().qsv_scale(self.h, float(s)))
+
 
 # ---------------------------------------------------------------------------
 # transports
@@ -596,11 +613,24 @@ class ShardedSimulator:
         return rest
 
     # -- gate stream ------------------------------------------------------------
-    def run(self, program, stats: dict | None = None):
-        """Apply every gate of an expanded Program (MEASURE / PMEASURE are
-        not supported on the sharded path)."""
+    def run(self, program, stats: dict | None = None, rng=None):
+        """Execute an expanded Program: gates (segment-planned, fused), and the
+        readouts PMEASURE (table appended to `self.tables`) and MEASURE
+        (collapse, bit into `self.cregs`; `rng` lives on rank 0, which draws
+        and broadcasts the outcome - the reference draws on its coordinator,
+        statevector.py:304)."""
+        self.cregs = [0] * program.creg_count
+        self.tables = []
         items = []
         for inst in program.instructions:
+            if inst.name in ("PMEASURE", "MEASURE"):
+                self._run_items(items, stats)
+                items = []
+                if inst.name == "PMEASURE":
+                    self.tables.append((inst.qubits, self.pmeasure(inst.qubits)))
+                else:
+                    self.cregs[inst.creg] = self.measure(inst.qubits[0], rng, inst.line)
+                continue
             if not inst.is_gate:
                 raise UnsupportedGate(f"{inst.name} is not supported on a sharded state", inst.line)
             u, targets, controls = gates.controlled_form(inst)
@@ -613,6 +643,10 @@ class ShardedSimulator:
                 self.stats.relabelled_swaps += 1
                 continue
             items.append((u, tuple(self.dq[t] for t in targets), tuple(self.dq[c] for c in controls)))
+        self._run_items(items, stats)
+
+    def _run_items(self, items, stats=None):
+        """Gates on DATA qubits: segment planning, exchanges, fused local runs."""
         if not items:
             self._materialize()
             return
@@ -648,6 +682,65 @@ class ShardedSimulator:
         self._flush(run, stats)
 
     # -- readout ----------------------------------------------------------------
+    def _allreduce(self, values) -> np.ndarray:
+        import torch
+
+        v = torch.tensor(np.asarray(values, dtype=np.float64), device=getattr(self.shard, "reduce_device", "cpu"))
+        self.dist.all_reduce(v, group=self.group)
+        return v.cpu().numpy()
+
+    def pmeasure(self, qubits) -> np.ndarray:
+        """Probability table over logical `qubits` (first listed = MSB,
+        statevector.py:311-328): each rank tabulates its shard over the probe
+        qubits that are local (global ones are fixed by its rank bits), the
+        tables are summed over ranks."""
+        self._materialize()
+        M = len(qubits)
+        pos = [self.perm[self.dq[q]] for q in qubits]
+        loc = [i for i, p in enumerate(pos) if p < self.n_local]
+        fixed = sum(self._rank_bit(p) << (M - 1 - i) for i, p in enumerate(pos) if p >= self.n_local)
+        part = self.shard.pmeasure_local([pos[i] for i in loc]) if loc else np.array([self.shard.norm_sq()])
+        full = np.zeros(1 << M)
+        for kl in range(len(part)):
+            key = fixed
+            for j, i in enumerate(loc):  # bit j of kl (MSB first over loc) -> probe bit i
+                if (kl >> (len(loc) - 1 - j)) & 1:
+                    key |= 1 << (M - 1 - i)
+            full[key] = part[kl]
+        return self._allreduce(full)
+
+    def measure(self, qubit: int, rng, line: int = 0) -> int:
+        """MEASURE (statevector.py:298-308): global bit-0 probability, outcome
+        drawn on rank 0 and broadcast, collapse + renormalisation per rank."""
+        import torch
+
+        from .errors import DegenerateState
+
+        if rng is None and self.rank == 0:
+            raise UnsupportedGate("MEASURE needs a random stream", line)
+        self._materialize()
+        p = self.perm[self.dq[qubit]]
+        norm = self.shard.norm_sq()
+        if p < self.n_local:
+            p0 = self.shard.prob_bit0(p)
+        else:
+            p0 = norm if self._rank_bit(p) == 0 else 0.0
+        p0, tot = self._allreduce([p0, norm])
+        p1 = tot - p0
+        if p0 < 1e-12 and p1 < 1e-12:
+            raise DegenerateState(f"both outcomes of qubit {qubit} have ~zero probability")
+        out = torch.tensor([0], dtype=torch.int64, device=getattr(self.shard, "reduce_device", "cpu"))
+        if self.rank == 0:
+            out[0] = 0 if rng.random() < p0 else 1
+        self.dist.broadcast(out, src=0, group=self.group)
+        outcome = int(out.item())
+        scale = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
+        if p < self.n_local:
+            self.shard.collapse(p, outcome, scale)
+        else:
+            self.shard.scale(scale if self._rank_bit(p) == outcome else 0.0)
+        return outcome
+
     def norm_sq(self) -> float:
         import torch
 

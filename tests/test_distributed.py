@@ -58,6 +58,24 @@ class OracleShard:
     def norm_sq(self):
         return float(np.vdot(self.buf, self.buf).real)
 
+    def pmeasure_local(self, positions):
+        st = O.OracleState(self.n_local, self.buf, 0)
+        return O.pmeasure(st, tuple(positions))
+
+    def prob_bit0(self, position):
+        idx = np.arange(self.buf.size)
+        a = self.buf[((idx >> position) & 1) == 0]
+        return float(np.vdot(a, a).real)
+
+    def collapse(self, position, outcome, scale):
+        idx = np.arange(self.buf.size)
+        keep = ((idx >> position) & 1) == outcome
+        self.buf[~keep] = 0
+        self.buf[keep] *= scale
+
+    def scale(self, s):
+        self.buf *= s
+
 
 def _worker(rank, world, port, cases, out_path, chunk_log2=0):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -176,3 +194,41 @@ def test_segment_planner_c3_shapes():
         O.apply_gate(st, *items[i])
     ref = O.run_full(prog).state.amplitudes
     assert np.abs(st.amplitudes - ref).max() <= 1e-12
+
+
+def _readout_worker(rank, world, port, text, seed, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        prog = parse_program(text)
+        n = prog.qubit_count
+        g = world.bit_length() - 1
+        sim = ShardedSimulator(n, OracleShard(n - g), chunk_log2=1)
+        sim.set_basis(0)
+        sim.run(prog, rng=np.random.default_rng(seed) if rank == 0 else None)
+        amps = sim.gather_amplitudes()
+        if rank == 0:
+            np.save(out_path, np.array([(amps, sim.cregs, sim.tables)], dtype=object), allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_readout_matches_oracle(world, tmp_path):
+    """PMEASURE and MEASURE on a sharded state (tables summed over ranks,
+    outcome drawn on rank 0 and broadcast, per-rank collapse) vs the oracle's
+    run_full with the same random stream."""
+    n = 9
+    body = workloads.rqc_for_qubits(n, 8, 3)
+    extra = "PMEASURE 0,8,4\nMEASURE 8,$0\nH 8\nCNOT 8,2\nPMEASURE 8,2\nMEASURE 2,$1\nMEASURE 0,$2\nPMEASURE 1,0,8,2\n"
+    text = body.replace(f"QINIT {n}", f"QINIT {n}\nCREG 3", 1) + extra
+    prog = parse_program(text)
+    out = str(tmp_path / "ro.npy")
+    mp.spawn(_readout_worker, args=(world, _free_port(), text, 11, out), nprocs=world, join=True)
+    amps, cregs, tables = np.load(out, allow_pickle=True)[0]
+    ref = O.run_full(prog, np.random.default_rng(11))
+    assert list(cregs) == list(ref.cregs)
+    assert len(tables) == len(ref.tables)
+    for (q, t), (q2, t2) in zip(tables, ref.tables):
+        assert tuple(q) == tuple(q2) and np.abs(t - t2).max() <= 1e-12
+    assert np.abs(amps - ref.state.amplitudes).max() <= 1e-12

@@ -245,6 +245,11 @@ def test_trajectories_full_size_c5():
         assert_parity(rep.kept[t], ref.state.amplitudes)
 
 
+# readouts on the sharded state too: tables summed over ranks, MEASURE drawn on rank 0
+_SHARDED_RQC = workloads.rqc_for_qubits(16, 12, 4).replace("QINIT 16", "QINIT 16\nCREG 2", 1) + (
+    "PMEASURE 0,15,7\nMEASURE 15,$0\nH 15\nPMEASURE 15,3\nMEASURE 3,$1\n")
+
+
 def _sharded_gpu_worker(rank, world, port, out, transport):
     import os
 
@@ -258,7 +263,7 @@ def _sharded_gpu_worker(rank, world, port, out, transport):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         res = {}
-        for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
+        for name, text in (("rqc", _SHARDED_RQC), ("qft", workloads.qft_text(15, True))):
             prog = parse_program(text)
             g = world.bit_length() - 1
             kind, _, variant = transport.partition("-")
@@ -271,10 +276,11 @@ def _sharded_gpu_worker(rank, world, port, out, transport):
             sim.fuse_exchange = variant == "fused"
             for _ in range(2):  # twice: the second run reuses buffers, handles and plans
                 sim.set_basis(1)
-                sim.run(prog)
+                sim.run(prog, rng=np.random.default_rng(5) if rank == 0 else None)
             amps = sim.gather_amplitudes()
             if rank == 0:
-                res[name] = (amps, len(sim.stats.swaps), sum(x.fused for x in sim.stats.swaps))
+                res[name] = (amps, len(sim.stats.swaps), sum(x.fused for x in sim.stats.swaps), sim.cregs,
+                             [t for _, t in sim.tables])
             if hasattr(tr, "close"):
                 tr.close()
             dist.barrier()
@@ -303,14 +309,18 @@ def test_sharded_path_on_gpu(world, transport, tmp_path):
     out = str(tmp_path / "sharded.npy")
     mp.spawn(_sharded_gpu_worker, args=(world, port, out, transport), nprocs=world, join=True)
     res = np.load(out, allow_pickle=True)[0]
-    for name, text in (("rqc", workloads.rqc_for_qubits(16, 12, 4)), ("qft", workloads.qft_text(15, True))):
+    for name, text in (("rqc", _SHARDED_RQC), ("qft", workloads.qft_text(15, True))):
         prog = parse_program(text)
         init = np.zeros(1 << prog.qubit_count, complex)
         init[1] = 1
-        ref = O.run_full(prog, initial=init).state.amplitudes
-        amps, swaps, fused = res[name]
+        ref_run = O.run_full(prog, np.random.default_rng(5), initial=init)
+        ref = ref_run.state.amplitudes
+        amps, swaps, fused, cregs, tables = res[name]
         assert swaps > 0
         assert_parity(amps, ref)
+        assert list(cregs) == list(ref_run.cregs)
+        for t, (_, t2) in zip(tables, ref_run.tables):
+            assert np.abs(t - t2).max() <= 1e-12
     if transport.endswith("fused"):
         assert sum(res[k][2] for k in res) > 0  # at least one exchange rode on a pass's stores
 
