@@ -144,14 +144,39 @@ struct LaunchTimer {
 
 size_t pass_smem_bytes(int m) { return ((size_t)16 << m) + sizeof(uint64_t) * ((1 << kLoTabBits) + (1 << kHiTabBits)); }
 
-template <int R>
-int configure_pass_kernel() {
+constexpr size_t kMaxSmemOps = (size_t)64 << 10;  // op records staged in shared memory up to this size
+
+template <int R, bool SO>
+int configure_pass_kernel(int *per_sm, size_t smem, int threads) {
     static bool done = false;
     if (!done) {
-        CUDA_TRY(cudaFuncSetAttribute(pass_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)pass_smem_bytes(kMaxTileQubits)));
+        CUDA_TRY(cudaFuncSetAttribute(pass_kernel<R, SO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(pass_smem_bytes(kMaxTileQubits) + (SO ? kMaxSmemOps : 0))));
         done = true;
     }
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, pass_kernel<R, SO>, threads, smem));
+    return QSV_OK;
+}
+
+template <int R>
+int launch_pass_r(qsv_state *st, const Plan &P, int pass_idx, const DevPass *pp, const DevStage *d_st,
+                  const DevOp *d_ops, uint64_t n_tiles, int threads) {
+    const DevPass &hp = P.passes[pass_idx];
+    const size_t n_ops = (size_t)(P.stages[hp.stage_end - 1].op_end - P.stages[hp.stage_begin].op_begin);
+    const size_t ops_bytes = n_ops * sizeof(DevOp);
+    const bool so = ops_bytes <= kMaxSmemOps;
+    const size_t smem = pass_smem_bytes(P.m) + (so ? ops_bytes : 0);
+    int per_sm = 1;
+    const int rc = so ? configure_pass_kernel<R, true>(&per_sm, smem, threads)
+                      : configure_pass_kernel<R, false>(&per_sm, smem, threads);
+    if (rc) return rc;
+    // one CTA per tile (a persistent grid measured slower when another
+    // stream's pass kernels share the GPU: CTAs that cannot become resident
+    // early leave their tiles to a few; the op records come from L2)
+    (void)per_sm;
+    const uint64_t grid = std::min<uint64_t>(n_tiles, 0x7fffffffull);
+    if (so) pass_kernel<R, true><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles);
+    else pass_kernel<R, false><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles);
     return QSV_OK;
 }
 
@@ -160,15 +185,13 @@ int launch_pass(qsv_state *st, const Plan &P, int pass_idx, const DevPass *d_pas
     const int m = P.m, r = P.r;
     const uint64_t n_tiles = 1ull << (st->n - m);
     const int threads = 1 << (m - r);
-    const uint64_t grid = std::min<uint64_t>(n_tiles, 0x7fffffffull);
-    const size_t smem = pass_smem_bytes(m);
     const DevPass *pp = d_pass + pass_idx;
     int rc = QSV_OK;
     switch (r) {
-        case 1: rc = configure_pass_kernel<1>(); if (!rc) pass_kernel<1><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
-        case 2: rc = configure_pass_kernel<2>(); if (!rc) pass_kernel<2><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
-        case 3: rc = configure_pass_kernel<3>(); if (!rc) pass_kernel<3><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
-        case 4: rc = configure_pass_kernel<4>(); if (!rc) pass_kernel<4><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles); break;
+        case 1: rc = launch_pass_r<1>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
+        case 2: rc = launch_pass_r<2>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
+        case 3: rc = launch_pass_r<3>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
+        case 4: rc = launch_pass_r<4>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
         default: return fail(QSV_E_UNSUPPORTED, "register qubits must be 1..4");
     }
     if (rc) return rc;

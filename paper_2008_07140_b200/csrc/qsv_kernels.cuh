@@ -35,15 +35,15 @@ __device__ __forceinline__ double2 cdot2(double2 u0, double2 x0, double2 u1, dou
     return make_double2(re, im);
 }
 
-__device__ __forceinline__ double2 ldm(const double *m, int k) {
-    return make_double2(__ldg(m + 2 * k), __ldg(m + 2 * k + 1));
-}
+// op records are read through generic pointers: the pass kernel stages its
+// ops in shared memory (uniform broadcast reads), or reads them from global
+__device__ __forceinline__ double2 ldm(const double *m, int k) { return make_double2(m[2 * k], m[2 * k + 1]); }
 
 // matrix entry load the compiler may not hoist out of a loop (keeps register
 // pressure bounded for dense 4x4 ops; the entries stay L1-resident)
 __device__ __forceinline__ double2 ldm_v(const double *m, int k) {
     double2 r;
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(m + 2 * k));
+    asm volatile("ld.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(m + 2 * k));
     return r;
 }
 
@@ -112,12 +112,12 @@ template <int V>
 __device__ __forceinline__ void mat1_pair(double2 &x0, double2 &x1, const double *m) {
     const double2 a = x0, b = x1;
     if constexpr (V == V_REAL) {
-        const double u00 = __ldg(m + 0), u01 = __ldg(m + 2), u10 = __ldg(m + 4), u11 = __ldg(m + 6);
+        const double u00 = m[0], u01 = m[2], u10 = m[4], u11 = m[6];
         x0 = make_double2(fma(u01, b.x, u00 * a.x), fma(u01, b.y, u00 * a.y));
         x1 = make_double2(fma(u11, b.x, u10 * a.x), fma(u11, b.y, u10 * a.y));
     } else if constexpr (V == V_RXL) {
         // [[p, i q], [i r, s]] with p, q, r, s real
-        const double p = __ldg(m + 0), q = __ldg(m + 3), r = __ldg(m + 5), t = __ldg(m + 6);
+        const double p = m[0], q = m[3], r = m[5], t = m[6];
         x0 = make_double2(fma(-q, b.y, p * a.x), fma(q, b.x, p * a.y));
         x1 = make_double2(fma(t, b.x, -r * a.y), fma(t, b.y, r * a.x));
     } else {
@@ -285,8 +285,8 @@ __device__ __forceinline__ void apply_diag(uint32_t code, uint32_t rs, const dou
 
 template <int R>
 __device__ __forceinline__ void apply_op(const DevOp *op, double2 (&v)[1 << R], uint32_t tpart, uint64_t base) {
-    const uint4 h = __ldg(reinterpret_cast<const uint4 *>(op));
-    const uint64_t ec = __ldg(reinterpret_cast<const unsigned long long *>(op) + 2);
+    const uint4 h = *reinterpret_cast<const uint4 *>(op);
+    const uint64_t ec = *(reinterpret_cast<const unsigned long long *>(op) + 2);
     const uint32_t code = h.x, rs = h.y, tc = h.z;
     if ((tpart & tc) != tc || (base & ec) != ec) return;  // a scalar control is 0 for this thread
     const uint32_t kind = code & 15, rc = rs & 0xff;
@@ -308,10 +308,13 @@ __device__ __forceinline__ void apply_op(const DevOp *op, double2 (&v)[1 << R], 
 // applies the stage's ops in registers and scatters them back; the last
 // stage's result streams back to HBM.  Tiles are independent (disjoint index
 // sets), so there is no inter-CTA communication and no atomics.
-template <int R>
+// SMEM_OPS: the pass's op records are staged in shared memory once per
+// (persistent) CTA and read as uniform broadcasts (global L1 reads per op and
+// thread were the interpreter's main stall, long_scoreboard ~4 per issue)
+template <int R, bool SMEM_OPS>
 __global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, const DevPass *__restrict__ pass,
                                                    const DevStage *__restrict__ stages,
-                                                   const DevOp *__restrict__ ops, uint64_t n_tiles) {
+                                                   const DevOp *__restrict__ ops_g, uint64_t n_tiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = pass->m;
     const uint32_t nloc = 1u << m;
@@ -323,6 +326,16 @@ __global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, co
     for (uint32_t e = threadIdx.x; e < (1u << kLoTabBits); e += T) lo_tab[e] = pass->lo_tab[e];
     for (uint32_t e = threadIdx.x; e < (1u << kHiTabBits); e += T) hi_tab[e] = pass->hi_tab[e];
     const int sb = pass->stage_begin, se = pass->stage_end;
+    const DevOp *ops = ops_g;
+    if constexpr (SMEM_OPS) {
+        const int o0 = stages[sb].op_begin, o1 = stages[se - 1].op_end;
+        DevOp *ops_s = reinterpret_cast<DevOp *>(hi_tab + (1 << kHiTabBits));
+        const uint4 *src = reinterpret_cast<const uint4 *>(ops_g + o0);
+        uint4 *dst = reinterpret_cast<uint4 *>(ops_s);
+        const uint32_t words = (uint32_t)(o1 - o0) * (uint32_t)(sizeof(DevOp) / 16);
+        for (uint32_t w = threadIdx.x; w < words; w += T) dst[w] = src[w];
+        ops = ops_s - o0;  // ops[o] for o in [o0, o1)
+    }
 
     for (uint64_t tile_id = blockIdx.x; tile_id < n_tiles; tile_id += gridDim.x) {
         uint64_t base = tile_id;
