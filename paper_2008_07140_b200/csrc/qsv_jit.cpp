@@ -1368,8 +1368,12 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
+    // (with one CTA per tile there is no next tile to prefetch: off unless the
+    // persistent grid is selected, QSV_JIT_GRID_TILES=0)
     const char *e = std::getenv("QSV_JIT_PREFETCH");
-    const bool prefetch = e ? std::atoi(e) != 0 : cost >= kPrefetchMinFp64;
+    const char *gt = std::getenv("QSV_JIT_GRID_TILES");
+    const bool persistent = gt && std::atoi(gt) == 0;
+    const bool prefetch = e ? std::atoi(e) != 0 : (persistent && cost >= kPrefetchMinFp64);
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
                                     sc, final_pass, nullptr, gang, xmask, tma && !xmask && !probe, probe);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);

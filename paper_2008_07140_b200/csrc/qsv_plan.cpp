@@ -35,7 +35,11 @@ void resolve_options(const qsv_options *opt, int n, int &m, int &r, int &L, int 
     // B200: fewer stages and barriers), 16 for the interpreted kernel
     const bool jit = opt ? (opt->jit > 0 || (opt->jit == 0 && n >= 16)) : n >= 16;
     r = (opt && opt->reg_qubits > 0) ? opt->reg_qubits : (jit ? 5 : 4);
-    L = (opt && opt->low_qubits > 0) ? opt->low_qubits : 5;
+    // forced low tile qubits: 3 keeps every warp access in full 128-byte lines
+    // and frees tile slots for gates (C2 10 -> 8 passes, 67.3 -> 64.6 ms; QFT
+    // 7 -> 5 passes, 47.8 -> 42.4 ms, with one CTA per tile); 5 was the
+    // default while the pass kernels ran persistent grids
+    L = (opt && opt->low_qubits > 0) ? opt->low_qubits : 3;
     m = std::min(std::min(m, kMaxTileQubits), n);
     r = std::max(std::min(std::min(r, kMaxRegQubits), m), std::min(2, m));
     m = std::min(m, r + 9);  // at most 512 threads per CTA (launch bound of pass_kernel)
