@@ -9,7 +9,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 out = ROOT / "profiles" / sys.argv[1]
-skip = int(sys.argv[sys.argv.index("--skip-full") + 1]) if "--skip-full" in sys.argv else 15
+skip = int(sys.argv[sys.argv.index("--skip-full") + 1]) if "--skip-full" in sys.argv else 11
 src = ROOT / "gpurun_out"
 out.mkdir(parents=True, exist_ok=True)
 

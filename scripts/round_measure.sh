@@ -6,7 +6,7 @@ timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_ful
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain_l.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1; echo "launches rc=$?"
 CMD1="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
-$CMD1 > gpurun_out/plain_f.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:qsv_pass -s ${NCU_SKIP_FULL:-15} -c 1 -o gpurun_out/prof_full -f $CMD1 > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
+$CMD1 > gpurun_out/plain_f.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:qsv_pass -s ${NCU_SKIP_FULL:-11} -c 1 -o gpurun_out/prof_full -f $CMD1 > gpurun_out/ncu_full.log 2>&1; echo "full rc=$?"
 # the other BASELINE configs on this one GPU (bench lines kept under profiles/<round>/)
 timeout 900 python bench.py --workload qft --no-e2e --no-cpu-baseline > gpurun_out/bench_qft.json 2>> gpurun_out/bench_full.err; echo "qft rc=$?"
 timeout 900 python bench.py --workload traj > gpurun_out/bench_traj.json 2>> gpurun_out/bench_full.err; echo "traj rc=$?"
