@@ -48,6 +48,9 @@ C2 = (5, 6, 24)
 SEED = 0
 
 
+FP64_PEAK_GINSTR = 18050.0  # DFMA lane-instructions/s (36.1 TFLOP/s measured)
+
+
 def measured_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu capture."""
     for p in sorted((ROOT / "profiles").glob("r*/traffic.json"), reverse=True):
@@ -322,6 +325,16 @@ def run_gpu(args) -> None:
     # gate touches the amplitudes whose controls are set (libqsv counts them)
     bytes_per_launch = (stats.algorithmic_bytes / max(1, launches)) if args.unfused else 32.0 * float(1 << n)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    # the specialised passes are FP64-issue-bound as much as HBM-bound: report
+    # the FP64 side too (generator's FP64 instruction count per amplitude per
+    # pass x 2^n, against the measured DFMA rate)
+    fp64_per_amp = 0.0
+    if not args.unfused:
+        for pi in range(int(info.passes)):
+            f = C.c_double()
+            if L.qsv_plan_pass_cost(plan, pi, C.byref(f)) == 0:
+                fp64_per_amp += f.value
+    fp64_rate = fp64_per_amp * float(1 << n) / (ms_step / 1e3)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"],
                 "traffic": args.traffic if args.traffic is not None else (
@@ -329,7 +342,11 @@ def run_gpu(args) -> None:
                 "peak_src": pk["src"],
                 "kernel": "qsv_pass (specialised fused pass)" if not args.unfused else "gate_kernel",
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
-                "kernel_share_of_step": stats.kernel_ms / total_ms}
+                "kernel_share_of_step": stats.kernel_ms / total_ms,
+                "fp64": None if args.unfused else {
+                    "instr_per_amplitude": fp64_per_amp, "achieved_ginstr_s": fp64_rate / 1e9,
+                    "peak_ginstr_s": FP64_PEAK_GINSTR, "frac": fp64_rate / 1e9 / FP64_PEAK_GINSTR,
+                    "peak_src": "scripts/fp64_pipes.cu: DFMA 36.1 TFLOP/s measured on B200 = 18.05e12 FP64 lane-instructions/s"}}
 
     # end to end through the public API: program text in, amplitudes out
     # (pinned host).  statevector.run_batch: every step parses the program,
