@@ -223,6 +223,12 @@ size_t plan_bytes(const Plan &P) {
 
 constexpr int kJitAutoQubits = 16;
 
+// register qubits chosen per pass (build_plan_auto) unless the caller fixed them
+inline bool auto_r_of(const qsv_options *opt, int n) {
+    const int jm = opt ? opt->jit : 0;
+    return !(opt && opt->reg_qubits > 0) && (jm > 0 || (jm == 0 && n >= kJitAutoQubits));
+}
+
 int ensure_barrier(qsv_state *st);
 
 int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, const qsv_options *opt,
@@ -515,7 +521,7 @@ int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const 
     int s;
     resolve_options(opt, n_qubits, m, r, L, s);
     auto p = std::make_unique<qsv_plan>();
-    p->p = build_plan(recs, n_qubits, m, r, L, s);
+    p->p = build_plan_auto(recs, n_qubits, m, r, L, s, auto_r_of(opt, n_qubits));
     *out = p.release();
     return QSV_OK;
 }
@@ -700,12 +706,12 @@ struct CachedPlan {
 };
 
 std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, const std::vector<GateRec> &recs,
-                                        int n, int m, int r, int L, int s, int jit, int device) {
+                                        int n, int m, int r, int L, int s, int jit, int device, bool auto_r = false) {
     static std::mutex mu;
     static std::list<std::shared_ptr<CachedPlan>> lru;
     constexpr size_t kEntries = 16;
     std::vector<unsigned char> key(sizeof(int) * 7 + sizeof(qsv_gate) * (size_t)n_gates);
-    const int head[7] = {n, m, r, L, s, jit, device};
+    const int head[7] = {n, m, r + (auto_r ? 100 : 0), L, s, jit, device};
     std::memcpy(key.data(), head, sizeof(head));
     std::memcpy(key.data() + sizeof(head), gates, sizeof(qsv_gate) * (size_t)n_gates);
     {
@@ -720,7 +726,7 @@ std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, 
     }
     auto e = std::make_shared<CachedPlan>();
     e->key.swap(key);
-    e->plan = build_plan(recs, n, m, r, L, s);
+    e->plan = build_plan_auto(recs, n, m, r, L, s, auto_r);
     std::lock_guard<std::mutex> lk(mu);
     lru.push_front(e);
     if (lru.size() > kEntries) lru.pop_back();
@@ -764,7 +770,7 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     int s;
     resolve_options(opt, st->n, m, r, L, s);
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, opt ? opt->jit : 0,
-                                                 st->device);
+                                                 st->device, auto_r_of(opt, st->n));
     Plan &P = cp->plan;
     bool jit_ready = false;
     {
@@ -1125,7 +1131,8 @@ int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, 
     if (!jit_available(why)) return QSV_OK;
     int m, r, L, sq;
     resolve_options(opt, st->n, m, r, L, sq);
-    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, jm, st->device);
+    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, jm, st->device,
+                                                 auto_r_of(opt, st->n));
     const Plan &P = cp->plan;
     *out = !use_supers(P) && !P.passes.empty() && positions && !(positions >> st->n);
     return QSV_OK;
@@ -1145,7 +1152,7 @@ int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, cons
     int m, r, L, sq;
     resolve_options(opt, st->n, m, r, L, sq);
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, opt ? opt->jit : 0,
-                                                 st->device);
+                                                 st->device, auto_r_of(opt, st->n));
     Plan &P = cp->plan;
     const int last = (int)P.passes.size() - 1;
     if (use_supers(P) || last < 0) return fail(QSV_E_UNSUPPORTED, "plan uses super-passes");

@@ -940,7 +940,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     double fp64 = 0;
     double sigma = scale_in;  // stored amplitudes = true amplitudes / sigma (see StageGen::flush_all)
     const DevPass &dp = P.passes[pi];
-    const int m = dp.m, R = P.r;
+    const int m = dp.m, R = pass_r(P, pi);
     std::vector<int> tq(dp.tq, dp.tq + m);
     const std::string thread_loop = host ? "    for (unsigned tid = 0; tid < " + std::to_string(1 << (m - R)) + "u; ++tid) {\n" : "";
     const std::string thread_end = host ? "    }\n" : "";
@@ -1248,9 +1248,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
 constexpr double kThreeCtaMinFp64 = 60.0;
 
 std::string kernel_head(const Plan &P, int m, bool host, const char *name, const char *params,
-                        double fp64_per_amp = 0, int gang = 1) {
+                        double fp64_per_amp = 0, int gang = 1, int r = 0) {
     std::ostringstream o;
-    const int T = 1 << (m - P.r);
+    if (r <= 0) r = P.r;
+    const int T = 1 << (m - r);
     if (host) {
         o << kHostPrelude << "extern \"C\" void " << name << "_host(" << params << ") {\n";
         o << "  static double2 tile[" << (1 << m) << "];\n";
@@ -1271,7 +1272,7 @@ std::string kernel_head(const Plan &P, int m, bool host, const char *name, const
             o << "extern \"C\" __global__ void __launch_bounds__(" << gang * T << ", 1) " << name << "(" << params
               << ") {\n";
             o << "  extern __shared__ double2 smem[];\n";
-            o << "  const unsigned tid = threadIdx.x & " << (T - 1) << "u, sub = threadIdx.x >> " << (m - P.r) << ";\n";
+            o << "  const unsigned tid = threadIdx.x & " << (T - 1) << "u, sub = threadIdx.x >> " << (m - r) << ";\n";
             o << "  double2 *tile = smem + ((size_t)sub << " << m << ");\n";
         } else {
         o << "extern \"C\" __global__ void __launch_bounds__(" << T << ", "
@@ -1311,7 +1312,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     if (host) probe = nullptr;
     const DevPass &dp = P.passes[pi];
     std::ostringstream o;
-    o << "// libqsv specialised pass kernel: n=" << P.n << " m=" << dp.m << " R=" << P.r << " pass=" << pi << "\n";
+    o << "// libqsv specialised pass kernel: n=" << P.n << " m=" << dp.m << " R=" << pass_r(P, pi) << " pass=" << pi << "\n";
     std::vector<int> ext;
     for (int q = 0; q < P.n; ++q)
         if (!((dp.tile_mask >> q) & 1)) ext.push_back(q);
@@ -1323,7 +1324,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     {
         std::ostringstream dry;
         cost = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
-               (double)(1 << P.r);
+               (double)(1 << pass_r(P, pi));
     }
     // QSV_JIT_GANG=G: compute-bound passes run G tiles per CTA in lock step
     // (one CTA per SM) instead of independent CTAs; QSV_JIT_TMA=1: their
@@ -1332,7 +1333,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     bool tma = false;
     if (!host) {
         static const int env_gang = std::getenv("QSV_JIT_GANG") ? std::atoi(std::getenv("QSV_JIT_GANG")) : 1;
-        const int T = 1 << (dp.m - P.r);
+        const int T = 1 << (dp.m - pass_r(P, pi));
         static const double gang_min =
             std::getenv("QSV_JIT_GANG_MIN") ? std::atof(std::getenv("QSV_JIT_GANG_MIN")) : kThreeCtaMinFp64;
         if (env_gang > 1 && cost >= gang_min && env_gang * T <= 1024 &&
@@ -1356,7 +1357,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
         gang = 1;
         params += ", double *__restrict__ probe_out";
     }
-    o << kernel_head(P, dp.m, host, "qsv_pass", params.c_str(), cost, gang);
+    o << kernel_head(P, dp.m, host, "qsv_pass", params.c_str(), cost, gang, pass_r(P, pi));
     const int PB = probe ? 1 << probe->size() : 0;
     if (probe) {
         o << "  // probe-out pass: qubits";
@@ -1376,7 +1377,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     const bool prefetch = e ? std::atoi(e) != 0 : (persistent && cost >= kPrefetchMinFp64);
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
                                     sc, final_pass, nullptr, gang, xmask, tma && !xmask && !probe, probe);
-    if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << P.r);
+    if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << pass_r(P, pi));
     if (probe) {
         // per-CTA partials in a fixed order (warp tree, then warps in order)
         o << "  {\n  __shared__ double qsv_pred[" << PB << "][32];\n";
@@ -1391,6 +1392,47 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     }
     o << "}\n";
     return o.str();
+}
+
+// Register qubits per pass.  32 amplitudes per thread (r = 5) needs the
+// fewest stages, but its straight-line code is twice as long per thread as
+// r = 4 and the three CTAs per SM then stall on instruction fetch; with one CTA
+// per tile, r = 4 measured faster on every C2 pass whose FP64 work it does not
+// raise (7.0-9.1 vs 7.9-9.5 ms, same FP64/amp), while QFT passes, whose extra
+// stages cost FP64 at r = 4 (+27-45 %), stay faster at r = 5.  Both
+// stagings of the same passes are generated and each pass takes r = 4 when its
+// FP64 work per amplitude is within kR4CostRatio of the r = 5 staging.
+constexpr double kR4CostRatio = 1.10;
+
+Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r) {
+    Plan P5 = build_plan(recs, n, m, r, L, s);
+    static const bool off = std::getenv("QSV_MIXED_R") && std::atoi(std::getenv("QSV_MIXED_R")) == 0;
+    if (off || !auto_r || r != 5 || P5.s != P5.m || P5.passes.empty()) return P5;
+    Plan P4 = build_plan(recs, n, m, 4, L, s);
+    if (P4.pass_gates != P5.pass_gates || P4.passes.size() != P5.passes.size()) return P5;
+    const int np = (int)P5.passes.size();
+    std::vector<int> rs(np, 5);
+    int n4 = 0;
+    for (int i = 0; i < np; ++i) {
+        double c5 = 0, c4 = 0;
+        jit_source(P5, i, false, &c5);
+        jit_source(P4, i, false, &c4);
+        if (c4 <= kR4CostRatio * c5) {
+            rs[i] = 4;
+            ++n4;
+        }
+    }
+    // QSV_MIXED_R_PATTERN (tests): e.g. "45" forces r = 4, 5, 4, 5, ... per pass
+    if (const char *pat = std::getenv("QSV_MIXED_R_PATTERN")) {
+        const std::string ps(pat);
+        if (!ps.empty()) {
+            n4 = 0;
+            for (int i = 0; i < np; ++i) n4 += (rs[i] = ps[i % ps.size()] == '4' ? 4 : 5) == 4;
+        }
+    }
+    if (n4 == 0) return P5;
+    if (n4 == np) return P4;
+    return rebuild_with_pass_r(P5, rs);
 }
 
 int super_batch(const Plan &P) {
@@ -1670,7 +1712,9 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
         int per_sm = 0;
         if (r == CUDA_SUCCESS)
-            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, gang << (u.m - P.r), (size_t)smem);
+            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn,
+                                                              gang << (u.m - (u.super ? P.r : pass_r(P, u.index))),
+                                                              (size_t)smem);
         if (r != CUDA_SUCCESS || per_sm < 1) {
             const char *s = nullptr;
             if (r != CUDA_SUCCESS) drv.GetErrorString(r, &s);
@@ -1716,7 +1760,7 @@ int jit_probe_prepare(const Plan &P, int pass, const std::vector<int> &probe, in
 
 int jit_launch_probe(const Plan &P, int pass, void *fn, int grid, void *psi, int n, cudaStream_t stream,
                      std::string &err, unsigned long long basis, double *probe_out) {
-    const int m = P.passes[pass].m, T = 1 << (m - P.r);
+    const int m = P.passes[pass].m, T = 1 << (m - pass_r(P, pass));
     unsigned long long n_tiles = 1ull << (n - m);
     void *args[] = {&psi, &n_tiles, &basis, &probe_out};
     const CUresult r = driver().LaunchKernel((CUfunction)fn, (unsigned)grid, 1, 1, T, 1, 1, (unsigned)((size_t)16 << m),
@@ -1765,7 +1809,8 @@ int jit_variant_prepare(const Plan &P, int pass, const std::string &src, int dev
     const int smem = (int)((size_t)16 << m);
     if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
     int per_sm = 0;
-    if (r == CUDA_SUCCESS) r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 1 << (m - P.r), (size_t)smem);
+    if (r == CUDA_SUCCESS)
+        r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 1 << (m - pass_r(P, pass)), (size_t)smem);
     if (r != CUDA_SUCCESS || per_sm < 1) {
         err = "loading a pass-kernel variant failed";
         return QSV_E_DEVICE;
@@ -1782,7 +1827,7 @@ int jit_variant_prepare(const Plan &P, int pass, const std::string &src, int dev
 int jit_launch_exchange(const Plan &P, int pass, void *fn, int grid_cap, void *psi, int n, cudaStream_t stream,
                         std::string &err, unsigned long long basis, const unsigned long long *dst8,
                         unsigned long long self_bits) {
-    const int m = P.passes[pass].m, T = 1 << (m - P.r);
+    const int m = P.passes[pass].m, T = 1 << (m - pass_r(P, pass));
     unsigned long long n_tiles = 1ull << (n - m);
     const unsigned grid = (unsigned)std::min<unsigned long long>(n_tiles, (unsigned long long)grid_cap);
     struct XDst {
@@ -1813,7 +1858,7 @@ static int cu_fail(CUresult r, const char *what, std::string &err) {
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
                unsigned long long basis) {
     const DevPass &dp = P.passes[pass];
-    const int m = dp.m, T = 1 << (m - P.r);
+    const int m = dp.m, T = 1 << (m - pass_r(P, pass));
     unsigned long long n_tiles = 1ull << (n - m);
     const int gang = pass < (int)P.jit_gangs.size() ? P.jit_gangs[pass] : 1;
     // One CTA per tile (group) by default: measured faster than the persistent

@@ -70,6 +70,10 @@ bool jit_double_buffer();
 // true when the plan's super-passes run as L2-resident persistent kernels
 bool use_supers(const Plan &P);
 
+// build_plan with the register qubits chosen per pass (r = 4 where it does not
+// add FP64 work, else r = 5) when auto_r and r = 5 (see qsv_jit.cpp)
+Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r);
+
 // The uniform scale every pass's specialised kernel expects the stored state
 // to carry (stored = true / scale); entry passes.size() is the plan's output (1).
 const std::vector<double> &pass_scales(const Plan &P);

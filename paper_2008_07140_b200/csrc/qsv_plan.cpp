@@ -476,8 +476,8 @@ void balance_passes(const std::vector<GateRec> &recs, std::vector<std::vector<in
 // The tile holds the forced low qubits plus the non-diagonal targets of
 // `taken`, padded with the lowest qubits of `pool` (the super-tile).
 void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int> &taken, uint64_t tile_res,
-               uint64_t pool) {
-    const int n = P.n, m = P.m, r = P.r;
+               uint64_t pool, int r_pass = 0) {
+    const int n = P.n, m = P.m, r = r_pass > 0 ? r_pass : P.r;
     uint64_t tmask = tile_res;
     for (int q = 0; q < n && popc(tmask) < m; ++q)
         if ((pool >> q) & 1) tmask |= 1ull << q;
@@ -486,6 +486,7 @@ void emit_pass(Plan &P, const std::vector<GateRec> &recs, const std::vector<int>
     std::memset(&dp, 0, sizeof(dp));
     dp.tile_mask = tmask;
     dp.m = m;
+    dp.r = r;
     {
         int j = 0;
         for (int q = 0; q < n; ++q)
@@ -784,6 +785,34 @@ void conjugate_pauli(GateRec &g, int q, int kind) {
     g.diag = diag;
     g.nmask = diag ? 0 : tmask;
     g.dmask = g.cmask | (diag ? tmask : 0);
+}
+
+Plan rebuild_with_pass_r(const Plan &B, const std::vector<int> &rs) {
+    Plan P;
+    P.recs = B.recs;
+    P.n = B.n;
+    P.m = B.m;
+    P.L = B.L;
+    P.s = B.s;
+    P.pass_budget = B.pass_budget;
+    P.gates = B.gates;
+    P.relabelled = B.relabelled;
+    P.r = 0;
+    for (int r : rs) P.r = std::max(P.r, r);
+    const std::vector<GateRec> recs = relabel_swaps(B.recs, B.n);
+    const uint64_t all = B.n >= 64 ? ~0ull : ((1ull << B.n) - 1);
+    for (size_t k = 0; k < B.passes.size(); ++k) {
+        SuperPass spp;
+        spp.mask = B.passes[k].tile_mask;
+        spp.pass_begin = (int32_t)P.passes.size();
+        emit_pass(P, recs, std::vector<int>(B.pass_gates[k].begin(), B.pass_gates[k].end()), B.passes[k].tile_mask,
+                  all, rs[k]);
+        P.pass_gates.push_back(B.pass_gates[k]);
+        spp.pass_end = (int32_t)P.passes.size();
+        P.supers.push_back(spp);
+    }
+    P.pass_op_begin.push_back((int64_t)P.ops.size());
+    return P;
 }
 
 // Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy

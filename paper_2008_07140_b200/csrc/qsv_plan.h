@@ -78,7 +78,7 @@ struct DevStage {
 
 struct alignas(16) DevPass {
     uint64_t tile_mask;
-    int32_t m, stage_begin, stage_end, pad;
+    int32_t m, stage_begin, stage_end, r;  // r: register qubits of this pass's stages
     int32_t tq[kMaxTileQubits + 3];         // local bit j <-> global qubit tq[j]
     uint64_t lo_tab[1 << kLoTabBits];       // offset of local bits [0,6)
     uint64_t hi_tab[1 << kHiTabBits];       // offset of local bits [6,m)
@@ -138,6 +138,16 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector
 
 // Builds the fused schedule.  m, r, L already clamped to the state size.
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s);
+
+// The same passes (tiles and gate sets) as the flat plan B, each re-staged with
+// its own number of register qubits rs[k] (P.r = max).
+Plan rebuild_with_pass_r(const Plan &B, const std::vector<int> &rs);
+
+// register qubits of pass pi's stages
+inline int pass_r(const Plan &P, int pi) {
+    const int r = P.passes[pi].r;
+    return r > 0 ? r : P.r;
+}
 
 // One pass over `tile_mask` applying recs[taken] (program order) with r
 // register qubits: the interpreted kernel's tables for a pass whose gates

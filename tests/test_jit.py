@@ -207,3 +207,17 @@ def test_exchange_out_pass_host(seed, n_pos):
     assert np.abs(got - ref).max() <= 1e-12
     written = sum(int(np.count_nonzero(d)) for d in dsts)
     assert written == np.count_nonzero(ref)
+
+
+@pytest.mark.parametrize("pattern", ["45", "54", "4", "5"])
+def test_mixed_register_qubits_per_pass(pattern, monkeypatch):
+    """Plans whose passes use different register-qubit counts (r = 4 / 5 per
+    pass, build_plan_auto): the per-pass kernels and the uniform-scale chain
+    across them, host rendering vs the oracle."""
+    monkeypatch.setenv("QSV_MIXED_R_PATTERN", pattern)
+    for text, seed in ((workloads.rqc_for_qubits(16, 14, 2), 3), (workloads.qft_text(16, round_trip=True), 4)):
+        prog = parse_program(text)
+        psi = workloads.gaussian_state(16, seed)
+        ref = O.run_full(prog, initial=psi).state.amplitudes
+        out = run_plan_host(compile_gates(prog.gate_instructions()), 16, psi, tile_qubits=9, jit=1)
+        assert np.abs(out - ref).max() <= 1e-12, pattern
