@@ -220,6 +220,20 @@ inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
 // registers and occupancy (2 CTAs/SM) hides the load latency.
 bool jit_double_buffer() { return false; }
 
+// One CTA per tile (default) or the persistent grid (QSV_JIT_GRID_TILES=0)
+bool jit_per_tile_grid() {
+    static const bool v = !std::getenv("QSV_JIT_GRID_TILES") || std::atoi(std::getenv("QSV_JIT_GRID_TILES")) != 0;
+    return v;
+}
+
+// L2 prefetch distance in tiles under one-CTA-per-tile grids (QSV_JIT_PREFETCH_DIST,
+// default 2 x 148: about one wave of resident CTAs ahead); 0 with persistent grids
+long gridDim_prefetch_distance() {
+    if (!jit_per_tile_grid()) return 0;
+    static const long d = std::getenv("QSV_JIT_PREFETCH_DIST") ? std::atol(std::getenv("QSV_JIT_PREFETCH_DIST")) : 296;
+    return d;
+}
+
 namespace {
 
 // Shared-memory slot map of one pass: slot(e) = e ^ G(e), G linear from the
@@ -1143,7 +1157,12 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             std::vector<int> runq(tq.begin() + lr, tq.end());
             // (fewer than 5 forced low qubits: more runs than threads, each
             // thread prefetches several)
-            o << "    { const u64 nt = t + (u64)gridDim.x * " << gang << "u;\n";
+            // persistent grid: this CTA's next tile; one CTA per tile: the tile a
+            // CTA launched about one residency wave later will take
+            if (gridDim_prefetch_distance() > 0 && gang == 1)
+                o << "    { const u64 nt = t + " << gridDim_prefetch_distance() << "ull;\n";
+            else
+                o << "    { const u64 nt = t + (u64)gridDim.x * " << gang << "u;\n";
             o << "      if (nt < ntiles" << (basis_param ? " && basis == ~0ull" : "") << ")\n";
             o << "      for (unsigned j = tid; j < " << (1u << (m - lr)) << "u; j += " << T
               << "u) prefetch_l2(psi + (" << base_of("nt")
@@ -1369,12 +1388,13 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     // L2 prefetch of the next tile pays only in compute-bound passes (measured
     // per pass on C2: it slows memory-bound passes by ~0.3 ms and speeds up
     // passes above ~55 FP64/amplitude); QSV_JIT_PREFETCH=0/1 forces it
-    // (with one CTA per tile there is no next tile to prefetch: off unless the
-    // persistent grid is selected, QSV_JIT_GRID_TILES=0)
+    // With one CTA per tile the prefetch targets the tile a CTA launched one
+    // residency wave later takes (gridDim_prefetch_distance): measured a gain
+    // for the r = 4 passes (two 8-warp CTAs per SM; C2 59.0 -> 57.6 ms) and a
+    // loss for the r = 5 ones (QFT 41.6 -> 45.8 ms)
     const char *e = std::getenv("QSV_JIT_PREFETCH");
-    const char *gt = std::getenv("QSV_JIT_GRID_TILES");
-    const bool persistent = gt && std::atoi(gt) == 0;
-    const bool prefetch = e ? std::atoi(e) != 0 : (persistent && cost >= kPrefetchMinFp64);
+    const bool prefetch = e ? std::atoi(e) != 0
+                            : (jit_per_tile_grid() ? pass_r(P, pi) == 4 : cost >= kPrefetchMinFp64);
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
                                     sc, final_pass, nullptr, gang, xmask, tma && !xmask && !probe, probe);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << pass_r(P, pi));
@@ -1866,7 +1886,7 @@ int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, s
     // scheduled CTAs keep the tiles in flight adjacent, and a kernel sharing the
     // GPU with another stream's kernels is not stuck with its early residents.
     // QSV_JIT_GRID_TILES=0 restores the persistent grid.
-    static const bool per_tile = !std::getenv("QSV_JIT_GRID_TILES") || std::atoi(std::getenv("QSV_JIT_GRID_TILES")) != 0;
+    const bool per_tile = jit_per_tile_grid();
     const unsigned long long cap = per_tile ? 0x7fffffffull : (unsigned long long)P.jit_grids[pass];
     const unsigned grid = (unsigned)std::min<unsigned long long>((n_tiles + gang - 1) / gang, cap);
     void *args[] = {&psi, &n_tiles, &basis};
