@@ -90,7 +90,7 @@ def test_device_source_compiles_for_sm100a():
         src = kernel_source(h, 0, False)
     finally:
         N.lib().qsv_plan_destroy(h)
-    assert "qsv_pass" in src and "__launch_bounds__(128," in src and "prefetch_l2" in src
+    assert "qsv_pass" in src and "__launch_bounds__(" in src and "prefetch_l2" in src
     size = C.c_int64()
     N.check(N.lib().qsv_jit_compile(src.encode(), C.byref(size)))
     assert size.value > 1000
