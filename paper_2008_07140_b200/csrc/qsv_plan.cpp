@@ -422,6 +422,61 @@ uint64_t search_tile(const std::vector<GateRec> &recs, const std::vector<int> &r
     return tile;
 }
 
+// Number of passes the greedy planner (absorb + single-swap search) needs for
+// `rem` (rollout for the look-ahead tile choice below); stops at `cap`.
+int rollout_passes(const std::vector<GateRec> &recs, std::vector<int> cur, uint64_t low, uint64_t all, int n, int m,
+                   int cap) {
+    int passes = 0;
+    while (!cur.empty() && passes < cap) {
+        Absorber tile;
+        tile.resident = low;
+        tile.capacity = m;
+        for (int gi : cur) tile.offer(recs[gi]);
+        const uint64_t res = search_tile(recs, cur, padded_tile(tile.resident, all, n, m), low, n);
+        std::vector<int> t, d;
+        scan_fixed_tile(recs, cur, res, &t, &d);
+        cur.swap(d);
+        ++passes;
+    }
+    return cur.empty() ? passes : cap + 1;
+}
+
+// Look-ahead tile choice (QSV_PLAN_ROLLOUT=K): among the best tile and its
+// single-swap neighbours absorbing at least 70 % as many gates, the K with the
+// most gates are completed greedily; the tile whose completion needs the fewest
+// passes wins (ties: more gates now).  Minimises HBM passes rather than
+// maximising each pass.
+uint64_t lookahead_tile(const std::vector<GateRec> &recs, const std::vector<int> &rem, uint64_t best, uint64_t fixed,
+                        uint64_t all, int n, int m, int K) {
+    const int best_count = scan_fixed_tile(recs, rem, best);
+    std::vector<std::pair<int, uint64_t>> cands{{best_count, best}};
+    for (int a = 0; a < n; ++a) {
+        if (!((best >> a) & 1) || ((fixed >> a) & 1)) continue;
+        for (int b = 0; b < n; ++b) {
+            if ((best >> b) & 1) continue;
+            const uint64_t t2 = best ^ (1ull << a) ^ (1ull << b);
+            const int c = scan_fixed_tile(recs, rem, t2);
+            const int thr = std::getenv("QSV_PLAN_ROLLOUT_PCT") ? std::atoi(std::getenv("QSV_PLAN_ROLLOUT_PCT")) : 70;
+            if (c * 100 >= best_count * thr) cands.push_back({c, t2});
+        }
+    }
+    std::stable_sort(cands.begin() + 1, cands.end(), [](auto &x, auto &y) { return x.first > y.first; });
+    if ((int)cands.size() > K) cands.resize(K);
+    uint64_t choice = best;
+    int best_passes = 1 << 30, choice_count = -1;
+    for (auto &c : cands) {
+        std::vector<int> t, d;
+        scan_fixed_tile(recs, rem, c.second, &t, &d);
+        const int p = rollout_passes(recs, d, fixed, all, n, m, best_passes);
+        if (p < best_passes || (p == best_passes && c.first > choice_count)) {
+            best_passes = p;
+            choice = c.second;
+            choice_count = c.first;
+        }
+    }
+    return choice;
+}
+
 // Greedy absorption front-loads the FP64 work: the first passes take every
 // gate they can and run compute-bound while the last ones are HBM-bound.  A
 // pass costs ~max(HBM time, FP64 time), so gates at the tail of a heavy pass
@@ -856,6 +911,10 @@ Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L,
             uint64_t res = tile.resident;
             if (search && P.pass_budget <= 0) {
                 res = search_tile(recs, remaining, padded_tile(res, all, n, m), low, n);
+                // look-ahead over 100 candidate tiles (n=32 RQC: 10 -> 8 passes; C2,
+                // QFT, C5 unchanged); QSV_PLAN_ROLLOUT=0 keeps the greedy tiles
+                const int rollout = std::getenv("QSV_PLAN_ROLLOUT") ? std::atoi(std::getenv("QSV_PLAN_ROLLOUT")) : 100;
+                if (rollout > 0) res = lookahead_tile(recs, remaining, res, low, all, n, m, rollout);
                 taken.clear();
                 deferred.clear();
                 scan_fixed_tile(recs, remaining, res, &taken, &deferred);

@@ -134,6 +134,7 @@ def test_plan_balanced_passes_keep_the_result(monkeypatch, work):
     recs = compile_gates(prog.gate_instructions())
     psi0 = workloads.gaussian_state(n, 5)
     cfg = dict(tile_qubits=7, reg_qubits=3, low_qubits=2)
+    monkeypatch.setenv("QSV_PLAN_ROLLOUT", "0")  # greedy tiles (front-loaded work to balance)
     monkeypatch.setenv("QSV_BALANCE_WORK", "0")
     _, flat = build_plan(recs, n, **cfg)
     monkeypatch.setenv("QSV_BALANCE_WORK", str(work))
