@@ -26,6 +26,13 @@
 
 namespace qsv {
 
+// File-scope declarations gathered while a kernel body is generated (per-thread
+// factor tables, StageGen::materialize); jit_source inserts them before the
+// kernel.  One generation at a time per thread.
+thread_local std::ostringstream *g_decls = nullptr;
+thread_local int g_decl_id = 0;
+
+
 namespace {
 
 // ---------------------------------------------------------------------------
@@ -318,6 +325,17 @@ struct StageGen {
     // factor that depends on thread/tile bits, applied once per stage
     std::vector<int> acc;           // acc[2k+b]: accumulator in use
     bool accG = false;
+    // factors not yet multiplied into their accumulator: per accumulator
+    // (k, b; k = -1: qG) a list of (scalar qubits, control condition, value
+    // table over the scalar bits).  Factors with the same scalar qubits and
+    // condition multiply at compile time (QFT: all CR phases controlled by one
+    // thread/tile qubit become one complex multiply per accumulator)
+    struct PendFactor {
+        std::vector<int> sq;
+        std::string ccond;
+        std::vector<cd> val;
+    };
+    std::map<std::pair<int, int>, std::vector<PendFactor>> pacc;
     // runtime sign flips (CZ-like diagonals on thread/tile qubits): each
     // register amplitude carries a pending set of runtime sign variables
     // (bit i <-> variable sg<id[i]>), applied to the sign bits with integer
@@ -328,6 +346,9 @@ struct StageGen {
     std::vector<int> svar_id;       // its emitted name
     std::map<uint64_t, std::string> smask;
     int next_id = 0;
+
+    int T = 0;                  // threads per tile (per-thread factor tables)
+    bool host_render = false;
 
     StageGen(std::ostringstream &out, int r, const std::vector<int> &t)
         : o(out), R(r), tq(t), pend(1u << r, cd(1, 0)), acc(2 * r, 0), psign(1u << r, 0) {}
@@ -386,8 +407,64 @@ struct StageGen {
         o << "\n";
     }
 
+    // emits the folded pending factors of accumulator (k, b) (k = -1: qG)
+    void materialize(int k, int b) {
+        auto it = pacc.find({k, b});
+        if (it == pacc.end()) return;
+        const std::string name = k < 0 ? std::string("qG") : "qA" + std::to_string(k) + "_" + std::to_string(b);
+        const std::string one = "make_double2(1.0, 0.0)";
+        // factors over thread bits only (no control condition) fold into one
+        // per-thread table, indexed by tid: one load and one complex multiply
+        // instead of a select chain + multiply per factor (QFT: the CR phases
+        // of every thread-bit control of a register target)
+        std::vector<const PendFactor *> thr;
+        for (const PendFactor &f : it->second) {
+            bool only = f.ccond.empty() && !f.sq.empty();
+            for (int q : f.sq) only &= thread_bit.count(q) > 0;
+            if (only) thr.push_back(&f);
+        }
+        if (g_decls && thr.size() >= 2 && T > 0) {
+            std::vector<cd> tab((size_t)T, cd(1, 0));
+            for (int tid = 0; tid < T; ++tid)
+                for (const PendFactor *f : thr) {
+                    int combo = 0;
+                    for (size_t si = 0; si < f->sq.size(); ++si)
+                        combo |= ((tid >> thread_bit.at(f->sq[si])) & 1) << si;
+                    tab[tid] *= f->val[combo];
+                }
+            const std::string tname = "qtab" + std::to_string(g_decl_id++);
+            *g_decls << (host_render ? "static const double2 " : "__device__ const double2 ") << tname << "[" << T
+                     << "] = {";
+            for (int tid = 0; tid < T; ++tid) {
+                const cd c = snap(tab[tid]);
+                *g_decls << (tid ? ", " : "") << "{" << lit(c.real()) << ", " << lit(c.imag()) << "}";
+            }
+            *g_decls << "};\n";
+            o << "    " << name << " = cmulc(" << name << ", " << tname << "[tid]);\n";
+            fp64 += 4;
+        } else {
+            thr.clear();
+        }
+        for (const PendFactor &f : it->second) {
+            if (std::find(thr.begin(), thr.end(), &f) != thr.end()) continue;
+            const std::string e = select_from(f.sq, f.val);
+            if (e == c2(cd(1, 0))) continue;
+            const std::string g = f.ccond.empty() ? e : "((" + f.ccond + ") ? " + e + " : " + one + ")";
+            o << "    " << name << " = cmulc(" << name << ", " << g << ");\n";
+            fp64 += 4;
+        }
+        pacc.erase(it);
+    }
+    void materialize_all() {
+        materialize(-1, 0);
+        for (int k = 0; k < R; ++k)
+            for (int b = 0; b < 2; ++b) materialize(k, b);
+    }
+
     // apply + reset the accumulators of register position k
     void flush_acc(int k) {
+        materialize(k, 0);
+        materialize(k, 1);
         for (int b = 0; b < 2; ++b) {
             if (!acc[2 * k + b]) continue;
             for (int rho = 0; rho < (1 << R); ++rho)
@@ -401,6 +478,7 @@ struct StageGen {
     // stage end: one product table over the active accumulators, then one
     // complex multiply per amplitude (plus its compile-time pending factor)
     void flush_runtime() {
+        materialize_all();
         std::vector<int> used;
         for (int k = 0; k < R; ++k)
             if (acc[2 * k] || acc[2 * k + 1]) used.push_back(k);
@@ -727,28 +805,71 @@ struct StageGen {
         return build(0, 0);
     }
 
+    // nested selects of constants over the scalar bits sq (val indexed by combo)
+    std::string select_from(const std::vector<int> &sq, const std::vector<cd> &val) const {
+        const int ns = (int)sq.size();
+        std::function<std::string(int, int)> build = [&](int si, int prefix) -> std::string {
+            if (si == ns) return c2(val[prefix]);
+            const std::string a = build(si + 1, prefix), b = build(si + 1, prefix | (1 << si));
+            if (a == b) return a;
+            return "(" + scalar_expr(sq[si]) + " ? " + b + " : " + a + ")";
+        };
+        return build(0, 0);
+    }
+
+    // value table of the factor over the scalar bits for register bit reg_bit
+    std::vector<cd> factor_table(const std::vector<int> &dq, const std::vector<cd> &d, const std::vector<int> &sq,
+                                 int reg_t, int reg_bit) const {
+        const int ns = (int)sq.size();
+        std::vector<cd> val(1u << ns);
+        for (int combo = 0; combo < (1 << ns); ++combo) {
+            int idx = 0;
+            for (size_t t = 0; t < dq.size(); ++t) {
+                int bit;
+                if ((int)t == reg_t) bit = reg_bit;
+                else {
+                    int si = 0;
+                    while (sq[si] != dq[t]) ++si;
+                    bit = (combo >> si) & 1;
+                }
+                idx = 2 * idx + bit;
+            }
+            val[combo] = d[idx];
+        }
+        return val;
+    }
+
+    void defer(int k, int b, const std::vector<int> &sq, const std::string &ccond, const std::vector<cd> &val) {
+        bool trivial = true;
+        for (const cd &x : val) trivial &= x == cd(1, 0);
+        if (trivial) return;
+        std::vector<PendFactor> &lst = pacc[{k, b}];
+        for (PendFactor &f : lst)
+            if (f.sq == sq && f.ccond == ccond) {
+                for (size_t i = 0; i < val.size(); ++i) f.val[i] *= val[i];
+                return;
+            }
+        lst.push_back(PendFactor{sq, ccond, val});
+    }
+
     void accumulate(const std::vector<int> &dq, const std::vector<cd> &d, const std::vector<int> &sq,
                     const std::string &ccond) {
         int reg_t = -1;
         for (size_t t = 0; t < dq.size(); ++t)
             if (regpos(dq[t]) >= 0) reg_t = (int)t;
-        const std::string one = "make_double2(1.0, 0.0)";
-        auto guard = [&](const std::string &e) { return ccond.empty() ? e : "((" + ccond + ") ? " + e + " : " + one + ")"; };
         if (reg_t < 0) {
-            const std::string e = select_expr(dq, d, sq, -1, 0);
-            if (e == c2(cd(1, 0))) return;
-            o << "    qG = cmulc(qG, " << guard(e) << ");\n";
+            defer(-1, 0, sq, ccond, factor_table(dq, d, sq, -1, 0));
             accG = true;
-            fp64 += 4;
             return;
         }
         const int k = regpos(dq[reg_t]);
         for (int b = 0; b < 2; ++b) {
-            const std::string e = select_expr(dq, d, sq, reg_t, b);
-            if (e == c2(cd(1, 0))) continue;
-            o << "    qA" << k << "_" << b << " = cmulc(qA" << k << "_" << b << ", " << guard(e) << ");\n";
+            const std::vector<cd> val = factor_table(dq, d, sq, reg_t, b);
+            bool trivial = true;
+            for (const cd &x : val) trivial &= x == cd(1, 0);
+            if (trivial) continue;
+            defer(k, b, sq, ccond, val);
             acc[2 * k + b] = 1;
-            fp64 += 4;
         }
     }
 
@@ -1024,6 +1145,8 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         const DevStage &st = P.stages[s];
         const bool first = s == dp.stage_begin, last = s + 1 == dp.stage_end;
         StageGen g(o, R, tq);
+        g.T = 1 << (m - R);
+        g.host_render = host;
         g.regq.resize(R);
         for (int k = 0; k < R; ++k) g.regq[k] = tq[st.rb[k]];
         std::vector<int> nonreg, nonreg_q;
@@ -1338,6 +1461,11 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     auto base_of = [&](const std::string &t) { return deposit_expr(t, ext, true); };
     const double sc = pass_scales(P)[pi];
     const bool final_pass = pi + 1 == (int)P.passes.size();
+    // per-thread factor tables land in `decls` (inserted before the kernel)
+    std::ostringstream decls;
+    std::ostringstream *saved_decls = g_decls;
+    g_decls = &decls;
+    g_decl_id = 0;
     // FP64 work per amplitude (dry run) decides the compute-bound tuning
     double cost;
     {
@@ -1345,6 +1473,8 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
         cost = emit_tile_loop(dry, P, pi, host, "n_tiles", base_of, true, false, false, sc, final_pass) /
                (double)(1 << pass_r(P, pi));
     }
+    decls.str("");
+    g_decl_id = 0;
     // QSV_JIT_GANG=G: compute-bound passes run G tiles per CTA in lock step
     // (one CTA per SM) instead of independent CTAs; QSV_JIT_TMA=1: their
     // tiles arrive by TMA bulk copies during the previous tile's last stage
@@ -1398,6 +1528,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
     const double f = emit_tile_loop(o, P, pi, host, "n_tiles", base_of, true, !host && !jit_double_buffer(), prefetch,
                                     sc, final_pass, nullptr, gang, xmask, tma && !xmask && !probe, probe);
     if (fp64_per_amp) *fp64_per_amp = f / (double)(1 << pass_r(P, pi));
+    g_decls = saved_decls;
     if (probe) {
         // per-CTA partials in a fixed order (warp tree, then warps in order)
         o << "  {\n  __shared__ double qsv_pred[" << PB << "][32];\n";
@@ -1411,7 +1542,13 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
           << " probe_out[(size_t)blockIdx.x * " << PB << "u + threadIdx.x] = s; }\n  }\n";
     }
     o << "}\n";
-    return o.str();
+    std::string src = o.str();
+    const std::string d = decls.str();
+    if (!d.empty()) {
+        const size_t at = src.find("extern \"C\"");
+        src.insert(at == std::string::npos ? 0 : at, d);
+    }
+    return src;
 }
 
 // Register qubits per pass.  32 amplitudes per thread (r = 5) needs the
