@@ -829,6 +829,218 @@ struct PauliPlacement {
     std::vector<PauliString> bnd;  // one per pass boundary (+ the end)
 };
 
+// ---- Pauli-frame propagation (single error event) ---------------------------
+// A Pauli string S = phase * X^x Z^z.  Moving it across a gate G in time
+// (forward: G S G^dagger; backward: G^dagger S G) keeps it a Pauli string when
+// G is Clifford on S's support (H, sqrt(X), sqrt(Y), CZ, S...) or commutes with
+// it (Z-type support through diagonal gates, T included).
+struct FrameString {
+    cd phase{1.0, 0.0};
+    uint64_t x = 0, z = 0;
+};
+
+// 2x2 Pauli matrices: 0 I, 1 X, 2 Y, 3 Z
+static const cd kPauli[4][4] = {{1, 0, 0, 1}, {0, 1, 1, 0}, {0, cd(0, -1), cd(0, 1), 0}, {1, 0, 0, -1}};
+
+// k-qubit (k <= 3) dense matrix of gate g over qubit list qs (qs[0] = MSB);
+// controls embedded
+static bool gate_dense(const GateRec &g, const std::vector<int> &qs, std::vector<cd> &Mout) {
+    const int k = (int)qs.size(), D = 1 << k;
+    auto bit = [&](int idx, int q) {
+        for (int i = 0; i < k; ++i)
+            if (qs[i] == q) return (idx >> (k - 1 - i)) & 1;
+        return -1;
+    };
+    Mout.assign((size_t)D * D, cd(0, 0));
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            // non-gate qubits of qs must be equal (identity there)
+            bool same = true, ctl = true;
+            for (int i = 0; i < k; ++i) {
+                const int q = qs[i];
+                const bool is_t = q == g.t[0] || (g.nt == 2 && q == g.t[1]);
+                if (!is_t && bit(r, q) != bit(c, q)) same = false;
+                if (((g.cmask >> q) & 1) && bit(r, q) != 1) ctl = false;
+            }
+            if (!same) continue;
+            int tr = 0, tc = 0;
+            for (int t = 0; t < g.nt; ++t) {
+                tr = 2 * tr + bit(r, g.t[t]);
+                tc = 2 * tc + bit(c, g.t[t]);
+            }
+            const bool targets_equal = tr == tc;
+            if (!ctl) Mout[(size_t)r * D + c] = targets_equal ? cd(1, 0) : cd(0, 0);
+            else Mout[(size_t)r * D + c] = g.u[tr * (1 << g.nt) + tc];
+        }
+    return true;
+}
+
+// conjugate S by gate g (forward: G S G^dag, else G^dag S G); false when the
+// result is not a Pauli string
+static bool frame_cross(FrameString &S, const GateRec &g, int n, bool forward) {
+    const uint64_t gq = g.nmask | g.dmask;
+    if (!((S.x | S.z) & gq)) return true;  // disjoint support
+    std::vector<int> qs;
+    for (int q = n - 1; q >= 0; --q)
+        if ((gq >> q) & 1) qs.push_back(q);
+    const int k = (int)qs.size();
+    if (k > 3) return false;
+    const int D = 1 << k;
+    std::vector<cd> G;
+    gate_dense(g, qs, G);
+    // S = phase * X^x Z^z = phi * (tensor of I/X/Y/Z) with phi = phase * (-i)^#Y
+    // (Y = i X Z); the qs part of the tensor is conjugated as a matrix
+    auto n_y = [](uint64_t x, uint64_t z) { return std::popcount(x & z); };
+    auto ipow = [](int e) {
+        static const cd p4[4] = {cd(1, 0), cd(0, 1), cd(-1, 0), cd(0, -1)};
+        return p4[((e % 4) + 4) % 4];
+    };
+    const cd phi = S.phase * ipow(-n_y(S.x, S.z));
+    std::vector<int> code(k);
+    for (int i = 0; i < k; ++i) {
+        const int xq = (S.x >> qs[i]) & 1, zq = (S.z >> qs[i]) & 1;
+        code[i] = xq && zq ? 2 : xq ? 1 : zq ? 3 : 0;
+    }
+    std::vector<cd> Sm((size_t)D * D);
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            cd v(1, 0);
+            for (int i = 0; i < k; ++i) v *= kPauli[code[i]][2 * ((r >> (k - 1 - i)) & 1) + ((c >> (k - 1 - i)) & 1)];
+            Sm[(size_t)r * D + c] = v;
+        }
+    // T = G Sm G^dag (forward) or G^dag Sm G
+    std::vector<cd> A((size_t)D * D), T((size_t)D * D);
+    auto Gd = [&](int r, int c) { return std::conj(G[(size_t)c * D + r]); };
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            cd s2(0, 0);
+            for (int t = 0; t < D; ++t) s2 += (forward ? G[(size_t)r * D + t] : Gd(r, t)) * Sm[(size_t)t * D + c];
+            A[(size_t)r * D + c] = s2;
+        }
+    for (int r = 0; r < D; ++r)
+        for (int c = 0; c < D; ++c) {
+            cd s2(0, 0);
+            for (int t = 0; t < D; ++t) s2 += A[(size_t)r * D + t] * (forward ? Gd(t, c) : G[(size_t)t * D + c]);
+            T[(size_t)r * D + c] = s2;
+        }
+    // T = f * tensor(cc) with f in {+-1, +-i}?
+    const int NT = 1 << (2 * k);
+    for (int tc = 0; tc < NT; ++tc) {
+        std::vector<int> cc(k);
+        for (int i = 0; i < k; ++i) cc[i] = (tc >> (2 * i)) & 3;
+        cd f(0, 0);
+        bool ok = true, have = false;
+        for (int r = 0; r < D && ok; ++r)
+            for (int c = 0; c < D && ok; ++c) {
+                cd v(1, 0);
+                for (int i = 0; i < k; ++i) v *= kPauli[cc[i]][2 * ((r >> (k - 1 - i)) & 1) + ((c >> (k - 1 - i)) & 1)];
+                const cd t = T[(size_t)r * D + c];
+                if (v == cd(0, 0)) {
+                    if (std::abs(t) > 1e-12) ok = false;
+                    continue;
+                }
+                const cd ratio = t / v;
+                if (!have) {
+                    f = ratio;
+                    have = true;
+                } else if (std::abs(ratio - f) > 1e-12) {
+                    ok = false;
+                }
+            }
+        if (!ok || !have) continue;
+        const cd fs(std::round(f.real()), std::round(f.imag()));
+        if (std::abs(f - fs) > 1e-12 || std::abs(std::abs(fs) - 1.0) > 1e-12) return false;
+        uint64_t nx = S.x, nz = S.z;
+        for (int i = 0; i < k; ++i) {
+            const uint64_t b = 1ull << qs[i];
+            nx &= ~b;
+            nz &= ~b;
+            if (cc[i] == 1 || cc[i] == 2) nx |= b;
+            if (cc[i] == 3 || cc[i] == 2) nz |= b;
+        }
+        S.phase = phi * fs * ipow(n_y(nx, nz));
+        S.x = nx;
+        S.z = nz;
+        return true;
+    }
+    return false;
+}
+
+// One error event (all Paulis before the same gate, distinct qubits): place
+// the Pauli string in the executed order of the plan's passes, in the slot
+// between the last earlier and the first later gate touching its qubits; if a
+// pass boundary lies in that slot the string is applied there, else it is
+// propagated through the rest (or the start) of its pass as a Pauli frame -
+// no gate changes, every pass keeps its compiled kernel.  False: not possible
+// (the frame met a non-Clifford gate on its X/Y support).
+static bool place_single_event(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &out) {
+    const int64_t g = pa[0].gate;
+    FrameString S;
+    for (int64_t i = 0; i < n; ++i) {
+        if (pa[i].gate != g) return false;
+        const uint64_t b = 1ull << pa[i].qubit;
+        if ((S.x | S.z) & b) return false;
+        if (pa[i].kind == 1 || pa[i].kind == 2) S.x |= b;
+        if (pa[i].kind == 3 || pa[i].kind == 2) S.z |= b;
+        if (pa[i].kind == 2) S.phase *= cd(0, 1);  // Y = i X Z
+    }
+    const int np = (int)P.passes.size();
+    std::vector<int> E, start(np + 1, 0);
+    std::vector<int> pos(P.recs.size(), -1);
+    for (int j = 0; j < np; ++j) {
+        start[j] = (int)E.size();
+        for (int gi : P.pass_gates[j]) {
+            pos[gi] = (int)E.size();
+            E.push_back(gi);
+        }
+    }
+    start[np] = (int)E.size();
+    const uint64_t Q = S.x | S.z;
+    int lo = -1, hi = (int)E.size();
+    for (size_t k = 0; k < P.recs.size(); ++k) {
+        if (!((P.recs[k].nmask | P.recs[k].dmask) & Q) || pos[k] < 0) continue;
+        if ((int64_t)k < g) lo = std::max(lo, pos[k]);
+        else hi = std::min(hi, pos[k]);
+    }
+    if (lo >= hi) return false;
+    auto put = [&](int b, const FrameString &F) {
+        out.recs = P.recs;
+        out.modified.assign(np, 0);
+        out.bnd.assign(np + 1, PauliString{});
+        out.bnd[b].phase = F.phase;
+        out.bnd[b].x = F.x;
+        out.bnd[b].z = F.z;
+        out.bnd[b].any = true;
+    };
+    for (int b = 0; b <= np; ++b)
+        if (lo < start[b] && start[b] <= hi) {
+            put(b, S);
+            return true;
+        }
+    // the slot lies inside one pass j
+    int j = 0;
+    while (j + 1 <= np && start[j + 1] <= lo + 1) ++j;
+    {
+        FrameString F = S;
+        bool ok = true;
+        for (int e = lo + 1; e < start[j + 1] && ok; ++e) ok = frame_cross(F, P.recs[E[e]], P.n, true);
+        if (ok) {
+            put(j + 1, F);
+            return true;
+        }
+    }
+    {
+        FrameString F = S;
+        bool ok = true;
+        for (int e = hi - 1; e >= start[j] && ok; --e) ok = frame_cross(F, P.recs[E[e]], P.n, false);
+        if (ok) {
+            put(j, F);
+            return true;
+        }
+    }
+    return false;
+}
+
 int place_paulis(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &out, std::string &msg) {
     const int np = (int)P.passes.size();
     if (P.relabelled || (int)P.pass_gates.size() != np || use_supers(P)) {
@@ -856,6 +1068,8 @@ int place_paulis(const Plan &P, const qsv_pauli *pa, int64_t n, PauliPlacement &
         order[i] = i;
     }
     std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return pa[a].gate < pa[b].gate; });
+    static const bool frame = !std::getenv("QSV_PAULI_FRAME") || std::atoi(std::getenv("QSV_PAULI_FRAME")) != 0;
+    if (frame && place_single_event(P, pa, n, out)) return QSV_OK;
     std::vector<int> chosen(n, 0);
     std::vector<char> seen(np);
     for (int64_t idx : order) {
