@@ -483,37 +483,55 @@ struct StageGen {
         for (int k = 0; k < R; ++k)
             if (acc[2 * k] || acc[2 * k + 1]) used.push_back(k);
         if (used.empty() && !accG) return;
-        std::vector<std::string> tab = {accG ? "qG" : ""};
+        // product tables over groups of the active register bits: one table
+        // over all of them costs 2^|used| live temporaries (spills at r = 5:
+        // QFT); with four or more bits two tables (~2 and ~3 bits) take fewer
+        // multiplies in total and a quarter of the registers
+        std::vector<std::vector<int>> groups;
+        if (used.size() >= 4) {
+            const size_t a = used.size() / 2;
+            groups.push_back(std::vector<int>(used.begin(), used.begin() + (long)a));
+            groups.push_back(std::vector<int>(used.begin() + (long)a, used.end()));
+        } else {
+            groups.push_back(used);
+        }
         int id = 0;
-        for (size_t u = 0; u < used.size(); ++u) {
-            const int k = used[u];
-            // entry index: bit u <-> register bit of position used[u]
-            std::vector<std::string> next(2 * tab.size());
-            for (size_t j = 0; j < tab.size(); ++j)
-                for (int b = 0; b < 2; ++b) {
-                    const std::string &t = tab[j];
-                    const std::string a = "qA" + std::to_string(k) + "_" + std::to_string(b);
-                    std::string &dst = next[j | ((size_t)b << u)];
-                    if (!acc[2 * k + b]) {
-                        dst = t;
-                    } else if (t.empty()) {
-                        dst = a;
-                    } else {
-                        dst = "qT" + std::to_string(id++);
-                        o << "    const double2 " << dst << " = cmulc(" << t << ", " << a << ");\n";
-                        fp64 += 4;
+        std::vector<std::vector<std::string>> tabs;
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            std::vector<std::string> tab = {gi == 0 && accG ? "qG" : ""};
+            const std::vector<int> &grp = groups[gi];
+            for (size_t u = 0; u < grp.size(); ++u) {
+                const int k = grp[u];
+                // entry index: bit u <-> register bit of position grp[u]
+                std::vector<std::string> next(2 * tab.size());
+                for (size_t j = 0; j < tab.size(); ++j)
+                    for (int b = 0; b < 2; ++b) {
+                        const std::string &t = tab[j];
+                        const std::string a = "qA" + std::to_string(k) + "_" + std::to_string(b);
+                        std::string &dst = next[j | ((size_t)b << u)];
+                        if (!acc[2 * k + b]) {
+                            dst = t;
+                        } else if (t.empty()) {
+                            dst = a;
+                        } else {
+                            dst = "qT" + std::to_string(id++);
+                            o << "    const double2 " << dst << " = cmulc(" << t << ", " << a << ");\n";
+                            fp64 += 4;
+                        }
                     }
-                }
-            tab.swap(next);
+                tab.swap(next);
+            }
+            tabs.push_back(tab);
         }
-        for (int rho = 0; rho < (1 << R); ++rho) {
-            int idx = 0;
-            for (size_t u = 0; u < used.size(); ++u) idx |= ((rho >> used[u]) & 1) << u;
-            const std::string &t = tab[idx];
-            if (t.empty()) continue;
-            o << "    v" << rho << " = cmulc(v" << rho << ", " << t << ");\n";
-            fp64 += 4;
-        }
+        for (int rho = 0; rho < (1 << R); ++rho)
+            for (size_t gi = 0; gi < groups.size(); ++gi) {
+                int idx = 0;
+                for (size_t u = 0; u < groups[gi].size(); ++u) idx |= ((rho >> groups[gi][u]) & 1) << u;
+                const std::string &t = tabs[gi][idx];
+                if (t.empty()) continue;
+                o << "    v" << rho << " = cmulc(v" << rho << ", " << t << ");\n";
+                fp64 += 4;
+            }
         for (int k = 0; k < 2 * R; ++k) acc[k] = 0;
         accG = false;
     }
