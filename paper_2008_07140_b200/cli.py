@@ -3,6 +3,8 @@
     python -m paper_2008_07140_b200.cli run script.qprog [--seed S] [--noise kind:p[:G,...]]
                                               [--out FILE] [--log FILE] [--max-qubits N]
                                               [--dump-state FILE] [--no-fuse]
+    python -m paper_2008_07140_b200.cli run script.qprog --mode partial --targets 0101,...|FILE
+                                              [--cut C] [--out FILE]
     python -m paper_2008_07140_b200.cli rqc --rows R --cols C --depth D [--seed S]
                                               [--pmeasure q,q] [--patterns 4|8] [--out FILE]
 
@@ -11,8 +13,10 @@ PMEASURE tables print one line per basis string in ascending binary order
 (first listed qubit leftmost) with 6 significant digits and exact zeros as
 "0"; MEASURE results print as "creg j: v"; errors are logged as
 "Class: message (line N)" and the process exits with the class's code
-(2 parse, 3 resource, 4 numeric).  Only the full-amplitude mode exists here
-(partial/single modes are different algorithms, out of scope).
+(2 parse, 3 resource, 4 numeric).  `--mode partial` (reference cli.py:163-174)
+runs the batched branch decomposition of `partition.py` on the same engine and
+prints "bits: re+imi" lines; single-amplitude graph contraction is a different
+algorithm and out of scope.
 """
 
 from __future__ import annotations
@@ -57,6 +61,19 @@ class _Log:
             Path(self.path).write_text("\n".join(self.lines) + "\n")
 
 
+def format_amplitude(z: complex) -> str:
+    """reference cli.py:19-20"""
+    return f"{z.real:.6f}{z.imag:+.6f}i"
+
+
+def _read_targets(value: str) -> list[str]:
+    """Comma-separated bit strings or a whitespace-separated file (cli.py:59-64)."""
+    path = Path(value)
+    if path.is_file():
+        return [t.strip() for t in path.read_text().split() if t.strip()]
+    return [t.strip() for t in value.split(",") if t.strip()]
+
+
 def _emit(text: str, out) -> None:
     if out:
         Path(out).write_text(text)
@@ -83,7 +100,9 @@ def _parser() -> argparse.ArgumentParser:
     sub = ap.add_subparsers(dest="command", required=True)
     run = sub.add_parser("run", help="execute an instruction script (full-amplitude mode)")
     run.add_argument("script")
-    run.add_argument("--mode", choices=("full",), default="full")
+    run.add_argument("--mode", choices=("full", "partial"), default="full")
+    run.add_argument("--cut", type=int, default=None, help="partition boundary (partial)")
+    run.add_argument("--targets", default=None, help="bit strings, comma-separated or a file (partial)")
     run.add_argument("--workers", type=int, default=1, help="accepted for compatibility; unused")
     run.add_argument("--seed", type=int, default=0)
     run.add_argument("--noise", default=None, help="kind:p[:MNEMONIC,...]")
@@ -114,6 +133,17 @@ def main(argv=None) -> int:
             _emit(rqc.generate_rqc(cfg), args.out)
             return 0
         prog = program.parse_program(Path(args.script).read_text())
+        if args.mode == "partial":
+            from . import partition
+            from .errors import ParseError
+
+            if not args.targets:
+                raise ParseError("partial mode requires --targets")
+            cut = args.cut if args.cut is not None else prog.qubit_count // 2
+            amps = partition.run_partial(prog, cut, _read_targets(args.targets), workers=args.workers,
+                                         max_qubits=args.max_qubits, fuse=not args.no_fuse)
+            _emit("\n".join(f"{t}: {format_amplitude(a)}" for t, a in amps.items()) + "\n", args.out)
+            return 0
         out, result = run_text(prog, args.seed, args.noise, args.max_qubits, warn=log, fuse=not args.no_fuse)
         if args.dump_state:
             from .dump import save_state

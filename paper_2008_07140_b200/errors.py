@@ -56,9 +56,11 @@ NonUnitaryU4 = _subclass("NonUnitaryU4", ParseError)
 MalformedTarget = _subclass("MalformedTarget", ParseError)
 UnsupportedGate = _subclass("UnsupportedGate", ParseError)
 InvalidProbability = _subclass("InvalidProbability", ParseError)
+UncuttableGate = _subclass("UncuttableGate", ParseError)  # partial mode (partition.py)
 
 # Resource errors (exit 3).
 TooManyQubits = _subclass("TooManyQubits", ResourceError)
+BranchExplosion = _subclass("BranchExplosion", ResourceError)  # partial mode branch budget
 
 # Numeric errors (exit 4).
 DegenerateState = _subclass("DegenerateState", NumericError)
