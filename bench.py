@@ -251,10 +251,107 @@ def run_traj(args) -> None:
         print(json.dumps(line), flush=True)
 
 
+PARTIAL = (6, 6, 12)  # partial-mode workload: n=36 RQC, cut 18
+
+
+def partial_workload():
+    from paper_2008_07140_b200 import workloads
+    from paper_2008_07140_b200.partition import plan_partition
+    from paper_2008_07140_b200.program import parse_program
+
+    prog = parse_program(workloads.rqc_text(*PARTIAL, seed=SEED))
+    n = prog.qubit_count
+    cut = n // 2
+    plan = plan_partition(prog, cut)
+    rng = np.random.default_rng(SEED)
+    targets = [format(int(i), f"0{n}b") for i in rng.integers(0, 1 << n, 256)]
+    return prog, cut, plan, targets
+
+
+def partial_updates(plan) -> float:
+    """Amplitude-gate updates of the reference's 2*2^c branch sub-circuits
+    (partition.py:96-140: every branch runs all non-crossing gates of its half,
+    a projector per crossing gate and the target action where its bit is 1)."""
+    n, cut, c = plan.qubit_count, plan.cut, plan.c
+    size = {"lower": float(1 << cut), "upper": float(1 << (n - cut))}
+    where = {cg.position for cg in plan.crossing_gates}
+    tot = 0.0
+    for pos, inst in enumerate(plan.program.instructions):
+        if inst.is_gate and pos not in where:
+            tot += size["lower" if all(q < cut for q in inst.all_qubits()) else "upper"] * (1 << c)
+    for cg in plan.crossing_gates:
+        tot += size["lower" if cg.control < cut else "upper"] * (1 << c)
+        tot += size["lower" if cg.target < cut else "upper"] * (1 << (c - 1))
+    return tot
+
+
+def run_partial_bench(args) -> None:
+    """Partial-amplitude mode (reference partition.py:151-192): 256 amplitudes of an
+    n=36 RQC cut at qubit 18.  The metric counts the reference's branch
+    sub-circuit work (2^c branches x both halves); each step is one full
+    `run_partial` call through the public API (program in, amplitudes out on the
+    host, device states allocated, run and freed inside the step)."""
+    import torch
+
+    from paper_2008_07140_b200.partition import batch_bits, decompose_crossing, run_partial
+
+    rank, _, local = dist_env()
+    torch.cuda.set_device(local)
+    prog, cut, plan, targets = partial_workload()
+    work = partial_updates(plan)
+    for _ in range(args.warmup):
+        run_partial(prog, cut, targets, device=local)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            run_partial(prog, cut, targets, device=local)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    cb = batch_bits(plan)
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        from oracle import oracle as O
+
+        threads = O.cpu_threads()
+        done, t0 = 0.0, time.perf_counter()
+        nb = 0
+        for br in decompose_crossing(plan):
+            for half in (br.lower_program, br.upper_program):
+                O.run_full(half, workers=threads)
+                done += len(half.instructions) * float(1 << half.qubit_count)
+            nb += 1
+            if time.perf_counter() - t0 >= args.cpu_seconds:
+                break
+        cdt = time.perf_counter() - t0
+        cpu = {"value": done / cdt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{nb} of {plan.branch_count} branches (both halves) through oracle run_full "
+                         f"({cdt:.1f} s, {threads} threads)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": work / dt, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+                "config": {"workload": f"partial mode: RQC {PARTIAL[0]}x{PARTIAL[1]} {PARTIAL[2]} cycles, "
+                                       f"n={plan.qubit_count}, cut {cut}, {len(targets)} targets",
+                           "crossing_gates": plan.c, "branch_qubits": cb,
+                           "half_states_qubits": [cut + cb, plan.qubit_count - cut + cb],
+                           "reference_branch_updates": work,
+                           "timing": "host wall clock around run_partial (public API, e2e)"},
+                "e2e": {"value": work / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 2 * len(targets) * (16 << cb)},
+                "cpu_baseline": cpu, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
     if args.workload == "traj":
         run_traj(args)
+        return
+    if args.workload == "partial":
+        run_partial_bench(args)
         return
     if world > 1:
         from paper_2008_07140_b200 import distributed
@@ -412,7 +509,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--qubits", type=int, default=0)
-    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj"))
+    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj", "partial"))
     ap.add_argument("--trajectories", type=int, default=1024)
     ap.add_argument("--dedup", action="store_true")
     ap.add_argument("--tile", type=int, default=0)
