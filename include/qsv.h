@@ -255,6 +255,17 @@ int qsv_max_abs_diff(qsv_state *st, const void *other_device_c128, double *out);
 /* reduced density matrix of 1 or 2 qubits (first listed = MSB), row-major complex
  * 2^nq x 2^nq; branch weights ||K psi||^2 = tr(K rho K^dag) (noise.py:173-185) */
 int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits_msb_first, double *out_c128);
+/* batched noisy trajectories (run_full(prog, rng_t, noise) per trajectory, statevector.py:343-357,
+ * noise.py:188-222): the state holds B = 2^batch_log2 trajectories as consecutive
+ * 2^(n - batch_log2)-amplitude blocks.  In ONE pass: apply trajectory b's own dense gate on
+ * gk = 0|1|2 qubits (first listed = MSB; mats = B slots of 16 complex128, the row-major
+ * 2^gk x 2^gk matrix U.K_c / sqrt(p) in the first 4^gk), then reduce every trajectory's reduced
+ * density of nk = 0|1|2 qubits (the next noisy gate's branch weights, or a MEASURE's p0/p1)
+ * into rdm_out = B x 16 complex128 slots (host; row-major 4x4 per trajectory, the
+ * 2^nk x 2^nk block top-left; returns after the copy when nk > 0) */
+int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits_msb_first,
+                         const double *mats_c128, int nk, const int32_t *next_qubits_msb_first,
+                         double *rdm_out_c128);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,8 @@ struct qsv_state {
     void *plan_buf = nullptr;  // scratch for one-shot plans
     size_t plan_buf_bytes = 0;
     int sm_count = 148;
+    double2 *nb_mats = nullptr;  // batched noisy step: per-trajectory gate matrices + rdm out
+    size_t nb_bytes = 0;
     uint64_t size() const { return 1ull << n; }
 };
 
@@ -436,6 +438,7 @@ int qsv_destroy(qsv_state *st) {
     if (st->result) cudaFree(st->result);
     if (st->plan_buf) cudaFree(st->plan_buf);
     if (st->barrier) cudaFree(st->barrier);
+    if (st->nb_mats) cudaFree(st->nb_mats);
     if (st->own_stream) cudaStreamDestroy(st->stream);
     delete st;
     return QSV_OK;
@@ -1614,6 +1617,78 @@ int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *ou
     rdm_finish<<<1, 32, 0, st->stream>>>(st->work, blocks, vals, st->result);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(out, st->result, sizeof(double) * vals, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
+int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits, const double *mats,
+                         int nk, const int32_t *next_qubits, double *rdm_out) {
+    const int nsub = st->n - batch_log2;
+    if (batch_log2 < 0 || nsub < 1 || batch_log2 > 16) return fail(QSV_E_PARSE, "bad batch size");
+    if (gk < 0 || gk > 2 || nk < 0 || nk > 2) return fail(QSV_E_UNSUPPORTED, "noisy step acts on 0..2 qubits");
+    if (gk == 0 && nk == 0) return QSV_OK;
+    NoisyArgs a{};
+    a.nsub = nsub;
+    a.gk = gk;
+    a.nk = nk;
+    int uq[4], nu = 0;
+    auto add = [&](int q) {
+        for (int i = 0; i < nu; ++i)
+            if (uq[i] == q) return;
+        uq[nu++] = q;
+    };
+    for (int i = 0; i < gk; ++i) {
+        if (gate_qubits[i] < 0 || gate_qubits[i] >= nsub) return fail(QSV_E_PARSE, "gate qubit out of range");
+        add(gate_qubits[i]);
+    }
+    for (int i = 0; i < nk; ++i) {
+        if (next_qubits[i] < 0 || next_qubits[i] >= nsub) return fail(QSV_E_PARSE, "qubit out of range");
+        add(next_qubits[i]);
+    }
+    if ((gk == 2 && gate_qubits[0] == gate_qubits[1]) || (nk == 2 && next_qubits[0] == next_qubits[1]))
+        return fail(QSV_E_PARSE, "repeated qubit");
+    if (nu > nsub) return fail(QSV_E_PARSE, "trajectory too small for the step");
+    std::sort(uq, uq + nu);
+    auto pos = [&](int q) { return (int)(std::find(uq, uq + nu, q) - uq); };
+    for (int i = 0; i < nu; ++i) a.uq[i] = uq[i];
+    for (int i = 0; i < gk; ++i) a.gpos[i] = pos(gate_qubits[i]);
+    for (int i = 0; i < nk; ++i) a.npos[i] = pos(next_qubits[i]);
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
+    const uint64_t B = 1ull << batch_log2;
+    const size_t need = sizeof(double2) * 16 * B + sizeof(double) * 32 * B;
+    if (st->nb_bytes < need) {
+        if (st->nb_mats) cudaFree(st->nb_mats);
+        st->nb_mats = nullptr;
+        st->nb_bytes = 0;
+        CUDA_TRY(cudaMalloc(&st->nb_mats, need));
+        st->nb_bytes = need;
+    }
+    double *dev_out = reinterpret_cast<double *>(st->nb_mats + 16 * B);
+    if (gk) CUDA_TRY(cudaMemcpyAsync(st->nb_mats, mats, sizeof(double2) * 16 * B, cudaMemcpyHostToDevice, st->stream));
+    const uint64_t groups = 1ull << (nsub - nu);
+    const uint64_t want = (groups + 255) / 256;
+    const uint64_t cap = std::max<uint64_t>(1, ((uint64_t)st->sm_count * 16 + B - 1) / B);
+    const int bx = (int)std::max<uint64_t>(1, std::min(want, cap));
+    const int vals = 32;  // 4x4 complex slots per trajectory
+    if (nk) {
+        rc = ensure_work(st, sizeof(double) * vals * bx * B);
+        if (rc) return rc;
+    }
+    const dim3 grid(bx, (unsigned)B);
+    switch (nu) {
+        case 1: noisy_batch_kernel<1><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
+        case 2: noisy_batch_kernel<2><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
+        case 3: noisy_batch_kernel<3><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
+        default: noisy_batch_kernel<4><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (!nk) return QSV_OK;
+    noisy_batch_finish<<<(unsigned)B, 32, 0, st->stream>>>(st->work, bx, vals, dev_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(rdm_out, dev_out, sizeof(double) * vals * B, cudaMemcpyDeviceToHost, st->stream));
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QSV_OK;
 }

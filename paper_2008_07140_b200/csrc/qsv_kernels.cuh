@@ -710,4 +710,168 @@ __global__ void rdm_finish(const double *partial, int n_blocks, int vals, double
     out[k] = s;
 }
 
+// ---------------------------------------------------------------------------
+// batched noisy trajectories (statevector.py:343-357 / noise.py:188-222 per trajectory):
+// B trajectories are consecutive 2^nsub-amplitude blocks of one state (block b = blockIdx.y).
+// One launch applies every trajectory's own dense gate U_b K_c(b) / sqrt(p) on the gate
+// qubits, then accumulates that trajectory's reduced density of the NEXT noisy gate's qubits
+// (its branch weights), so a noisy gate costs one HBM pass, not a weight sweep + an apply.
+// Union qubits uq[0..NU) ascending; gate / next qubits are given as positions in the union
+// (first listed = MSB).
+// ---------------------------------------------------------------------------
+struct NoisyArgs {
+    int nsub;      // qubits per trajectory
+    int uq[4];     // union of gate + next qubits, ascending
+    int gk, nk;    // gate / next qubit counts (0..2)
+    int gpos[2];   // union positions of the gate qubits, MSB first
+    int npos[2];   // union positions of the next qubits, MSB first
+};
+
+template <int NU>
+__device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const double2 *m, int p0) {
+#pragma unroll
+    for (int p = 0; p < NU; ++p) {
+        if (p != p0) continue;  // uniform branch: every index below is compile-time
+#pragma unroll
+        for (int l = 0; l < (1 << NU); ++l) {
+            if ((l >> p) & 1) continue;
+            const double2 x0 = x[l], x1 = x[l | (1 << p)];
+            x[l] = cdot2(m[0], x0, m[1], x1);
+            x[l | (1 << p)] = cdot2(m[2], x0, m[3], x1);
+        }
+    }
+}
+
+template <int NU>
+__device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const double2 *m, int p0, int p1) {
+#pragma unroll
+    for (int pa = 0; pa < NU; ++pa)
+#pragma unroll
+        for (int pb = 0; pb < NU; ++pb) {
+            if (pa == pb || pa != p0 || pb != p1) continue;
+#pragma unroll
+            for (int l = 0; l < (1 << NU); ++l) {
+                if (((l >> pa) & 1) || ((l >> pb) & 1)) continue;
+                const int idx[4] = {l, l | (1 << pb), l | (1 << pa), l | (1 << pa) | (1 << pb)};
+                double2 y[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) y[c] = x[idx[c]];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const double2 p = cdot2(m[4 * r], y[0], m[4 * r + 1], y[1]);
+                    const double2 q = cdot2(m[4 * r + 2], y[2], m[4 * r + 3], y[3]);
+                    x[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
+                }
+            }
+        }
+}
+
+// acc: row-major 4x4 complex slots; the 2^nk x 2^nk block sits top-left
+template <int NU, int D>
+__device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double (&acc)[32], int pa, int pb) {
+#pragma unroll
+    for (int l = 0; l < (1 << NU); ++l) {
+        if (((l >> pa) & 1) || (D == 4 && ((l >> pb) & 1))) continue;
+        int idx[4];
+        if (D == 2) {
+            idx[0] = l, idx[1] = l | (1 << pa), idx[2] = idx[3] = l;
+        } else {
+            idx[0] = l, idx[1] = l | (1 << pb), idx[2] = l | (1 << pa), idx[3] = l | (1 << pa) | (1 << pb);
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r)
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double2 xr = x[idx[r]], xc = x[idx[c]];
+                acc[2 * (r * 4 + c)] = fma(xr.x, xc.x, fma(xr.y, xc.y, acc[2 * (r * 4 + c)]));
+                acc[2 * (r * 4 + c) + 1] = fma(xr.y, xc.x, fma(-xr.x, xc.y, acc[2 * (r * 4 + c) + 1]));
+            }
+    }
+}
+
+template <int NU>
+__device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[32], int nk, int p0, int p1) {
+#pragma unroll
+    for (int pa = 0; pa < NU; ++pa) {
+        if (pa != p0) continue;
+        if (nk == 1) {
+            noisy_rdm_at<NU, 2>(x, acc, pa, 0);
+            continue;
+        }
+#pragma unroll
+        for (int pb = 0; pb < NU; ++pb)
+            if (pb != pa && pb == p1) noisy_rdm_at<NU, 4>(x, acc, pa, pb);
+    }
+}
+
+template <int NU>
+__global__ void __launch_bounds__(256) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,
+                                                          const double2 *__restrict__ mats, double *partial) {
+    constexpr int L = 1 << NU;
+    const uint32_t b = blockIdx.y;
+    __shared__ double2 m[16];
+    if (threadIdx.x < 16) m[threadIdx.x] = mats[(size_t)b * 16 + threadIdx.x];
+    __syncthreads();
+    double acc[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    const uint64_t groups = 1ull << (a.nsub - NU);
+    const uint64_t base = (uint64_t)b << a.nsub;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        uint64_t i = g;
+#pragma unroll
+        for (int p = 0; p < NU; ++p) i = insert_zero(i, a.uq[p]);
+        i |= base;
+        double2 x[L];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            uint64_t o = i;
+#pragma unroll
+            for (int p = 0; p < NU; ++p)
+                if ((l >> p) & 1) o |= 1ull << a.uq[p];
+            x[l] = psi[o];
+        }
+        if (a.gk) {
+            if (a.gk == 1)
+                noisy_mat1<NU>(x, m, a.gpos[0]);
+            else
+                noisy_mat2<NU>(x, m, a.gpos[0], a.gpos[1]);
+#pragma unroll
+            for (int l = 0; l < L; ++l) {
+                uint64_t o = i;
+#pragma unroll
+                for (int p = 0; p < NU; ++p)
+                    if ((l >> p) & 1) o |= 1ull << a.uq[p];
+                psi[o] = x[l];
+            }
+        }
+        if (a.nk) noisy_rdm<NU>(x, acc, a.nk, a.npos[0], a.npos[1]);
+    }
+    if (!a.nk) return;
+    __shared__ double red[8][32];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const double v = warp_sum(acc[k]);
+        if (l == 0) red[w][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
+        partial[((size_t)b * gridDim.x + blockIdx.x) * 32 + threadIdx.x] = s;
+    }
+}
+
+// per-trajectory fixed-order sum of the block partials
+__global__ void noisy_batch_finish(const double *partial, int n_blocks, int vals, double *out) {
+    const uint32_t b = blockIdx.x;
+    const int k = threadIdx.x;
+    if (k >= vals) return;
+    double s = 0.0;
+    for (int i = 0; i < n_blocks; ++i) s += partial[((size_t)b * n_blocks + i) * vals + k];
+    out[(size_t)b * vals + k] = s;
+}
+
 }  // namespace qsv

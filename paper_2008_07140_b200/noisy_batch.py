@@ -1,0 +1,208 @@
+"""Batched noisy trajectories for any Kraus channel.
+
+Per trajectory the semantics are exactly the reference's
+`run_full(program, rng_t, noise_model)` (statevector.py:343-430,
+noise.py:188-222): before each noisy gate the branch weights ||K_i psi||^2
+come from the current state, ONE `rng_t.random()` draw picks the branch, the
+gate U.K_c is applied and the state renormalised when its norm left 1;
+MEASURE draws against p0 and collapses; PMEASURE records a table.  State-
+dependent channels (ampdamp, phasedamp) are therefore supported, not only the
+pre-sampled Pauli case of `trajectories.py`.
+
+B200 layout: the B = 2^b trajectories are consecutive 2^n-amplitude blocks of
+one (n + b)-qubit device state.  Gates without noise are identical for every
+trajectory and run through the fused scheduler over the whole batch
+(`qsv_run`, trajectories as extra top qubits).  A noisy gate or MEASURE is one
+`qsv_noisy_batch_step` launch: every trajectory's own matrix
+U.K_c(t)/sqrt(p) is applied and, in the same pass, every trajectory's
+reduced density of the NEXT noisy gate's qubits is reduced — the weights that
+gate needs — so a run of noisy gates costs one HBM pass + one small D2H each
+(the reference: #Kraus + 2 passes per noisy gate per trajectory).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import gates
+from .errors import DegenerateBranch, DegenerateState, UnsupportedGate
+from .program import Program
+
+_SLOTS = 16  # complex128 slots per trajectory (row-major 4x4) in the step's matrix / rdm buffers
+
+
+@dataclass
+class NoisyBatchResult:
+    """Per-trajectory `RunResult` analogue: cregs[t], tables[t] (list of
+    (qubits, table)) and the batched device `state` (trajectory t's amplitudes
+    are `amplitudes(t)`)."""
+
+    cregs: list
+    tables: list
+    choices: list  # per trajectory: Kraus branch index per noisy gate (diagnostic)
+    state: object = None
+    qubit_count: int = 0
+    stats: dict = field(default_factory=dict)
+
+    def amplitudes(self, t: int) -> np.ndarray:
+        out = np.empty(1 << self.qubit_count, dtype=np.complex128)
+        return self.state.download(out, t << self.qubit_count)
+
+    def close(self) -> None:
+        if self.state is not None:
+            self.state.close()
+            self.state = None
+
+
+def _step_info(inst, noise):
+    """('noisy', dense base with controls embedded, qubits MSB-first, kraus) for a noisy
+    gate; ('measure', None, (q,), None); None for everything else."""
+    if inst.name == "MEASURE":
+        return "measure", None, (inst.qubits[0],), None
+    if not inst.is_gate:
+        return None
+    base, targets, controls = gates.controlled_form(inst)
+    qubits = tuple(controls) + tuple(targets)
+    if len(qubits) > 2:
+        return None
+    kraus = noise.kraus_for(inst, len(qubits))
+    if kraus is None:
+        return None
+    return "noisy", gates.embed_controls(base, len(controls)), qubits, kraus
+
+
+def _weights(rho: np.ndarray, kraus) -> list[float]:
+    """||K psi||^2 = tr(K rho K^dag) for every branch (noise.py:173-185)."""
+    return [float(np.real(np.trace(k @ rho @ k.conj().T))) for k in kraus]
+
+
+def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubits: int = 30,
+                    fuse: bool = True) -> NoisyBatchResult:
+    """Run len(rngs) = 2^b trajectories of `program` under `noise` in one batched state.
+
+    rngs[t] plays the role of the `rng` argument of the reference `run_full` for
+    trajectory t (e.g. `np.random.default_rng(seed_t)`); draws happen in program
+    order, one per noisy gate and per MEASURE, as in the reference."""
+    from .statevector import init_state
+
+    B = len(rngs)
+    if B < 1 or B & (B - 1):
+        raise ValueError("the batch holds a power-of-two number of trajectories")
+    b = B.bit_length() - 1
+    n = program.qubit_count
+    if n > max_qubits:
+        from .errors import TooManyQubits
+
+        raise TooManyQubits(f"{n} qubits exceed the limit of {max_qubits}")
+    L = N.lib()
+    state = init_state(n + b, max_qubits=n + b, device=device)
+    state.set_basis(0)
+    # every trajectory block starts at |0..0>
+    starts = np.zeros(1, dtype=np.complex128)
+    starts[0] = 1.0
+    for t in range(1, B):
+        N.check(L.qsv_upload(state.handle, starts.ctypes.data, t << n, 1))
+    res = NoisyBatchResult(cregs=[[0] * program.creg_count for _ in range(B)], tables=[[] for _ in range(B)],
+                           choices=[[] for _ in range(B)], state=state, qubit_count=n)
+    opts = N.options(fuse=fuse)
+    insts = list(program.instructions)
+    if noise is not None:
+        info = [_step_info(i, noise) for i in insts]
+    else:
+        info = [("measure", None, (i.qubits[0],), None) if i.name == "MEASURE" else None for i in insts]
+    mats = np.zeros((B, _SLOTS), dtype=np.complex128)
+    rdm = np.zeros((B, _SLOTS), dtype=np.complex128)
+    pending: tuple | None = None  # qubits whose per-trajectory rdm is in `rdm`
+    batch: list = []
+    steps = 0
+
+    def flush():
+        nonlocal pending
+        if batch:
+            from .statevector import compile_gates
+
+            rec = compile_gates(batch)
+            st = N.qsv_run_stats()
+            N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(st)))
+            batch.clear()
+            pending = None
+
+    def step(gate_qubits, next_qubits):
+        nonlocal pending, steps
+        gq = (C.c_int32 * 2)(*(list(gate_qubits) + [0, 0])[:2])
+        nq = (C.c_int32 * 2)(*(list(next_qubits) + [0, 0])[:2])
+        N.check(L.qsv_noisy_batch_step(state.handle, b, len(gate_qubits), gq, mats.ctypes.data,
+                                       len(next_qubits), nq, rdm.ctypes.data))
+        steps += 1
+        pending = tuple(next_qubits) if next_qubits else None
+
+    def next_need(pos):
+        """Qubits whose rdm the instruction after `pos` needs, if it is noisy / MEASURE."""
+        if pos + 1 < len(insts) and info[pos + 1] is not None:
+            return info[pos + 1][2]
+        return ()
+
+    for pos, inst in enumerate(insts):
+        kind = info[pos]
+        if kind is None:
+            if inst.name == "PMEASURE":
+                flush()
+                qs = [n + j for j in range(b - 1, -1, -1)] + list(inst.qubits)
+                if len(qs) > 30:
+                    raise UnsupportedGate("PMEASURE table too large for the batch", inst.line)
+                arr = (C.c_int32 * len(qs))(*qs)
+                table = np.zeros(1 << len(qs), dtype=np.float64)
+                N.check(L.qsv_pmeasure(state.handle, arr, len(qs), table.ctypes.data))
+                per = table.reshape(B, -1)
+                for t in range(B):
+                    res.tables[t].append((tuple(inst.qubits), per[t].copy()))
+                pending = None
+            else:
+                batch.append(inst)
+            continue
+        flush()
+        what, u, qubits, kraus = kind
+        if pending != tuple(qubits):
+            step((), qubits)  # weights of this step's qubits
+        D = 1 << len(qubits)
+        rhos = rdm.reshape(B, 4, 4)[:, :D, :D]
+        mats[:] = 0
+        if what == "measure":
+            for t in range(B):
+                p0 = float(rhos[t, 0, 0].real)
+                p1 = float(rhos[t, 1, 1].real)
+                if p0 < 1e-12 and p1 < 1e-12:
+                    raise DegenerateState("measurement of a (numerically) zero state")
+                outcome = 0 if rngs[t].random() < p0 else 1
+                res.cregs[t][inst.creg] = outcome
+                mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
+        else:
+            for t in range(B):
+                probs = _weights(rhos[t], kraus)
+                total = sum(probs)
+                if total < 1e-12:
+                    raise DegenerateBranch("all Kraus branches have ~zero probability")
+                r = rngs[t].random() * total
+                acc, choice = 0.0, len(probs) - 1
+                for i, p in enumerate(probs):
+                    acc += p
+                    if r < acc:
+                        choice = i
+                        break
+                res.choices[t].append(choice)
+                m = u @ kraus[choice]
+                # the reference renormalises by the post-apply norm when it left 1
+                # (noise.py:219-221); for a normalised state that norm is probs[choice]
+                if abs(probs[choice] - 1.0) > 1e-12:
+                    m = m / math.sqrt(probs[choice])
+                mats[t, : D * D] = m.reshape(-1)
+        step(qubits, next_need(pos))
+    flush()
+    state.synchronize()
+    res.stats = {"noisy_steps": steps, "trajectories": B}
+    return res

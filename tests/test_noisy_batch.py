@@ -1,0 +1,108 @@
+"""Batched noisy trajectories for every Kraus channel (noisy_batch.py) against
+the oracle's restatement of the reference trajectory semantics
+(oracle.sample_noisy_gate / measure, restating noise.py:188-222 and
+statevector.py:298-308), trajectory by trajectory with the same seeds."""
+
+import numpy as np
+import pytest
+
+from paper_2008_07140_b200 import _native as N
+from paper_2008_07140_b200.noise import make_noise_model
+from paper_2008_07140_b200.program import parse_program
+from paper_2008_07140_b200.rqc import RqcConfig, generate_rqc
+
+
+def test_step_symbol_declared_and_exported():
+    from conftest import ROOT
+
+    assert "qsv_noisy_batch_step" in (ROOT / "include" / "qsv.h").read_text()
+    assert hasattr(N.lib(), "qsv_noisy_batch_step")
+
+
+def _program(extra=""):
+    return parse_program(generate_rqc(RqcConfig(2, 4, depth=6, seed=7)) + extra)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,p", [("ampdamp", 0.15), ("depolarizing", 0.08), ("phasedamp", 0.2),
+                                    ("bitflip", 0.9), ("bitphaseflip", 0.95)])
+def test_batched_trajectories_match_oracle(kind, p):
+    from oracle import oracle as O
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = _program("PMEASURE 0,3,5\n")
+    B = 16
+    seeds = [1000 + t for t in range(B)]
+    res = run_noisy_batch(prog, make_noise_model(kind, p), [np.random.default_rng(s) for s in seeds])
+    try:
+        for t, s in enumerate(seeds):
+            ref = O.run_full(prog, np.random.default_rng(s), (kind, p))
+            got = res.amplitudes(t)
+            assert np.abs(got - ref.state.amplitudes).max() <= 1e-10, (kind, t)
+            (q, table), = res.tables[t]
+            (rq, rtable), = ref.tables
+            assert tuple(q) == tuple(rq)
+            assert np.abs(table - rtable).max() <= 1e-12
+    finally:
+        res.close()
+
+
+@pytest.mark.gpu
+def test_batched_measure_and_noise_free_gates():
+    """MEASURE per trajectory (own draw, own collapse) between noiseless and
+    noisy gates (noise only on CNOT)."""
+    from oracle import oracle as O
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    text = "QINIT 6\nCREG 2\n" + "".join(f"H {q}\n" for q in range(6)) + \
+        "CNOT 0,1\nT 1\nMEASURE 1,$0\nCNOT 1,2\nRY 3,\"0.4\"\nCNOT 3,4\nMEASURE 4,$1\nCNOT 4,5\nPMEASURE 5,2\n"
+    prog = parse_program(text)
+    B = 32
+    seeds = list(range(B))
+    model = make_noise_model("ampdamp", 0.3, ["CNOT"])
+    res = run_noisy_batch(prog, model, [np.random.default_rng(s) for s in seeds])
+    try:
+        outcomes = set()
+        for t, s in enumerate(seeds):
+            rng = np.random.default_rng(s)
+            st = O.init_state(6)
+            st.amplitudes[:] = 0
+            st.amplitudes[0] = 1
+            cregs = [0, 0]
+            tables = []
+            for inst in prog.instructions:
+                if inst.name == "CNOT":
+                    base, targets, controls = O.controlled_form(inst)
+                    k1 = O.kraus_ops("ampdamp", 0.3)
+                    O.sample_noisy_gate(st, O.embed_controls(base, 1), controls + targets,
+                                        [np.kron(a, b) for a in k1 for b in k1], rng)
+                else:
+                    r = O.OracleResult(cregs=cregs)
+                    O.apply_instruction(st, inst, rng, None, r)
+                    tables += r.tables
+            assert res.cregs[t] == cregs
+            outcomes.add(tuple(cregs))
+            assert np.abs(res.amplitudes(t) - st.amplitudes).max() <= 1e-10
+            assert np.abs(res.tables[t][0][1] - tables[0][1]).max() <= 1e-12
+        assert len(outcomes) > 1  # the trajectories really diverge
+    finally:
+        res.close()
+
+
+@pytest.mark.gpu
+def test_batched_matches_sequential_run_full():
+    """The batched engine and the sequential reference-shaped path (run_full with a
+    noise model) draw identically: same branch choices, same amplitudes."""
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+    from paper_2008_07140_b200.statevector import run_full
+
+    prog = parse_program(generate_rqc(RqcConfig(3, 4, depth=8, seed=3)))
+    model = make_noise_model("depolarizing", 0.02)
+    B = 8
+    res = run_noisy_batch(prog, model, [np.random.default_rng(50 + t) for t in range(B)])
+    try:
+        for t in range(B):
+            ref = run_full(prog, np.random.default_rng(50 + t), model).state.amplitudes
+            assert np.abs(res.amplitudes(t) - ref).max() <= 1e-10
+    finally:
+        res.close()
