@@ -345,6 +345,78 @@ def run_partial_bench(args) -> None:
         print(json.dumps(line), flush=True)
 
 
+NOISY = (4, 5, 20)  # general-channel trajectories: C1-shape RQC (n=20)
+
+
+def run_noisy_bench(args) -> None:
+    """General-channel noisy trajectories (noisy_batch.py): the C1-shape RQC
+    (4x5, 20 cycles, n=20) under amplitude damping p=1e-3 on EVERY gate
+    (state-dependent branch weights, reference noise.py:188-222), 256 trajectories
+    in one batched state.  Each step is one `run_noisy_batch` call through the
+    public API; the metric counts trajectories x gates x 2^n."""
+    import torch
+
+    from paper_2008_07140_b200 import workloads
+    from paper_2008_07140_b200.noise import make_noise_model
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+    from paper_2008_07140_b200.program import parse_program
+
+    rank, _, local = dist_env()
+    torch.cuda.set_device(local)
+    prog = parse_program(workloads.rqc_text(*NOISY, seed=SEED))
+    n = prog.qubit_count
+    G = len(prog.gate_instructions())
+    B = args.trajectories if args.trajectories != 1024 else 256
+    kind, p = "ampdamp", 1e-3
+    model = make_noise_model(kind, p)
+
+    def once(step):
+        rngs = [np.random.default_rng((SEED, step, t)) for t in range(B)]
+        r = run_noisy_batch(prog, model, rngs, device=local)
+        r.close()
+        return r
+
+    for w in range(args.warmup):
+        once(-1 - w)
+    torch.cuda.synchronize()
+    times = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            t0 = time.perf_counter()
+            r = once(k)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+    dt = statistics.median(times)
+    work = float(B) * G * float(1 << n)
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        from oracle import oracle as O
+
+        threads = O.cpu_threads()
+        done, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            O.run_full(prog, np.random.default_rng(done), (kind, p), workers=threads)
+            done += 1
+        cdt = time.perf_counter() - t0
+        cpu = {"value": done * G * float(1 << n) / cdt, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{done} trajectories through oracle run_full with ampdamp noise "
+                         f"({cdt:.1f} s, {threads} threads; #Kraus + 2 state sweeps per noisy gate as "
+                         f"reference noise.py:188-222)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": work / dt, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+                "config": {"workload": f"general-channel trajectories: RQC {NOISY[0]}x{NOISY[1]} "
+                                       f"{NOISY[2]} cycles, n={n}, {kind} p={p} on every gate",
+                           "trajectories": B, "gates": G, "noisy_steps": r.stats["noisy_steps"],
+                           "batched_state_gib": (B << n) * 16 / 2**30,
+                           "timing": "host wall clock around run_noisy_batch (public API, e2e)"},
+                "e2e": {"value": work / dt, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": None},
+                "cpu_baseline": cpu, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
     if args.workload == "traj":
@@ -352,6 +424,9 @@ def run_gpu(args) -> None:
         return
     if args.workload == "partial":
         run_partial_bench(args)
+        return
+    if args.workload == "noisy":
+        run_noisy_bench(args)
         return
     if world > 1:
         from paper_2008_07140_b200 import distributed
@@ -509,7 +584,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--qubits", type=int, default=0)
-    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj", "partial"))
+    ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj", "partial", "noisy"))
     ap.add_argument("--trajectories", type=int, default=1024)
     ap.add_argument("--dedup", action="store_true")
     ap.add_argument("--tile", type=int, default=0)

@@ -76,11 +76,6 @@ def _step_info(inst, noise):
     return "noisy", gates.embed_controls(base, len(controls)), qubits, kraus
 
 
-def _weights(rho: np.ndarray, kraus) -> list[float]:
-    """||K psi||^2 = tr(K rho K^dag) for every branch (noise.py:173-185)."""
-    return [float(np.real(np.trace(k @ rho @ k.conj().T))) for k in kraus]
-
-
 def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubits: int = 30,
                     fuse: bool = True) -> NoisyBatchResult:
     """Run len(rngs) = 2^b trajectories of `program` under `noise` in one batched state.
@@ -182,25 +177,25 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
                 res.cregs[t][inst.creg] = outcome
                 mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
         else:
+            K = np.asarray(kraus)  # (k, D, D)
+            # ||K_i psi_t||^2 = tr(K_i rho_t K_i^dag) for all trajectories and branches at once
+            probs = np.einsum("kij,bjl,kil->bk", K, rhos, K.conj()).real
+            total = probs.sum(axis=1)
+            if (total < 1e-12).any():
+                raise DegenerateBranch("all Kraus branches have ~zero probability")
+            r = np.array([g.random() for g in rngs]) * total
+            cum = np.cumsum(probs, axis=1)  # the reference's running `acc += p` (noise.py:206-212)
+            hit = r[:, None] < cum
+            choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(kraus) - 1)
+            pc = probs[np.arange(B), choice]
+            m = np.einsum("ij,bjk->bik", u, K[choice])
+            # the reference renormalises by the post-apply norm when it left 1
+            # (noise.py:219-221); for a normalised state that norm is probs[choice]
+            renorm = np.abs(pc - 1.0) > 1e-12
+            m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
+            mats[:, : D * D] = m.reshape(B, -1)
             for t in range(B):
-                probs = _weights(rhos[t], kraus)
-                total = sum(probs)
-                if total < 1e-12:
-                    raise DegenerateBranch("all Kraus branches have ~zero probability")
-                r = rngs[t].random() * total
-                acc, choice = 0.0, len(probs) - 1
-                for i, p in enumerate(probs):
-                    acc += p
-                    if r < acc:
-                        choice = i
-                        break
-                res.choices[t].append(choice)
-                m = u @ kraus[choice]
-                # the reference renormalises by the post-apply norm when it left 1
-                # (noise.py:219-221); for a normalised state that norm is probs[choice]
-                if abs(probs[choice] - 1.0) > 1e-12:
-                    m = m / math.sqrt(probs[choice])
-                mats[t, : D * D] = m.reshape(-1)
+                res.choices[t].append(int(choice[t]))
         step(qubits, next_need(pos))
     flush()
     state.synchronize()
