@@ -377,7 +377,7 @@ def run_noisy_bench(args) -> None:
         return r
 
     for w in range(args.warmup):
-        once(-1 - w)
+        once(10_000 + w)
     torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clk:
