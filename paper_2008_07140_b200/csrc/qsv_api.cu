@@ -1678,12 +1678,22 @@ int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *g
         if (rc) return rc;
     }
     const dim3 grid(bx, (unsigned)B);
+#define QSV_NB(NU_, NK_) noisy_batch_kernel<NU_, NK_><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work)
+#define QSV_NB_K(NU_)        \
+    if (nk == 0)             \
+        QSV_NB(NU_, 0);      \
+    else if (nk == 1)        \
+        QSV_NB(NU_, 1);      \
+    else                     \
+        QSV_NB(NU_, 2);
     switch (nu) {
-        case 1: noisy_batch_kernel<1><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
-        case 2: noisy_batch_kernel<2><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
-        case 3: noisy_batch_kernel<3><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
-        default: noisy_batch_kernel<4><<<grid, 256, 0, st->stream>>>(st->amps, a, st->nb_mats, st->work); break;
+        case 1: QSV_NB_K(1) break;
+        case 2: QSV_NB_K(2) break;
+        case 3: QSV_NB_K(3) break;
+        default: QSV_NB_K(4) break;
     }
+#undef QSV_NB_K
+#undef QSV_NB
     CUDA_TRY(cudaGetLastError());
     if (!nk) return QSV_OK;
     noisy_batch_finish<<<(unsigned)B, 32, 0, st->stream>>>(st->work, bx, vals, dev_out);

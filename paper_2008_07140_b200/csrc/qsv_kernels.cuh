@@ -767,8 +767,8 @@ __device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const double2 
 }
 
 // acc: row-major 4x4 complex slots; the 2^nk x 2^nk block sits top-left
-template <int NU, int D>
-__device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double (&acc)[32], int pa, int pb) {
+template <int NU, int D, int A>
+__device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double (&acc)[A], int pa, int pb) {
 #pragma unroll
     for (int l = 0; l < (1 << NU); ++l) {
         if (((l >> pa) & 1) || (D == 4 && ((l >> pb) & 1))) continue;
@@ -783,18 +783,20 @@ __device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double
 #pragma unroll
             for (int c = 0; c < D; ++c) {
                 const double2 xr = x[idx[r]], xc = x[idx[c]];
-                acc[2 * (r * 4 + c)] = fma(xr.x, xc.x, fma(xr.y, xc.y, acc[2 * (r * 4 + c)]));
-                acc[2 * (r * 4 + c) + 1] = fma(xr.y, xc.x, fma(-xr.x, xc.y, acc[2 * (r * 4 + c) + 1]));
+                acc[2 * (r * D + c)] = fma(xr.x, xc.x, fma(xr.y, xc.y, acc[2 * (r * D + c)]));
+                acc[2 * (r * D + c) + 1] = fma(xr.y, xc.x, fma(-xr.x, xc.y, acc[2 * (r * D + c) + 1]));
             }
     }
 }
 
-template <int NU>
-__device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[32], int nk, int p0, int p1) {
+// acc: row-major 2^NK x 2^NK complex block
+template <int NU, int NK>
+__device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[2 << (2 * NK)], int p0,
+                                          int p1) {
 #pragma unroll
     for (int pa = 0; pa < NU; ++pa) {
         if (pa != p0) continue;
-        if (nk == 1) {
+        if (NK == 1) {
             noisy_rdm_at<NU, 2>(x, acc, pa, 0);
             continue;
         }
@@ -804,17 +806,18 @@ __device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&
     }
 }
 
-template <int NU>
+template <int NU, int NK>
 __global__ void __launch_bounds__(256) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,
                                                           const double2 *__restrict__ mats, double *partial) {
     constexpr int L = 1 << NU;
+    constexpr int A = NK ? 2 << (2 * NK) : 2;
     const uint32_t b = blockIdx.y;
     __shared__ double2 m[16];
     if (threadIdx.x < 16) m[threadIdx.x] = mats[(size_t)b * 16 + threadIdx.x];
     __syncthreads();
-    double acc[32];
+    double acc[A];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) acc[k] = 0.0;
+    for (int k = 0; k < A; ++k) acc[k] = 0.0;
     const uint64_t groups = 1ull << (a.nsub - NU);
     const uint64_t base = (uint64_t)b << a.nsub;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -846,21 +849,23 @@ __global__ void __launch_bounds__(256) noisy_batch_kernel(double2 *__restrict__ 
                 psi[o] = x[l];
             }
         }
-        if (a.nk) noisy_rdm<NU>(x, acc, a.nk, a.npos[0], a.npos[1]);
+        if (NK) noisy_rdm<NU, NK>(x, acc, a.npos[0], a.npos[1]);
     }
-    if (!a.nk) return;
-    __shared__ double red[8][32];
+    if (!NK) return;
+    __shared__ double red[8][A];
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < A; ++k) {
         const double v = warp_sum(acc[k]);
         if (l == 0) red[w][k] = v;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
+    if (threadIdx.x < A) {
+        // scatter the 2^NK x 2^NK block into the 4x4 slot layout of the partials
+        const int r = (threadIdx.x >> 1) >> NK, c = (threadIdx.x >> 1) & ((1 << NK) - 1);
         double s = 0.0;
         for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
-        partial[((size_t)b * gridDim.x + blockIdx.x) * 32 + threadIdx.x] = s;
+        partial[((size_t)b * gridDim.x + blockIdx.x) * 32 + 2 * (r * 4 + c) + (threadIdx.x & 1)] = s;
     }
 }
 
