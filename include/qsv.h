@@ -255,6 +255,10 @@ int qsv_max_abs_diff(qsv_state *st, const void *other_device_c128, double *out);
 /* reduced density matrix of 1 or 2 qubits (first listed = MSB), row-major complex
  * 2^nq x 2^nq; branch weights ||K psi||^2 = tr(K rho K^dag) (noise.py:173-185) */
 int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits_msb_first, double *out_c128);
+/* copy n_rows runs of row_len amplitudes starting at row_offsets[r] into host_out (packed,
+ * row-major) with one device gather + one D2H: partial-mode recombination reads each target's
+ * 2^c branch amplitudes (partition.py:182-191) */
+int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint64_t row_len, void *host_out);
 /* batched noisy trajectories (run_full(prog, rng_t, noise) per trajectory, statevector.py:343-357,
  * noise.py:188-222): the state holds B = 2^batch_log2 trajectories as consecutive
  * 2^(n - batch_log2)-amplitude blocks.  In ONE pass: apply trajectory b's own dense gate on

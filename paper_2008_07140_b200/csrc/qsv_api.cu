@@ -1703,4 +1703,28 @@ int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *g
     return QSV_OK;
 }
 
+int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint64_t row_len, void *host_out) {
+    if (n_rows < 0 || n_rows > 65535) return fail(QSV_E_PARSE, "1..65535 rows per gather");
+    if (n_rows == 0 || row_len == 0) return QSV_OK;
+    for (int r = 0; r < n_rows; ++r)
+        if (row_offsets[r] + row_len > st->size()) return fail(QSV_E_PARSE, "gather row out of bounds");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
+    const size_t idx_bytes = ((sizeof(uint64_t) * n_rows + 255) / 256) * 256;
+    const size_t out_bytes = sizeof(double2) * row_len * n_rows;
+    rc = ensure_work(st, idx_bytes + out_bytes);
+    if (rc) return rc;
+    uint64_t *d_offs = reinterpret_cast<uint64_t *>(st->work);
+    double2 *d_out = reinterpret_cast<double2 *>(reinterpret_cast<char *>(st->work) + idx_bytes);
+    CUDA_TRY(cudaMemcpyAsync(d_offs, row_offsets, sizeof(uint64_t) * n_rows, cudaMemcpyHostToDevice, st->stream));
+    const unsigned bx = (unsigned)std::min<uint64_t>((row_len + 255) / 256, 64);
+    gather_rows_kernel<<<dim3(bx, (unsigned)n_rows), 256, 0, st->stream>>>(st->amps, d_offs, row_len, d_out);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(host_out, d_out, out_bytes, cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
 }  // extern "C"

@@ -727,8 +727,12 @@ struct NoisyArgs {
     int npos[2];   // union positions of the next qubits, MSB first
 };
 
+// the per-trajectory matrix is re-read from shared memory (broadcast) at each use: volatile
+// keeps the compiler from hoisting all 16 entries into registers, which would cap occupancy
+__device__ __forceinline__ double2 vld(const volatile double2 *m, int k) { return make_double2(m[k].x, m[k].y); }
+
 template <int NU>
-__device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const double2 *m, int p0) {
+__device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const volatile double2 *m, int p0) {
 #pragma unroll
     for (int p = 0; p < NU; ++p) {
         if (p != p0) continue;  // uniform branch: every index below is compile-time
@@ -736,14 +740,14 @@ __device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const double2 
         for (int l = 0; l < (1 << NU); ++l) {
             if ((l >> p) & 1) continue;
             const double2 x0 = x[l], x1 = x[l | (1 << p)];
-            x[l] = cdot2(m[0], x0, m[1], x1);
-            x[l | (1 << p)] = cdot2(m[2], x0, m[3], x1);
+            x[l] = cdot2(vld(m, 0), x0, vld(m, 1), x1);
+            x[l | (1 << p)] = cdot2(vld(m, 2), x0, vld(m, 3), x1);
         }
     }
 }
 
 template <int NU>
-__device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const double2 *m, int p0, int p1) {
+__device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const volatile double2 *m, int p0, int p1) {
 #pragma unroll
     for (int pa = 0; pa < NU; ++pa)
 #pragma unroll
@@ -758,8 +762,8 @@ __device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const double2 
                 for (int c = 0; c < 4; ++c) y[c] = x[idx[c]];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
-                    const double2 p = cdot2(m[4 * r], y[0], m[4 * r + 1], y[1]);
-                    const double2 q = cdot2(m[4 * r + 2], y[2], m[4 * r + 3], y[3]);
+                    const double2 p = cdot2(vld(m, 4 * r), y[0], vld(m, 4 * r + 1), y[1]);
+                    const double2 q = cdot2(vld(m, 4 * r + 2), y[2], vld(m, 4 * r + 3), y[3]);
                     x[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
                 }
             }
@@ -806,8 +810,12 @@ __device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&
     }
 }
 
+// resident CTAs per SM the register budget is capped for (HBM-bound: occupancy hides latency)
 template <int NU, int NK>
-__global__ void __launch_bounds__(256) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,
+constexpr int noisy_min_blocks() { return NU <= 2 ? (NK == 2 ? 2 : 4) : (NU == 3 ? 2 : 1); }
+
+template <int NU, int NK>
+__global__ void __launch_bounds__(256, noisy_min_blocks<NU, NK>()) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,
                                                           const double2 *__restrict__ mats, double *partial) {
     constexpr int L = 1 << NU;
     constexpr int A = NK ? 2 << (2 * NK) : 2;
@@ -877,6 +885,15 @@ __global__ void noisy_batch_finish(const double *partial, int n_blocks, int vals
     double s = 0.0;
     for (int i = 0; i < n_blocks; ++i) s += partial[((size_t)b * n_blocks + i) * vals + k];
     out[(size_t)b * vals + k] = s;
+}
+
+// rows of `len` amplitudes at arbitrary offsets -> one packed buffer (partial-mode recombination)
+__global__ void gather_rows_kernel(const double2 *__restrict__ psi, const uint64_t *__restrict__ offs, uint64_t len,
+                                   double2 *__restrict__ out) {
+    const uint64_t r = blockIdx.y;
+    const uint64_t o = offs[r];
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < len; k += (uint64_t)gridDim.x * blockDim.x)
+        out[r * len + k] = psi[o + k];
 }
 
 }  // namespace qsv

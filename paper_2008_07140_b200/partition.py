@@ -42,7 +42,6 @@ from .program import Instruction, Program
 
 DEFAULT_BRANCH_BUDGET = 1 << 16
 DEFAULT_BATCH_QUBITS = 28  # 4 GiB per batched half-state
-_FULL_DOWNLOAD_AMPS = 1 << 22  # download whole half-states up to 64 MiB
 
 _PROJ_EQ = np.diag([1.0, 0.0, 0.0, 1.0]).astype(np.complex128)  # keep bit(control) == bit(branch)
 
@@ -221,16 +220,16 @@ def _run_half(triplets, m: int, cb: int, device: int, max_qubits: int, options):
 
 
 def _slices(st, m: int, cb: int, rows) -> dict:
-    """{row: 2^cb amplitudes of half-index `row` across the branches}."""
+    """{row: 2^cb amplitudes of half-index `row` across the branches}: one
+    device gather of the requested rows + one D2H (`qsv_gather_rows`)."""
     rows = sorted(set(rows))
-    if (1 << m) <= _FULL_DOWNLOAD_AMPS or len(rows) << cb >= (1 << m) // 4:
-        full = st.amplitudes.reshape(-1, 1 << cb)
-        return {r: full[r] for r in rows}
     out = {}
-    for r in rows:
-        buf = np.empty(1 << cb, dtype=np.complex128)
-        st.download(buf, r << cb)
-        out[r] = buf
+    for s0 in range(0, len(rows), 4096):
+        part = rows[s0:s0 + 4096]
+        offs = np.array([r << cb for r in part], dtype=np.uint64)
+        buf = np.empty((len(part), 1 << cb), dtype=np.complex128)
+        N.check(N.lib().qsv_gather_rows(st.handle, offs.ctypes.data, len(part), 1 << cb, buf.ctypes.data))
+        out.update(zip(part, buf))
     return out
 
 
@@ -258,8 +257,8 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
     acc = {t: 0j for t, _ in wanted}
     for fixed in range(1 << (plan.c - cb)):
         (tl, ml), (tu, mu) = branch_streams(plan, cb, fixed)
-        lo = _run_half(tl, ml, cb, device, max_qubits, opts)
-        up = _run_half(tu, mu, cb, device, max_qubits, opts)
+        lo = _run_half(tl, ml, cb, device, max_qubits, opts)  # each state runs on its own stream:
+        up = _run_half(tu, mu, cb, device, max_qubits, opts)  # the two halves overlap
         try:
             lo_rows = _slices(lo, ml, cb, rows_lo)
             up_rows = _slices(up, mu, cb, rows_up)
