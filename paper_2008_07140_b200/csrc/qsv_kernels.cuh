@@ -770,7 +770,11 @@ __device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const volatile
         }
 }
 
-// acc: row-major 4x4 complex slots; the 2^nk x 2^nk block sits top-left
+// rho is Hermitian: acc packs row r's diagonal (real) then its upper entries (re, im), D^2 doubles
+__host__ __device__ constexpr int herm_index(int r, int c, int D) {
+    return r + 2 * (r * (D - 1) - r * (r - 1) / 2) + (c == r ? 0 : 1 + 2 * (c - r - 1));
+}
+
 template <int NU, int D, int A>
 __device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double (&acc)[A], int pa, int pb) {
 #pragma unroll
@@ -785,17 +789,21 @@ __device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double
 #pragma unroll
         for (int r = 0; r < D; ++r)
 #pragma unroll
-            for (int c = 0; c < D; ++c) {
+            for (int c = r; c < D; ++c) {
                 const double2 xr = x[idx[r]], xc = x[idx[c]];
-                acc[2 * (r * D + c)] = fma(xr.x, xc.x, fma(xr.y, xc.y, acc[2 * (r * D + c)]));
-                acc[2 * (r * D + c) + 1] = fma(xr.y, xc.x, fma(-xr.x, xc.y, acc[2 * (r * D + c) + 1]));
+                const int k = herm_index(r, c, D);
+                if (c == r) {
+                    acc[k] = fma(xr.x, xr.x, fma(xr.y, xr.y, acc[k]));
+                } else {  // x_r * conj(x_c)
+                    acc[k] = fma(xr.x, xc.x, fma(xr.y, xc.y, acc[k]));
+                    acc[k + 1] = fma(xr.y, xc.x, fma(-xr.x, xc.y, acc[k + 1]));
+                }
             }
     }
 }
 
-// acc: row-major 2^NK x 2^NK complex block
 template <int NU, int NK>
-__device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[2 << (2 * NK)], int p0,
+__device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[1 << (2 * NK)], int p0,
                                           int p1) {
 #pragma unroll
     for (int pa = 0; pa < NU; ++pa) {
@@ -812,13 +820,13 @@ __device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&
 
 // resident CTAs per SM the register budget is capped for (HBM-bound: occupancy hides latency)
 template <int NU, int NK>
-constexpr int noisy_min_blocks() { return NU <= 2 ? (NK == 2 ? 2 : 4) : (NU == 3 ? 2 : 1); }
+constexpr int noisy_min_blocks() { return NU <= 2 ? (NK == 2 ? 2 : 4) : 2; }
 
 template <int NU, int NK>
 __global__ void __launch_bounds__(256, noisy_min_blocks<NU, NK>()) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,
                                                           const double2 *__restrict__ mats, double *partial) {
     constexpr int L = 1 << NU;
-    constexpr int A = NK ? 2 << (2 * NK) : 2;
+    constexpr int A = 1 << (2 * NK);  // packed Hermitian block: D^2 doubles
     const uint32_t b = blockIdx.y;
     __shared__ double2 m[16];
     if (threadIdx.x < 16) m[threadIdx.x] = mats[(size_t)b * 16 + threadIdx.x];
@@ -868,12 +876,17 @@ __global__ void __launch_bounds__(256, noisy_min_blocks<NU, NK>()) noisy_batch_k
         if (l == 0) red[w][k] = v;
     }
     __syncthreads();
-    if (threadIdx.x < A) {
-        // scatter the 2^NK x 2^NK block into the 4x4 slot layout of the partials
-        const int r = (threadIdx.x >> 1) >> NK, c = (threadIdx.x >> 1) & ((1 << NK) - 1);
+    if (threadIdx.x < 32) {
+        // unpack into the row-major 4x4 complex slot layout: upper triangle + real diagonal of
+        // the 2^NK x 2^NK block; every other slot 0 (the host mirrors the lower triangle)
+        constexpr int D = 1 << NK;
+        const int r = (threadIdx.x >> 1) >> 2, c = (threadIdx.x >> 1) & 3, part = threadIdx.x & 1;
         double s = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][threadIdx.x];
-        partial[((size_t)b * gridDim.x + blockIdx.x) * 32 + 2 * (r * 4 + c) + (threadIdx.x & 1)] = s;
+        if (r < D && c < D && r <= c && !(r == c && part)) {
+            const int k = herm_index(r, c, D) + part;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i][k];
+        }
+        partial[((size_t)b * gridDim.x + blockIdx.x) * 32 + threadIdx.x] = s;
     }
 }
 

@@ -165,7 +165,8 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
         if pending != tuple(qubits):
             step((), qubits)  # weights of this step's qubits
         D = 1 << len(qubits)
-        rhos = rdm.reshape(B, 4, 4)[:, :D, :D]
+        up = rdm.reshape(B, 4, 4)[:, :D, :D]  # the kernel returns the upper triangle (rho is Hermitian)
+        rhos = np.triu(up) + np.conj(np.swapaxes(np.triu(up, 1), 1, 2))
         mats[:] = 0
         if what == "measure":
             for t in range(B):
