@@ -820,7 +820,7 @@ __device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&
 
 // resident CTAs per SM the register budget is capped for (HBM-bound: occupancy hides latency)
 template <int NU, int NK>
-constexpr int noisy_min_blocks() { return NU <= 2 ? (NK == 2 ? 2 : 4) : 2; }
+constexpr int noisy_min_blocks() { return NU <= 2 ? (NK == 2 ? 2 : 4) : (NU == 3 ? 2 : 1); }
 
 template <int NU, int NK>
 __global__ void __launch_bounds__(256, noisy_min_blocks<NU, NK>()) noisy_batch_kernel(double2 *__restrict__ psi, const NoisyArgs a,

@@ -60,7 +60,7 @@ class NoisyBatchResult:
 
 
 def _step_info(inst, noise):
-    """('noisy', dense base with controls embedded, qubits MSB-first, kraus) for a noisy
+    """('noisy', dense base with controls embedded, qubits MSB-first, (K, K^dag K)) for a noisy
     gate; ('measure', None, (q,), None); None for everything else."""
     if inst.name == "MEASURE":
         return "measure", None, (inst.qubits[0],), None
@@ -73,7 +73,8 @@ def _step_info(inst, noise):
     kraus = noise.kraus_for(inst, len(qubits))
     if kraus is None:
         return None
-    return "noisy", gates.embed_controls(base, len(controls)), qubits, kraus
+    K = np.asarray(kraus)
+    return "noisy", gates.embed_controls(base, len(controls)), qubits, (K, np.einsum("kji,kjl->kil", K.conj(), K))
 
 
 def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubits: int = 30,
@@ -113,6 +114,7 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
     mats = np.zeros((B, _SLOTS), dtype=np.complex128)
     rdm = np.zeros((B, _SLOTS), dtype=np.complex128)
     pending: tuple | None = None  # qubits whose per-trajectory rdm is in `rdm`
+    choices: list = []  # per noisy gate: the B branch indices
     batch: list = []
     steps = 0
 
@@ -178,16 +180,16 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
                 res.cregs[t][inst.creg] = outcome
                 mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
         else:
-            K = np.asarray(kraus)  # (k, D, D)
-            # ||K_i psi_t||^2 = tr(K_i rho_t K_i^dag) for all trajectories and branches at once
-            probs = np.einsum("kij,bjl,kil->bk", K, rhos, K.conj()).real
+            K, KdK = kraus
+            # ||K_i psi_t||^2 = tr(K_i^dag K_i rho_t) for all trajectories and branches at once
+            probs = np.einsum("klj,bjl->bk", KdK, rhos).real
             total = probs.sum(axis=1)
             if (total < 1e-12).any():
                 raise DegenerateBranch("all Kraus branches have ~zero probability")
             r = np.array([g.random() for g in rngs]) * total
             cum = np.cumsum(probs, axis=1)  # the reference's running `acc += p` (noise.py:206-212)
             hit = r[:, None] < cum
-            choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(kraus) - 1)
+            choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(K) - 1)
             pc = probs[np.arange(B), choice]
             m = np.einsum("ij,bjk->bik", u, K[choice])
             # the reference renormalises by the post-apply norm when it left 1
@@ -195,10 +197,11 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
             renorm = np.abs(pc - 1.0) > 1e-12
             m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
             mats[:, : D * D] = m.reshape(B, -1)
-            for t in range(B):
-                res.choices[t].append(int(choice[t]))
+            choices.append(choice)
         step(qubits, next_need(pos))
     flush()
     state.synchronize()
+    if choices:
+        res.choices = np.stack(choices, axis=1).tolist()
     res.stats = {"noisy_steps": steps, "trajectories": B}
     return res
