@@ -351,7 +351,7 @@ NOISY = (4, 5, 20)  # general-channel trajectories: C1-shape RQC (n=20)
 def run_noisy_bench(args) -> None:
     """General-channel noisy trajectories (noisy_batch.py): the C1-shape RQC
     (4x5, 20 cycles, n=20) under amplitude damping p=1e-3 on EVERY gate
-    (state-dependent branch weights, reference noise.py:188-222), 256 trajectories
+    (state-dependent branch weights, reference noise.py:188-222), 1024 trajectories
     in one batched state.  Each step is one `run_noisy_batch` call through the
     public API; the metric counts trajectories x gates x 2^n."""
     import torch
@@ -366,7 +366,7 @@ def run_noisy_bench(args) -> None:
     prog = parse_program(workloads.rqc_text(*NOISY, seed=SEED))
     n = prog.qubit_count
     G = len(prog.gate_instructions())
-    B = args.trajectories if args.trajectories != 1024 else 256
+    B = args.trajectories  # default 1024, as C5 (one 16 GiB batched state at n=20)
     kind, p = "ampdamp", 1e-3
     model = make_noise_model(kind, p)
 
