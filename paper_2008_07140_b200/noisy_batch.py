@@ -111,6 +111,11 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
         info = [_step_info(i, noise) for i in insts]
     else:
         info = [("measure", None, (i.qubits[0],), None) if i.name == "MEASURE" else None for i in insts]
+    # each trajectory draws exactly once per noisy gate / MEASURE, in program order, so its
+    # whole stream is drawn up front: rng.random(k) yields the same doubles as k scalar calls
+    n_draws = sum(1 for x in info if x is not None)
+    uniforms = np.stack([g.random(n_draws) for g in rngs]) if n_draws else None
+    draw = 0
     mats = np.zeros((B, _SLOTS), dtype=np.complex128)
     rdm = np.zeros((B, _SLOTS), dtype=np.complex128)
     pending: tuple | None = None  # qubits whose per-trajectory rdm is in `rdm`
@@ -176,7 +181,7 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
                 p1 = float(rhos[t, 1, 1].real)
                 if p0 < 1e-12 and p1 < 1e-12:
                     raise DegenerateState("measurement of a (numerically) zero state")
-                outcome = 0 if rngs[t].random() < p0 else 1
+                outcome = 0 if uniforms[t, draw] < p0 else 1
                 res.cregs[t][inst.creg] = outcome
                 mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
         else:
@@ -186,7 +191,7 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
             total = probs.sum(axis=1)
             if (total < 1e-12).any():
                 raise DegenerateBranch("all Kraus branches have ~zero probability")
-            r = np.array([g.random() for g in rngs]) * total
+            r = uniforms[:, draw] * total
             cum = np.cumsum(probs, axis=1)  # the reference's running `acc += p` (noise.py:206-212)
             hit = r[:, None] < cum
             choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(K) - 1)
@@ -198,6 +203,7 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
             m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
             mats[:, : D * D] = m.reshape(B, -1)
             choices.append(choice)
+        draw += 1
         step(qubits, next_need(pos))
     flush()
     state.synchronize()

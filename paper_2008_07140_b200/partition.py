@@ -204,10 +204,36 @@ def branch_streams(plan: PartitionPlan, cb: int, fixed: int = 0):
     return (halves["lower"], cut + cb), (halves["upper"], n - cut + cb)
 
 
-def _run_half(triplets, m: int, cb: int, device: int, max_qubits: int, options):
+# device states kept between run_partial calls (keyed by device and qubit count), so
+# repeated calls do not pay cudaMalloc/cudaFree of two multi-GiB buffers each time
+_POOL: dict = {}
+
+
+def release_cached_states() -> None:
+    """Free the device states run_partial keeps for reuse."""
+    for sts in _POOL.values():
+        for st in sts:
+            st.close()
+    _POOL.clear()
+
+
+def _take_state(m: int, device: int):
     from .statevector import init_state
 
-    st = init_state(m, max_qubits=max(max_qubits, m), device=device)
+    free = _POOL.get((device, m))
+    if free:
+        return free.pop()
+    if _POOL:  # keep only states of the current shape
+        release_cached_states()
+    return init_state(m, max_qubits=m, device=device)
+
+
+def _give_state(st, device: int) -> None:
+    _POOL.setdefault((device, st.qubit_count), []).append(st)
+
+
+def _run_half(triplets, m: int, cb: int, device: int, max_qubits: int, options):
+    st = _take_state(m, device)
     st.set_basis(0)
     if cb:
         ones = np.ones(1 << cb, dtype=np.complex128)  # every branch starts at |0..0>
@@ -263,8 +289,8 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
             lo_rows = _slices(lo, ml, cb, rows_lo)
             up_rows = _slices(up, mu, cb, rows_up)
         finally:
-            lo.close()
-            up.close()
+            _give_state(lo, device)
+            _give_state(up, device)
         for (t, _), rl, ru in zip(wanted, rows_lo, rows_up):
             acc[t] += complex(np.dot(up_rows[ru], lo_rows[rl]))  # branch order b = 0 .. 2^cb - 1
     return acc
