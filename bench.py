@@ -409,6 +409,7 @@ def run_noisy_bench(args) -> None:
                 "config": {"workload": f"general-channel trajectories: RQC {NOISY[0]}x{NOISY[1]} "
                                        f"{NOISY[2]} cycles, n={n}, {kind} p={p} on every gate",
                            "trajectories": B, "gates": G, "noisy_steps": r.stats["noisy_steps"],
+                           "step_ms": [round(t * 1e3, 1) for t in times],
                            "batched_state_gib": (B << n) * 16 / 2**30,
                            "timing": "host wall clock around run_noisy_batch (public API, e2e)"},
                 "e2e": {"value": work / dt, "unit": UNIT, "h2d_bytes_per_step": 0,

@@ -134,6 +134,9 @@ int qsv_device_ptr(qsv_state *st, void **out);
 int qsv_set_basis(qsv_state *st, uint64_t index);
 int qsv_upload(qsv_state *st, const void *host_c128, uint64_t offset, uint64_t count);
 int qsv_download(qsv_state *st, void *host_c128, uint64_t offset, uint64_t count);
+/* amplitude k of host_c128 -> index offset + k * stride, k < count (one 2-D copy): the start
+ * amplitudes of batched trajectory blocks (noisy_batch.py) */
+int qsv_upload_strided(qsv_state *st, const void *host_c128, uint64_t offset, uint64_t count, uint64_t stride);
 /* enqueues the download on the state's stream and returns: `host_c128` must be
  * pinned and is complete after qsv_synchronize(st) (overlaps another state's
  * simulation; used by the batched run, statevector.run_batch) */

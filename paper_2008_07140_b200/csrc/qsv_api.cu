@@ -1727,4 +1727,16 @@ int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint
     return QSV_OK;
 }
 
+int qsv_upload_strided(qsv_state *st, const void *host, uint64_t offset, uint64_t count, uint64_t stride) {
+    if (count == 0) return QSV_OK;
+    if (stride == 0 || offset + (count - 1) * stride >= st->size()) return fail(QSV_E_PARSE, "strided upload out of bounds");
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    rc = materialize(st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpy2DAsync(st->amps + offset, stride * 16, host, 16, 16, count, cudaMemcpyHostToDevice, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QSV_OK;
+}
+
 }  // extern "C"
