@@ -12,4 +12,9 @@ timeout 900 python bench.py --workload qft --no-e2e --no-cpu-baseline > gpurun_o
 timeout 900 python bench.py --workload traj > gpurun_out/bench_traj.json 2>> gpurun_out/bench_full.err; echo "traj rc=$?"
 timeout 900 python bench.py --workload traj --dedup > gpurun_out/bench_traj_dedup.json 2>> gpurun_out/bench_full.err; echo "traj dedup rc=$?"
 timeout 900 python bench.py --qubits 32 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_n32.json 2>> gpurun_out/bench_full.err; echo "n32 rc=$?"
+timeout 900 python bench.py --workload partial > gpurun_out/bench_partial.json 2>> gpurun_out/bench_full.err; echo "partial rc=$?"
+timeout 900 python bench.py --workload noisy > gpurun_out/bench_noisy.json 2>> gpurun_out/bench_full.err; echo "noisy rc=$?"
+NCMD="python bench.py --workload noisy --steps 1 --warmup 1 --no-cpu-baseline --trajectories 256"
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv -k regex:noisy_batch -c 60 --log-file gpurun_out/noisy_launches.csv $NCMD > gpurun_out/ncu_noisy_l.log 2>&1; echo "noisy launches rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:noisy_batch_kernel -s 30 -c 1 -o gpurun_out/prof_noisy -f $NCMD > gpurun_out/ncu_noisy_full.log 2>&1; echo "noisy full rc=$?"
 timeout 600 python scripts/exchange_pass_bench.py > gpurun_out/exchange_pass.log 2>&1; echo "exchange rc=$?"
