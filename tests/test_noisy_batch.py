@@ -106,3 +106,21 @@ def test_batched_matches_sequential_run_full():
             assert np.abs(res.amplitudes(t) - ref).max() <= 1e-10
     finally:
         res.close()
+
+
+@pytest.mark.gpu
+def test_batched_without_noise_and_single_trajectory():
+    """noise=None: only MEASURE draws; B = 1 is the reference's single run_full."""
+    from oracle import oracle as O
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = parse_program("QINIT 3\nCREG 1\nH 0\nCNOT 0,1\nMEASURE 1,$0\nH 2\n")
+    res = run_noisy_batch(prog, None, [np.random.default_rng(9)])
+    try:
+        ref = O.run_full(prog, np.random.default_rng(9))
+        assert res.cregs[0] == ref.cregs
+        assert np.abs(res.amplitudes(0) - ref.state.amplitudes).max() <= 1e-12
+    finally:
+        res.close()
+    with pytest.raises(ValueError):
+        run_noisy_batch(prog, None, [np.random.default_rng(0)] * 3)

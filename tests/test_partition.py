@@ -178,3 +178,13 @@ def test_run_partial_gpu_matches_full_state():
     all_t = [format(i, "08b") for i in range(256)]
     tot = sum(abs(a) ** 2 for a in run_partial(small, 4, all_t).values())
     assert tot == pytest.approx(1.0, abs=1e-9)
+
+
+@pytest.mark.gpu
+def test_run_partial_gpu_edge_cases():
+    """No targets, duplicate targets, no crossing gates (c = 0), PMEASURE ignored."""
+    prog = parse_program("QINIT 4\nH 0\nCNOT 0,1\nH 2\nCNOT 2,3\nPMEASURE 0,1\n")
+    assert run_partial(prog, 2, []) == {}
+    amps = run_partial(prog, 2, ["0000", "0000", "1111"])
+    assert list(amps) == ["0000", "1111"]
+    assert abs(amps["0000"] - 0.5) < 1e-12 and abs(amps["1111"] - 0.5) < 1e-12
