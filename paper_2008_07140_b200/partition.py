@@ -272,6 +272,7 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
     plan = plan_partition(program, cut, branch_budget)
     n = program.qubit_count
     wanted = [(t, parse_target(t, n)) for t in targets]
+    wanted = list(dict(wanted).items())  # a repeated target string is one output entry (partition.py:184-191)
     m_half = max(cut, n - cut)
     if m_half > max_qubits:
         raise TooManyQubits(f"{m_half} qubits in one half exceed the limit of {max_qubits}")
