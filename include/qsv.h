@@ -273,6 +273,13 @@ int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint
 int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits_msb_first,
                          const double *mats_c128, int nk, const int32_t *next_qubits_msb_first,
                          double *rdm_out_c128);
+/* the same step split in two: _async enqueues it on the state's stream (mats are staged through
+ * pinned memory, so the caller may reuse them on return) and _wait blocks until it finished and
+ * copies the reduced densities out (rdm_out may be NULL).  Two batched states on their own
+ * streams then overlap one group's host sampling with the other group's pass. */
+int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits_msb_first,
+                               const double *mats_c128, int nk, const int32_t *next_qubits_msb_first);
+int qsv_noisy_batch_wait(qsv_state *st, int batch_log2, double *rdm_out_c128);
 
 #ifdef __cplusplus
 }

@@ -98,6 +98,8 @@ _SIGNATURES = {
     "qsv_reduced_density": ([_P, C.c_int, _P, _P], C.c_int),
     "qsv_upload_strided": ([_P, _P, C.c_uint64, C.c_uint64, C.c_uint64], C.c_int),
     "qsv_gather_rows": ([_P, _P, C.c_int, C.c_uint64, _P], C.c_int),
+    "qsv_noisy_batch_step_async": ([_P, C.c_int, C.c_int, _P, _P, C.c_int, _P], C.c_int),
+    "qsv_noisy_batch_wait": ([_P, C.c_int, _P], C.c_int),
     "qsv_noisy_batch_step": ([_P, C.c_int, C.c_int, _P, _P, C.c_int, _P, _P], C.c_int),
     "qsv_plan_kernel_source": ([_P, C.c_int64, C.c_int, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_plan_exchange_source": ([_P, C.c_int64, C.c_int, C.c_uint64, C.c_char_p, C.c_int64, C.POINTER(C.c_int64)],

@@ -64,6 +64,7 @@ struct qsv_state {
     int sm_count = 148;
     double2 *nb_mats = nullptr;  // batched noisy step: per-trajectory gate matrices + rdm out
     size_t nb_bytes = 0;
+    double2 *nb_host = nullptr;  // pinned staging of the same two regions (async steps)
     uint64_t size() const { return 1ull << n; }
 };
 
@@ -439,6 +440,7 @@ int qsv_destroy(qsv_state *st) {
     if (st->plan_buf) cudaFree(st->plan_buf);
     if (st->barrier) cudaFree(st->barrier);
     if (st->nb_mats) cudaFree(st->nb_mats);
+    if (st->nb_host) cudaFreeHost(st->nb_host);
     if (st->own_stream) cudaStreamDestroy(st->stream);
     delete st;
     return QSV_OK;
@@ -1621,8 +1623,8 @@ int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *ou
     return QSV_OK;
 }
 
-int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits, const double *mats,
-                         int nk, const int32_t *next_qubits, double *rdm_out) {
+int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits,
+                               const double *mats, int nk, const int32_t *next_qubits) {
     const int nsub = st->n - batch_log2;
     if (batch_log2 < 0 || nsub < 1 || batch_log2 > 16) return fail(QSV_E_PARSE, "bad batch size");
     if (gk < 0 || gk > 2 || nk < 0 || nk > 2) return fail(QSV_E_UNSUPPORTED, "noisy step acts on 0..2 qubits");
@@ -1660,14 +1662,24 @@ int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *g
     const uint64_t B = 1ull << batch_log2;
     const size_t need = sizeof(double2) * 16 * B + sizeof(double) * 32 * B;
     if (st->nb_bytes < need) {
+        CUDA_TRY(cudaStreamSynchronize(st->stream));
         if (st->nb_mats) cudaFree(st->nb_mats);
-        st->nb_mats = nullptr;
+        if (st->nb_host) cudaFreeHost(st->nb_host);
+        st->nb_mats = st->nb_host = nullptr;
         st->nb_bytes = 0;
         CUDA_TRY(cudaMalloc(&st->nb_mats, need));
+        CUDA_TRY(cudaHostAlloc(&st->nb_host, need, cudaHostAllocDefault));
         st->nb_bytes = need;
     }
     double *dev_out = reinterpret_cast<double *>(st->nb_mats + 16 * B);
-    if (gk) CUDA_TRY(cudaMemcpyAsync(st->nb_mats, mats, sizeof(double2) * 16 * B, cudaMemcpyHostToDevice, st->stream));
+    double *host_out = reinterpret_cast<double *>(st->nb_host + 16 * B);
+    if (gk) {
+        // the previous step on this stream has completed its copy (callers wait for it before
+        // building the next matrices), so the pinned staging area is free
+        std::memcpy(st->nb_host, mats, sizeof(double2) * 16 * B);
+        CUDA_TRY(cudaMemcpyAsync(st->nb_mats, st->nb_host, sizeof(double2) * 16 * B, cudaMemcpyHostToDevice,
+                                 st->stream));
+    }
     const uint64_t groups = 1ull << (nsub - nu);
     const uint64_t want = (groups + 255) / 256;
     const uint64_t cap = std::max<uint64_t>(1, ((uint64_t)st->sm_count * 16 + B - 1) / B);
@@ -1698,9 +1710,25 @@ int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *g
     if (!nk) return QSV_OK;
     noisy_batch_finish<<<(unsigned)B, 32, 0, st->stream>>>(st->work, bx, vals, dev_out);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(rdm_out, dev_out, sizeof(double) * vals * B, cudaMemcpyDeviceToHost, st->stream));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(cudaMemcpyAsync(host_out, dev_out, sizeof(double) * vals * B, cudaMemcpyDeviceToHost, st->stream));
     return QSV_OK;
+}
+
+int qsv_noisy_batch_wait(qsv_state *st, int batch_log2, double *rdm_out) {
+    int rc = set_device(st->device);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    const uint64_t B = 1ull << batch_log2;
+    if (rdm_out && st->nb_host && st->nb_bytes >= sizeof(double2) * 16 * B + sizeof(double) * 32 * B)
+        std::memcpy(rdm_out, st->nb_host + 16 * B, sizeof(double) * 32 * B);
+    return QSV_OK;
+}
+
+int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits, const double *mats,
+                         int nk, const int32_t *next_qubits, double *rdm_out) {
+    const int rc = qsv_noisy_batch_step_async(st, batch_log2, gk, gate_qubits, mats, nk, next_qubits);
+    if (rc) return rc;
+    return qsv_noisy_batch_wait(st, batch_log2, nk ? rdm_out : nullptr);
 }
 
 int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint64_t row_len, void *host_out) {

@@ -10,14 +10,17 @@ dependent channels (ampdamp, phasedamp) are therefore supported, not only the
 pre-sampled Pauli case of `trajectories.py`.
 
 B200 layout: the B = 2^b trajectories are consecutive 2^n-amplitude blocks of
-one (n + b)-qubit device state.  Gates without noise are identical for every
-trajectory and run through the fused scheduler over the whole batch
-(`qsv_run`, trajectories as extra top qubits).  A noisy gate or MEASURE is one
+batched device states (two groups of B/2, each an (n + b - 1)-qubit state on
+its own stream).  Gates without noise are identical for every trajectory and
+run through the fused scheduler over a whole group (`qsv_run`, trajectories
+as extra top qubits).  A noisy gate or MEASURE is one
 `qsv_noisy_batch_step` launch: every trajectory's own matrix
 U.K_c(t)/sqrt(p) is applied and, in the same pass, every trajectory's
 reduced density of the NEXT noisy gate's qubits is reduced — the weights that
 gate needs — so a run of noisy gates costs one HBM pass + one small D2H each
-(the reference: #Kraus + 2 passes per noisy gate per trajectory).
+(the reference: #Kraus + 2 passes per noisy gate per trajectory).  Steps are
+enqueued asynchronously (`qsv_noisy_batch_step_async` / `_wait`), so one
+group's host sampling overlaps the other group's pass.
 """
 
 from __future__ import annotations
@@ -39,7 +42,7 @@ _SLOTS = 16  # complex128 slots per trajectory (row-major 4x4) in the step's mat
 @dataclass
 class NoisyBatchResult:
     """Per-trajectory `RunResult` analogue: cregs[t], tables[t] (list of
-    (qubits, table)) and the batched device `state` (trajectory t's amplitudes
+    (qubits, table)) and the batched device `states` (trajectory t's amplitudes
     are `amplitudes(t)`)."""
 
     cregs: list
@@ -49,14 +52,19 @@ class NoisyBatchResult:
     qubit_count: int = 0
     stats: dict = field(default_factory=dict)
 
+    states: list = field(default_factory=list)  # one batched state per group
+    group_log2: int = 0  # trajectories per group = 2^group_log2
+
     def amplitudes(self, t: int) -> np.ndarray:
         out = np.empty(1 << self.qubit_count, dtype=np.complex128)
-        return self.state.download(out, t << self.qubit_count)
+        g, k = divmod(t, 1 << self.group_log2)
+        return self.states[g].download(out, k << self.qubit_count)
 
     def close(self) -> None:
-        if self.state is not None:
-            self.state.close()
-            self.state = None
+        for st in self.states:
+            st.close()
+        self.states = []
+        self.state = None
 
 
 def _step_info(inst, noise):
@@ -77,13 +85,40 @@ def _step_info(inst, noise):
     return "noisy", gates.embed_controls(base, len(controls)), qubits, (K, np.einsum("kji,kjl->kil", K.conj(), K))
 
 
+class _Group:
+    """Trajectories [lo, lo + 2^bg) in one batched device state on its own stream."""
+
+    def __init__(self, state, lo: int, bg: int):
+        self.state, self.lo, self.bg = state, lo, bg
+        self.B = 1 << bg
+        self.mats = np.zeros((self.B, _SLOTS), dtype=np.complex128)
+        self.rdm = np.zeros((self.B, _SLOTS), dtype=np.complex128)
+        self.pending: tuple | None = None  # qubits whose rdm the in-flight / last step reduces
+        self.inflight = False
+
+    def launch(self, gate_qubits, next_qubits) -> None:
+        gq = (C.c_int32 * 2)(*(list(gate_qubits) + [0, 0])[:2])
+        nq = (C.c_int32 * 2)(*(list(next_qubits) + [0, 0])[:2])
+        N.check(N.lib().qsv_noisy_batch_step_async(self.state.handle, self.bg, len(gate_qubits), gq,
+                                                   self.mats.ctypes.data, len(next_qubits), nq))
+        self.inflight = True
+        self.pending = tuple(next_qubits) if next_qubits else None
+
+    def wait(self) -> None:
+        if self.inflight:
+            N.check(N.lib().qsv_noisy_batch_wait(self.state.handle, self.bg, self.rdm.ctypes.data))
+            self.inflight = False
+
+
 def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubits: int = 30,
-                    fuse: bool = True) -> NoisyBatchResult:
-    """Run len(rngs) = 2^b trajectories of `program` under `noise` in one batched state.
+                    fuse: bool = True, groups: int = 2) -> NoisyBatchResult:
+    """Run len(rngs) = 2^b trajectories of `program` under `noise`.
 
     rngs[t] plays the role of the `rng` argument of the reference `run_full` for
     trajectory t (e.g. `np.random.default_rng(seed_t)`); draws happen in program
-    order, one per noisy gate and per MEASURE, as in the reference."""
+    order, one per noisy gate and per MEASURE, as in the reference.  The batch is
+    split into `groups` (1 or 2) batched states on their own streams: while one
+    group's pass runs, the host samples the other group's branches."""
     from .statevector import init_state
 
     B = len(rngs)
@@ -95,14 +130,26 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
         from .errors import TooManyQubits
 
         raise TooManyQubits(f"{n} qubits exceed the limit of {max_qubits}")
+    G = 2 if (groups >= 2 and B >= 2) else 1
+    bg = b - (G - 1)
     L = N.lib()
-    state = init_state(n + b, max_qubits=n + b, device=device)
-    state.set_basis(0)
-    # every trajectory block starts at |0..0>: amplitude 1 at t << n (one strided copy)
-    starts = np.ones(B, dtype=np.complex128)
-    N.check(L.qsv_upload_strided(state.handle, starts.ctypes.data, 0, B, 1 << n))
+    grps = []
+    try:
+        for g in range(G):
+            st = init_state(n + bg, max_qubits=n + bg, device=device)
+            grps.append(_Group(st, g << bg, bg))
+            st.set_basis(0)
+            # every trajectory block starts at |0..0>: amplitude 1 at t << n (one strided copy)
+            starts = np.ones(1 << bg, dtype=np.complex128)
+            N.check(L.qsv_upload_strided(st.handle, starts.ctypes.data, 0, 1 << bg, 1 << n))
+    except Exception:
+        for gr in grps:
+            gr.state.close()
+        raise
     res = NoisyBatchResult(cregs=[[0] * program.creg_count for _ in range(B)], tables=[[] for _ in range(B)],
-                           choices=[[] for _ in range(B)], state=state, qubit_count=n)
+                           choices=[[] for _ in range(B)], state=grps[0].state, qubit_count=n)
+    res.states = [gr.state for gr in grps]
+    res.group_log2 = bg
     opts = N.options(fuse=fuse)
     insts = list(program.instructions)
     if noise is not None:
@@ -114,32 +161,20 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
     n_draws = sum(1 for x in info if x is not None)
     uniforms = np.stack([g.random(n_draws) for g in rngs]) if n_draws else None
     draw = 0
-    mats = np.zeros((B, _SLOTS), dtype=np.complex128)
-    rdm = np.zeros((B, _SLOTS), dtype=np.complex128)
-    pending: tuple | None = None  # qubits whose per-trajectory rdm is in `rdm`
     choices: list = []  # per noisy gate: the B branch indices
     batch: list = []
     steps = 0
 
     def flush():
-        nonlocal pending
         if batch:
             from .statevector import compile_gates
 
             rec = compile_gates(batch)
-            st = N.qsv_run_stats()
-            N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(st)))
+            for gr in grps:
+                stt = N.qsv_run_stats()
+                N.check(L.qsv_run(gr.state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(stt)))
+                gr.pending = None
             batch.clear()
-            pending = None
-
-    def step(gate_qubits, next_qubits):
-        nonlocal pending, steps
-        gq = (C.c_int32 * 2)(*(list(gate_qubits) + [0, 0])[:2])
-        nq = (C.c_int32 * 2)(*(list(next_qubits) + [0, 0])[:2])
-        N.check(L.qsv_noisy_batch_step(state.handle, b, len(gate_qubits), gq, mats.ctypes.data,
-                                       len(next_qubits), nq, rdm.ctypes.data))
-        steps += 1
-        pending = tuple(next_qubits) if next_qubits else None
 
     def next_need(pos):
         """Qubits whose rdm the instruction after `pos` needs, if it is noisy / MEASURE."""
@@ -152,60 +187,71 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
         if kind is None:
             if inst.name == "PMEASURE":
                 flush()
-                qs = [n + j for j in range(b - 1, -1, -1)] + list(inst.qubits)
-                if len(qs) > 30:
-                    raise UnsupportedGate("PMEASURE table too large for the batch", inst.line)
-                arr = (C.c_int32 * len(qs))(*qs)
-                table = np.zeros(1 << len(qs), dtype=np.float64)
-                N.check(L.qsv_pmeasure(state.handle, arr, len(qs), table.ctypes.data))
-                per = table.reshape(B, -1)
-                for t in range(B):
-                    res.tables[t].append((tuple(inst.qubits), per[t].copy()))
-                pending = None
+                for gr in grps:
+                    qs = [n + j for j in range(bg - 1, -1, -1)] + list(inst.qubits)
+                    if len(qs) > 30:
+                        raise UnsupportedGate("PMEASURE table too large for the batch", inst.line)
+                    arr = (C.c_int32 * len(qs))(*qs)
+                    table = np.zeros(1 << len(qs), dtype=np.float64)
+                    N.check(L.qsv_pmeasure(gr.state.handle, arr, len(qs), table.ctypes.data))
+                    per = table.reshape(gr.B, -1)
+                    for t in range(gr.B):
+                        res.tables[gr.lo + t].append((tuple(inst.qubits), per[t].copy()))
             else:
                 batch.append(inst)
             continue
         flush()
         what, u, qubits, kraus = kind
-        if pending != tuple(qubits):
-            step((), qubits)  # weights of this step's qubits
         D = 1 << len(qubits)
-        up = rdm.reshape(B, 4, 4)[:, :D, :D]  # the kernel returns the upper triangle (rho is Hermitian)
-        rhos = np.triu(up) + np.conj(np.swapaxes(np.triu(up, 1), 1, 2))
-        mats[:] = 0
-        if what == "measure":
-            for t in range(B):
-                p0 = float(rhos[t, 0, 0].real)
-                p1 = float(rhos[t, 1, 1].real)
-                if p0 < 1e-12 and p1 < 1e-12:
-                    raise DegenerateState("measurement of a (numerically) zero state")
-                outcome = 0 if uniforms[t, draw] < p0 else 1
-                res.cregs[t][inst.creg] = outcome
-                mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
-        else:
-            K, KdK = kraus
-            # ||K_i psi_t||^2 = tr(K_i^dag K_i rho_t) for all trajectories and branches at once
-            probs = np.einsum("klj,bjl->bk", KdK, rhos).real
-            total = probs.sum(axis=1)
-            if (total < 1e-12).any():
-                raise DegenerateBranch("all Kraus branches have ~zero probability")
-            r = uniforms[:, draw] * total
-            cum = np.cumsum(probs, axis=1)  # the reference's running `acc += p` (noise.py:206-212)
-            hit = r[:, None] < cum
-            choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(K) - 1)
-            pc = probs[np.arange(B), choice]
-            m = np.einsum("ij,bjk->bik", u, K[choice])
-            # the reference renormalises by the post-apply norm when it left 1
-            # (noise.py:219-221); for a normalised state that norm is probs[choice]
-            renorm = np.abs(pc - 1.0) > 1e-12
-            m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
-            mats[:, : D * D] = m.reshape(B, -1)
-            choices.append(choice)
+        nxt = next_need(pos)
+        step_choice = []
+        for gr in grps:
+            if gr.pending != tuple(qubits):
+                gr.launch((), qubits)  # weights of this step's qubits
+                steps += 1
+            gr.wait()
+            Bg, U = gr.B, uniforms[gr.lo:gr.lo + gr.B, draw]
+            up = gr.rdm.reshape(Bg, 4, 4)[:, :D, :D]  # the kernel returns the upper triangle
+            rhos = np.triu(up) + np.conj(np.swapaxes(np.triu(up, 1), 1, 2))  # (rho is Hermitian)
+            gr.mats[:] = 0
+            if what == "measure":
+                for t in range(Bg):
+                    p0 = float(rhos[t, 0, 0].real)
+                    p1 = float(rhos[t, 1, 1].real)
+                    if p0 < 1e-12 and p1 < 1e-12:
+                        raise DegenerateState("measurement of a (numerically) zero state")
+                    outcome = 0 if U[t] < p0 else 1
+                    res.cregs[gr.lo + t][inst.creg] = outcome
+                    gr.mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
+            else:
+                K, KdK = kraus
+                # ||K_i psi_t||^2 = tr(K_i^dag K_i rho_t) for all trajectories and branches at once
+                probs = np.einsum("klj,bjl->bk", KdK, rhos).real
+                total = probs.sum(axis=1)
+                if (total < 1e-12).any():
+                    raise DegenerateBranch("all Kraus branches have ~zero probability")
+                r = U * total
+                cum = np.cumsum(probs, axis=1)  # the reference's running `acc += p` (noise.py:206-212)
+                hit = r[:, None] < cum
+                choice = np.where(hit.any(axis=1), hit.argmax(axis=1), len(K) - 1)
+                pc = probs[np.arange(Bg), choice]
+                m = np.einsum("ij,bjk->bik", u, K[choice])
+                # the reference renormalises by the post-apply norm when it left 1
+                # (noise.py:219-221); for a normalised state that norm is probs[choice]
+                renorm = np.abs(pc - 1.0) > 1e-12
+                m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
+                gr.mats[:, : D * D] = m.reshape(Bg, -1)
+                step_choice.append(choice)
+            gr.launch(qubits, nxt)
+            steps += 1
+        if step_choice:
+            choices.append(np.concatenate(step_choice))
         draw += 1
-        step(qubits, next_need(pos))
     flush()
-    state.synchronize()
+    for gr in grps:
+        gr.wait()
+        gr.state.synchronize()
     if choices:
         res.choices = np.stack(choices, axis=1).tolist()
-    res.stats = {"noisy_steps": steps, "trajectories": B}
+    res.stats = {"noisy_steps": steps, "trajectories": B, "groups": G}
     return res

@@ -124,3 +124,22 @@ def test_batched_without_noise_and_single_trajectory():
         res.close()
     with pytest.raises(ValueError):
         run_noisy_batch(prog, None, [np.random.default_rng(0)] * 3)
+
+
+@pytest.mark.gpu
+def test_one_and_two_groups_agree():
+    """Splitting the batch over two asynchronous states changes nothing per trajectory."""
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = _program("PMEASURE 1,2\n")
+    model = make_noise_model("depolarizing", 0.05)
+    a = run_noisy_batch(prog, model, [np.random.default_rng(70 + t) for t in range(8)], groups=1)
+    b = run_noisy_batch(prog, model, [np.random.default_rng(70 + t) for t in range(8)], groups=2)
+    try:
+        assert a.choices == b.choices
+        for t in range(8):
+            assert np.abs(a.amplitudes(t) - b.amplitudes(t)).max() <= 1e-13
+            assert np.abs(a.tables[t][0][1] - b.tables[t][0][1]).max() <= 1e-14
+    finally:
+        a.close()
+        b.close()
