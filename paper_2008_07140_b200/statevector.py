@@ -303,17 +303,30 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
              max_qubits: int = DEFAULT_MAX_QUBITS, initial_index: int = 0,
              initial_state=None, fuse: bool = True, tile_qubits: int = 0, reg_qubits: int = 0,
              low_qubits: int = 0, jit: int = 0, device: int = 0, stream=None,
-             state: StateVector | None = None, profile: bool = False) -> RunResult:
+             state: StateVector | None = None, profile: bool = False,
+             noise_engine: str = "fused") -> RunResult:
     """Run a program on the B200 full-amplitude backend (statevector.py:397-430).
 
     Extra keywords over the reference: `initial_state` (host amplitudes to
     start from), `fuse`/`tile_qubits`/`reg_qubits`/`low_qubits` (scheduler
     knobs), `device`/`stream`, `state` (reuse an existing device state) and
-    `profile` (per-launch CUDA-event timing into `RunResult.stats`) and `jit`
-    (0: specialised per-pass kernels from n >= 16, 1: always, -1: never).
+    `profile` (per-launch CUDA-event timing into `RunResult.stats`), `jit`
+    (0: specialised per-pass kernels from n >= 16, 1: always, -1: never) and
+    `noise_engine` ("fused": a noisy run is a batch of one in `noisy_batch`, one
+    pass per noisy gate; "sequential": branch weights via `qsv_reduced_density`,
+    then the gate, per noisy gate).
     `workers`, `pool` and `chunk_log2` are accepted and ignored.
     """
     n = program.qubit_count
+    if (noise is not None and noise_engine == "fused" and rng is not None and state is None
+            and initial_state is None and initial_index == 0 and stream is None):
+        # one trajectory = a batch of one: each noisy gate is ONE pass that applies U.K_c and
+        # reduces the next noisy gate's branch weights (noisy_batch.py), instead of a weight
+        # pass + an apply pass per noisy gate; the same draws from `rng`
+        from .noisy_batch import run_noisy_batch
+
+        nb = run_noisy_batch(program, noise, [rng], device=device, max_qubits=max_qubits, fuse=fuse, groups=1)
+        return RunResult(cregs=nb.cregs[0], tables=nb.tables[0], state=nb.states[0], stats=nb.stats)
     if state is None:
         state = init_state(n, chunk_log2=chunk_log2, max_qubits=max_qubits, device=device, stream=stream)
     elif state.qubit_count != n:

@@ -79,11 +79,13 @@ def test_qft_random_state_golden(golden, golden_arrays, n):
         assert_parity(res.state.amplitudes, golden_arrays[f"qft{n}/{tag}"])
 
 
-def test_reference_noise_semantics(golden, golden_arrays):
-    """run_full with a depolarising NoiseModel reproduces the reference trajectory."""
+@pytest.mark.parametrize("engine", ["fused", "sequential"])
+def test_reference_noise_semantics(golden, golden_arrays, engine):
+    """run_full with a depolarising NoiseModel reproduces the reference trajectory
+    (fused: batch-of-one noisy steps; sequential: weights pass + gate per noisy gate)."""
     for rec in golden["noise"]:
         res = SV.run_full(parse_program(rec["text"]), np.random.default_rng(rec["traj_seed"]),
-                          make_noise_model("depolarizing", rec["p"]))
+                          make_noise_model("depolarizing", rec["p"]), noise_engine=engine)
         assert_parity(res.state.amplitudes, golden_arrays[rec["key"]])
 
 

@@ -102,7 +102,8 @@ def test_batched_matches_sequential_run_full():
     res = run_noisy_batch(prog, model, [np.random.default_rng(50 + t) for t in range(B)])
     try:
         for t in range(B):
-            ref = run_full(prog, np.random.default_rng(50 + t), model).state.amplitudes
+            ref = run_full(prog, np.random.default_rng(50 + t), model,
+                           noise_engine="sequential").state.amplitudes
             assert np.abs(res.amplitudes(t) - ref).max() <= 1e-10
     finally:
         res.close()
