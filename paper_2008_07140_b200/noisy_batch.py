@@ -82,7 +82,9 @@ def _step_info(inst, noise):
     if kraus is None:
         return None
     K = np.asarray(kraus)
-    return "noisy", gates.embed_controls(base, len(controls)), qubits, (K, np.einsum("kji,kjl->kil", K.conj(), K))
+    unitary = inst.name not in ("P0", "P1")
+    return "noisy", gates.embed_controls(base, len(controls)), qubits, (K, np.einsum("kji,kjl->kil", K.conj(), K),
+                                                                         unitary)
 
 
 class _Group:
@@ -224,7 +226,7 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
                     res.cregs[gr.lo + t][inst.creg] = outcome
                     gr.mats[t, 3 * outcome] = 1.0 / math.sqrt(p0 if outcome == 0 else p1)
             else:
-                K, KdK = kraus
+                K, KdK, unitary = kraus
                 # ||K_i psi_t||^2 = tr(K_i^dag K_i rho_t) for all trajectories and branches at once
                 probs = np.einsum("klj,bjl->bk", KdK, rhos).real
                 total = probs.sum(axis=1)
@@ -237,7 +239,10 @@ def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubit
                 pc = probs[np.arange(Bg), choice]
                 m = np.einsum("ij,bjk->bik", u, K[choice])
                 # the reference renormalises by the post-apply norm when it left 1
-                # (noise.py:219-221); for a normalised state that norm is probs[choice]
+                # (noise.py:219-221); for a normalised state and a unitary gate that norm is
+                # probs[choice]; for a noisy projector it is tr(M^dag M rho)
+                if not unitary:
+                    pc = np.einsum("bji,bjk,bki->b", m.conj(), m, rhos).real
                 renorm = np.abs(pc - 1.0) > 1e-12
                 m[renorm] /= np.sqrt(pc[renorm])[:, None, None]
                 gr.mats[:, : D * D] = m.reshape(Bg, -1)

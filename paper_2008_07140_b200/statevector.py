@@ -260,8 +260,11 @@ def _noisy(state, inst, noise, rng) -> bool:
             choice = i
             break
     noisy = gates.embed_controls(base, len(controls)) @ kraus[choice]
-    if abs(probs[choice] - 1.0) > 1e-12:
-        noisy = noisy / math.sqrt(probs[choice])
+    # post-apply norm (noise.py:219-221): probs[choice] for a unitary gate, tr(M^dag M rho)
+    # for a noisy projector
+    nsq = probs[choice] if inst.name not in ("P0", "P1") else float(np.real(np.trace(noisy.conj().T @ noisy @ rho)))
+    if abs(nsq - 1.0) > 1e-12:
+        noisy = noisy / math.sqrt(nsq)
     _apply_gate(state, noisy, qubits)
     return True
 

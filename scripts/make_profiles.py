@@ -56,10 +56,33 @@ n = bench["config"]["n_qubits"]
     "algorithmic_bytes_per_launch": 32 * 2 ** n, "round": int(sys.argv[1][1:])}, indent=1) + "\n")
 (out / "bench.json").write_text(json.dumps(bench, indent=1) + "\n")
 # the other configs' bench lines (scripts/round_measure.sh)
-for name in ("bench_qft", "bench_traj", "bench_traj_dedup", "bench_n32"):
+for name in ("bench_qft", "bench_traj", "bench_traj_dedup", "bench_n32", "bench_partial", "bench_noisy"):
     f = src / f"{name}.json"
     if f.exists() and f.read_text().strip():
         (out / f"{name}.json").write_text(json.dumps(json.loads(f.read_text().strip().splitlines()[-1]), indent=1) + "\n")
+# batched noisy-trajectory kernel: launch list + one full capture
+if (src / "noisy_launches.csv").exists():
+    shutil.copy(src / "noisy_launches.csv", out / "noisy_launches.csv")
+    agg = collections.defaultdict(list)
+    nrows = [r for r in csv.reader(open(src / "noisy_launches.csv")) if len(r) > 10]
+    nh = {k: i for i, k in enumerate(nrows[0])}
+    for r in nrows[1:]:
+        agg[(r[nh["Kernel Name"]].split("(")[0], r[nh["Metric Name"]])].append(float(r[nh["Metric Value"]].replace(",", "")))
+    nl = ["ncu launch list: python bench.py --workload noisy --steps 1 --warmup 1 --no-cpu-baseline --trajectories 256",
+          "(first 60 noisy_batch* launches, --clock-control none; 2 groups of 128 trajectories x 2^20 amplitudes:",
+          " algorithmic bytes per apply+reduce launch = 2 x 16 x 2^27 = 4.29 GB)", "",
+          "kernel | launches | avg us | avg dram read+write GB | GB/s"]
+    for k in sorted({k for k, _ in agg}):
+        t = agg[(k, "gpu__time_duration.sum")]; rr = agg[(k, "dram__bytes_read.sum")]; ww = agg[(k, "dram__bytes_write.sum")]
+        T = sum(t) / len(t); Bb = sum(rr) / len(rr) + sum(ww) / len(ww)
+        nl.append(f"{k} | {len(t)} | {T / 1e3:.1f} | {Bb / 1e9:.3f} | {Bb / T:.0f}")
+    (out / "noisy_launches_summary.txt").write_text("\n".join(nl) + "\n")
+if (src / "prof_noisy.ncu-rep").exists():
+    summ = subprocess.run([sys.executable, str(ROOT / "scripts/ncu_summary.py"), str(src / "prof_noisy.ncu-rep")],
+                          capture_output=True, text=True).stdout
+    (out / "ncu_full_noisy_batch.txt").write_text(
+        "ncu --set full --clock-control none -k regex:noisy_batch_kernel -s 30 -c 1 "
+        "python bench.py --workload noisy --steps 1 --warmup 1 --no-cpu-baseline --trajectories 256\n\n" + summ)
 if (src / "exchange_pass.log").exists():
     shutil.copy(src / "exchange_pass.log", out / "exchange_pass.log")
 print("wrote", out)

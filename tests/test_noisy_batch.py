@@ -144,3 +144,18 @@ def test_one_and_two_groups_agree():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["fused", "sequential"])
+def test_noisy_projectors_renormalise_like_reference(engine):
+    """A noisy P0/P1 is renormalised by its post-apply norm (noise.py:219-221)."""
+    from oracle import oracle as O
+    from paper_2008_07140_b200.statevector import run_full
+
+    prog = parse_program('QINIT 3\nH 0\nRY 1,"0.7"\nCNOT 0,2\nP1 0\nH 1\nP0 1\nRX 2,"0.3"\n')
+    for s in range(6):
+        res = run_full(prog, np.random.default_rng(s), make_noise_model("bitflip", 0.8), noise_engine=engine)
+        ref = O.run_full(prog, np.random.default_rng(s), ("bitflip", 0.8))
+        assert np.abs(res.state.amplitudes - ref.state.amplitudes).max() <= 1e-12
+        res.state.close()
