@@ -153,7 +153,11 @@ def test_noisy_projectors_renormalise_like_reference(engine):
     from oracle import oracle as O
     from paper_2008_07140_b200.statevector import run_full
 
-    prog = parse_program('QINIT 3\nH 0\nRY 1,"0.7"\nCNOT 0,2\nP1 0\nH 1\nP0 1\nRX 2,"0.3"\n')
+    from paper_2008_07140_b200.program import Instruction, Program
+
+    # projectors are not user mnemonics (program.py:407); partial mode builds them as Instructions
+    base = parse_program('QINIT 3\nH 0\nRY 1,"0.7"\nCNOT 0,2\nH 1\nRX 2,"0.3"\n').instructions
+    prog = Program(3, 0, base[:3] + (Instruction("P1", (0,)),) + base[3:4] + (Instruction("P0", (1,)),) + base[4:])
     for s in range(6):
         res = run_full(prog, np.random.default_rng(s), make_noise_model("bitflip", 0.8), noise_engine=engine)
         ref = O.run_full(prog, np.random.default_rng(s), ("bitflip", 0.8))
