@@ -731,43 +731,67 @@ struct NoisyArgs {
 // keeps the compiler from hoisting all 16 entries into registers, which would cap occupancy
 __device__ __forceinline__ double2 vld(const volatile double2 *m, int k) { return make_double2(m[k].x, m[k].y); }
 
-template <int NU>
-__device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const volatile double2 *m, int p0) {
+template <int NU, int P>
+__device__ __forceinline__ void noisy_mat1_at(double2 (&x)[1 << NU], const volatile double2 *m) {
 #pragma unroll
-    for (int p = 0; p < NU; ++p) {
-        if (p != p0) continue;  // uniform branch: every index below is compile-time
+    for (int l = 0; l < (1 << NU); ++l) {
+        if ((l >> P) & 1) continue;
+        const double2 x0 = x[l], x1 = x[l | (1 << P)];
+        x[l] = cdot2(vld(m, 0), x0, vld(m, 1), x1);
+        x[l | (1 << P)] = cdot2(vld(m, 2), x0, vld(m, 3), x1);
+    }
+}
+
+template <int NU, int PA, int PB>
+__device__ __forceinline__ void noisy_mat2_at(double2 (&x)[1 << NU], const volatile double2 *m) {
+    if constexpr (PA != PB && PA < NU && PB < NU) {
 #pragma unroll
         for (int l = 0; l < (1 << NU); ++l) {
-            if ((l >> p) & 1) continue;
-            const double2 x0 = x[l], x1 = x[l | (1 << p)];
-            x[l] = cdot2(vld(m, 0), x0, vld(m, 1), x1);
-            x[l | (1 << p)] = cdot2(vld(m, 2), x0, vld(m, 3), x1);
+            if (((l >> PA) & 1) || ((l >> PB) & 1)) continue;
+            const int idx[4] = {l, l | (1 << PB), l | (1 << PA), l | (1 << PA) | (1 << PB)};
+            double2 y[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) y[c] = x[idx[c]];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const double2 p = cdot2(vld(m, 4 * r), y[0], vld(m, 4 * r + 1), y[1]);
+                const double2 q = cdot2(vld(m, 4 * r + 2), y[2], vld(m, 4 * r + 3), y[3]);
+                x[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
+            }
         }
+    }
+}
+
+// positions are runtime values but uniform per launch: a switch to compile-time
+// instantiations keeps every register index static and lets the compiler allocate
+// registers per case (max over cases, not the sum of predicated variants)
+template <int NU>
+__device__ __forceinline__ void noisy_mat1(double2 (&x)[1 << NU], const volatile double2 *m, int p0) {
+    switch (p0) {
+        case 0: noisy_mat1_at<NU, 0>(x, m); break;
+        case 1: if constexpr (NU > 1) noisy_mat1_at<NU, 1>(x, m); break;
+        case 2: if constexpr (NU > 2) noisy_mat1_at<NU, 2>(x, m); break;
+        default: if constexpr (NU > 3) noisy_mat1_at<NU, 3>(x, m); break;
     }
 }
 
 template <int NU>
 __device__ __forceinline__ void noisy_mat2(double2 (&x)[1 << NU], const volatile double2 *m, int p0, int p1) {
-#pragma unroll
-    for (int pa = 0; pa < NU; ++pa)
-#pragma unroll
-        for (int pb = 0; pb < NU; ++pb) {
-            if (pa == pb || pa != p0 || pb != p1) continue;
-#pragma unroll
-            for (int l = 0; l < (1 << NU); ++l) {
-                if (((l >> pa) & 1) || ((l >> pb) & 1)) continue;
-                const int idx[4] = {l, l | (1 << pb), l | (1 << pa), l | (1 << pa) | (1 << pb)};
-                double2 y[4];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) y[c] = x[idx[c]];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const double2 p = cdot2(vld(m, 4 * r), y[0], vld(m, 4 * r + 1), y[1]);
-                    const double2 q = cdot2(vld(m, 4 * r + 2), y[2], vld(m, 4 * r + 3), y[3]);
-                    x[idx[r]] = make_double2(p.x + q.x, p.y + q.y);
-                }
-            }
-        }
+    switch (p0 * 4 + p1) {
+        case 1: noisy_mat2_at<NU, 0, 1>(x, m); break;
+        case 2: noisy_mat2_at<NU, 0, 2>(x, m); break;
+        case 3: noisy_mat2_at<NU, 0, 3>(x, m); break;
+        case 4: noisy_mat2_at<NU, 1, 0>(x, m); break;
+        case 6: noisy_mat2_at<NU, 1, 2>(x, m); break;
+        case 7: noisy_mat2_at<NU, 1, 3>(x, m); break;
+        case 8: noisy_mat2_at<NU, 2, 0>(x, m); break;
+        case 9: noisy_mat2_at<NU, 2, 1>(x, m); break;
+        case 11: noisy_mat2_at<NU, 2, 3>(x, m); break;
+        case 12: noisy_mat2_at<NU, 3, 0>(x, m); break;
+        case 13: noisy_mat2_at<NU, 3, 1>(x, m); break;
+        case 14: noisy_mat2_at<NU, 3, 2>(x, m); break;
+        default: break;
+    }
 }
 
 // rho is Hermitian: acc packs row r's diagonal (real) then its upper entries (re, im), D^2 doubles
@@ -805,16 +829,32 @@ __device__ __forceinline__ void noisy_rdm_at(const double2 (&x)[1 << NU], double
 template <int NU, int NK>
 __device__ __forceinline__ void noisy_rdm(const double2 (&x)[1 << NU], double (&acc)[1 << (2 * NK)], int p0,
                                           int p1) {
-#pragma unroll
-    for (int pa = 0; pa < NU; ++pa) {
-        if (pa != p0) continue;
-        if (NK == 1) {
-            noisy_rdm_at<NU, 2>(x, acc, pa, 0);
-            continue;
+    if constexpr (NK == 1) {
+        switch (p0) {
+            case 0: noisy_rdm_at<NU, 2>(x, acc, 0, 0); break;
+            case 1: if constexpr (NU > 1) noisy_rdm_at<NU, 2>(x, acc, 1, 0); break;
+            case 2: if constexpr (NU > 2) noisy_rdm_at<NU, 2>(x, acc, 2, 0); break;
+            default: if constexpr (NU > 3) noisy_rdm_at<NU, 2>(x, acc, 3, 0); break;
         }
-#pragma unroll
-        for (int pb = 0; pb < NU; ++pb)
-            if (pb != pa && pb == p1) noisy_rdm_at<NU, 4>(x, acc, pa, pb);
+    } else if constexpr (NK == 2) {
+#define QSV_RDM2(A_, B_) \
+    if constexpr (A_ < NU && B_ < NU) noisy_rdm_at<NU, 4>(x, acc, A_, B_);
+        switch (p0 * 4 + p1) {
+            case 1: QSV_RDM2(0, 1) break;
+            case 2: QSV_RDM2(0, 2) break;
+            case 3: QSV_RDM2(0, 3) break;
+            case 4: QSV_RDM2(1, 0) break;
+            case 6: QSV_RDM2(1, 2) break;
+            case 7: QSV_RDM2(1, 3) break;
+            case 8: QSV_RDM2(2, 0) break;
+            case 9: QSV_RDM2(2, 1) break;
+            case 11: QSV_RDM2(2, 3) break;
+            case 12: QSV_RDM2(3, 0) break;
+            case 13: QSV_RDM2(3, 1) break;
+            case 14: QSV_RDM2(3, 2) break;
+            default: break;
+        }
+#undef QSV_RDM2
     }
 }
 
