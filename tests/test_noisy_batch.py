@@ -163,3 +163,48 @@ def test_noisy_projectors_renormalise_like_reference(engine):
         ref = O.run_full(prog, np.random.default_rng(s), ("bitflip", 0.8))
         assert np.abs(res.state.amplitudes - ref.state.amplitudes).max() <= 1e-12
         res.state.close()
+
+
+@pytest.fixture
+def fake_native(monkeypatch):
+    from fake_qsv import FakeLib
+
+    fake = FakeLib()
+    monkeypatch.setattr(N, "lib", lambda: fake)
+    return fake
+
+
+@pytest.mark.parametrize("groups", [1, 2])
+@pytest.mark.parametrize("kind,p", [("ampdamp", 0.2), ("depolarizing", 0.1), ("phasedamp", 0.3)])
+def test_host_logic_against_oracle_on_cpu(fake_native, groups, kind, p):
+    """The batched host logic (draw order, weights from the upper-triangle reduced
+    densities, branch choice, renormalisation, MEASURE/PMEASURE bookkeeping,
+    grouping) over a numpy stand-in of the native steps, against the oracle's
+    restatement of the reference sampling, trajectory by trajectory."""
+    from oracle import oracle as O
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = parse_program(generate_rqc(RqcConfig(2, 3, depth=5, seed=4)) + "PMEASURE 0,4\n")
+    B = 8
+    res = run_noisy_batch(prog, make_noise_model(kind, p), [np.random.default_rng(300 + t) for t in range(B)],
+                          groups=groups)
+    for t in range(B):
+        ref = O.run_full(prog, np.random.default_rng(300 + t), (kind, p))
+        assert np.abs(res.amplitudes(t) - ref.state.amplitudes).max() <= 1e-12
+        assert np.abs(res.tables[t][0][1] - ref.tables[0][1]).max() <= 1e-12
+    assert len({tuple(c) for c in res.choices}) > 1  # trajectories took different branches
+
+
+def test_host_measure_logic_on_cpu(fake_native):
+    from oracle import oracle as O
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = parse_program("QINIT 4\nCREG 2\nH 0\nH 1\nCNOT 1,2\nMEASURE 2,$1\nRY 3,\"1.1\"\nMEASURE 3,$0\n")
+    res = run_noisy_batch(prog, None, [np.random.default_rng(t) for t in range(16)])
+    seen = set()
+    for t in range(16):
+        ref = O.run_full(prog, np.random.default_rng(t))
+        assert res.cregs[t] == ref.cregs
+        assert np.abs(res.amplitudes(t) - ref.state.amplitudes).max() <= 1e-12
+        seen.add(tuple(ref.cregs))
+    assert len(seen) > 2
