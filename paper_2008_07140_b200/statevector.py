@@ -315,12 +315,21 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
     knobs), `device`/`stream`, `state` (reuse an existing device state) and
     `profile` (per-launch CUDA-event timing into `RunResult.stats`), `jit`
     (0: specialised per-pass kernels from n >= 16, 1: always, -1: never) and
-    `noise_engine` ("fused": a noisy run is a batch of one in `noisy_batch`, one
-    pass per noisy gate; "sequential": branch weights via `qsv_reduced_density`,
-    then the gate, per noisy gate).
+    `noise_engine` ("fused": mixed-unitary channels (flips, depolarising) draw their
+    branches up front and the run stays fused; other channels run as a batch of one in
+    `noisy_batch`, one pass per noisy gate; "sequential": branch weights via
+    `qsv_reduced_density`, then the gate, per noisy gate).
     `workers`, `pool` and `chunk_log2` are accepted and ignored.
     """
     n = program.qubit_count
+    if noise is not None and noise_engine == "fused" and rng is not None and _mixed_unitary(program, noise):
+        # every matching channel is a mixture of scaled unitaries: its branch weights do not
+        # depend on the state, so the branches are drawn up front and the run stays fused
+        return _run_presampled(program, rng, noise, state=state, device=device, stream=stream,
+                               max_qubits=max_qubits, chunk_log2=chunk_log2, initial_index=initial_index,
+                               initial_state=initial_state,
+                               opts=N.options(fuse=fuse, tile_qubits=tile_qubits, reg_qubits=reg_qubits,
+                                              low_qubits=low_qubits, profile=profile, jit=jit))
     if (noise is not None and noise_engine == "fused" and rng is not None and state is None
             and initial_state is None and initial_index == 0 and stream is None):
         # one trajectory = a batch of one: each noisy gate is ONE pass that applies U.K_c and
@@ -349,6 +358,106 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
         _flush(state, batch, opts, result.stats)
         apply_instruction(state, inst, None, rng, noise, result)
     _flush(state, batch, opts, result.stats)
+    return result
+
+
+def _noisy_kraus(inst, noise):
+    """(dense base with controls embedded, qubits, kraus) of a noisy gate, else None
+    (the reference's _noisy_dispatch conditions, statevector.py:343-357)."""
+    if not inst.is_gate:
+        return None
+    base, targets, controls = gates.controlled_form(inst)
+    qubits = tuple(controls) + tuple(targets)
+    if len(qubits) > 2:
+        return None
+    kraus = noise.kraus_for(inst, len(qubits))
+    if kraus is None:
+        return None
+    return gates.embed_controls(base, len(controls)), qubits, kraus
+
+
+def _mixed_unitary(program, noise) -> bool:
+    """True when every noisy gate's Kraus operators are scaled unitaries
+    (K^dag K = w I: bit/phase/bit-phase flips, depolarising) on a unitary gate, so
+    ||K_i psi||^2 = w_i for every normalised state."""
+    for inst in program.instructions:
+        if inst.is_gate and inst.name in ("P0", "P1") and noise.kraus_for(inst, 1) is not None:
+            return False
+        nk = _noisy_kraus(inst, noise)
+        if nk is None:
+            continue
+        for k in nk[2]:
+            kk = k.conj().T @ k
+            if np.abs(kk - kk[0, 0] * np.eye(k.shape[0])).max() > 1e-14:
+                return False
+    return True
+
+
+class _Replay:
+    """Hands out pre-drawn uniforms in order (stands in for `rng.random()`)."""
+
+    def __init__(self, values):
+        self.values, self.i = values, 0
+
+    def random(self):
+        v = self.values[self.i]
+        self.i += 1
+        return float(v)
+
+
+def _run_presampled(program, rng, noise, *, state, device, stream, max_qubits, chunk_log2, initial_index,
+                    initial_state, opts) -> RunResult:
+    """run_full for mixed-unitary noise (the reference trajectory, noise.py:188-222): one
+    uniform per noisy gate and per MEASURE, in program order, drawn up front (the same
+    stream); noisy gate j becomes the dense gate U.K_c / sqrt(w_c) (the reference's
+    renormalised result, K_c = sqrt(w_c) x unitary), and the whole program runs through
+    the fused scheduler between MEASUREs — as many HBM passes as the noiseless run."""
+    n = program.qubit_count
+    infos = [_noisy_kraus(i, noise) for i in program.instructions]
+    n_draws = sum(1 for i, x in zip(program.instructions, infos) if x is not None or i.name == "MEASURE")
+    replay = _Replay(rng.random(n_draws) if n_draws else [])
+    if state is None:
+        state = init_state(n, chunk_log2=chunk_log2, max_qubits=max_qubits, device=device, stream=stream)
+    elif state.qubit_count != n:
+        raise ValueError("state has a different qubit count")
+    if initial_state is not None:
+        state.amplitudes = initial_state
+    else:
+        state.set_basis(initial_index)
+    result = RunResult(cregs=[0] * program.creg_count, state=state)
+    pending: list = []
+
+    def flush():
+        if pending:
+            rec = N.gate_records(pending)
+            st = N.qsv_run_stats()
+            N.check(N.lib().qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(st)))
+            for k, v in st.as_dict().items():
+                result.stats[k] = result.stats.get(k, 0) + v
+            pending.clear()
+
+    for inst, nk in zip(program.instructions, infos):
+        if nk is not None:
+            u, qubits, kraus = nk
+            w = [float(np.real(np.trace(k.conj().T @ k))) / k.shape[0] for k in kraus]
+            r = replay.random() * sum(w)
+            acc, choice = 0.0, len(w) - 1
+            for i, wi in enumerate(w):
+                acc += wi
+                if r < acc:
+                    choice = i
+                    break
+            m = u @ kraus[choice]
+            if abs(w[choice] - 1.0) > 1e-12:
+                m = m / math.sqrt(w[choice])
+            pending.append((m, qubits, ()))
+        elif inst.is_gate:
+            pending.append(_gate_triplet(inst))
+        else:
+            flush()
+            apply_instruction(state, inst, None, replay, None, result)
+    flush()
+    result.stats["noise_engine"] = "presampled"
     return result
 
 

@@ -27,6 +27,7 @@ class FakeLib:
         self.states = {}
         self._ids = itertools.count(1)
         self.staged = {}
+        self.run_calls = 0
 
     def qsv_create(self, n, device, stream, out):
         h = next(self._ids)
@@ -59,6 +60,7 @@ class FakeLib:
         return 0
 
     def qsv_run(self, h, rec_ptr, n_rec, opts, stats):
+        self.run_calls += 1
         psi = self._psi(h)
         n = psi.size.bit_length() - 1
         for r in _arr(rec_ptr, N.GATE_DTYPE, n_rec):
@@ -69,6 +71,8 @@ class FakeLib:
 
     def qsv_pmeasure(self, h, qubits, m, table_ptr):
         psi = self._psi(h)
+        if isinstance(qubits, int):  # a raw pointer (statevector.pmeasure) or a ctypes array
+            qubits = _arr(qubits, np.int32, m)
         idx = np.arange(psi.size)
         key = np.zeros(psi.size, dtype=np.int64)
         for pos in range(m):
@@ -101,6 +105,23 @@ class FakeLib:
         out = self.staged.get(h.value if hasattr(h, "value") else h)
         if rdm_ptr and out is not None:
             _arr(rdm_ptr, np.complex128, out.size)[:] = out.reshape(-1)
+        return 0
+
+    def qsv_prob_bit0(self, h, k, out):
+        psi = self._psi(h)
+        idx = np.arange(psi.size)
+        out._obj.value = float(np.sum(np.abs(psi[((idx >> k) & 1) == 0]) ** 2))
+        return 0
+
+    def qsv_norm_sq(self, h, out):
+        out._obj.value = float(np.sum(np.abs(self._psi(h)) ** 2))
+        return 0
+
+    def qsv_collapse(self, h, k, outcome, scale):
+        psi = self._psi(h)
+        idx = np.arange(psi.size)
+        psi[((idx >> k) & 1) != outcome] = 0
+        psi *= scale
         return 0
 
     def qsv_last_error(self):

@@ -208,3 +208,34 @@ def test_host_measure_logic_on_cpu(fake_native):
         assert np.abs(res.amplitudes(t) - ref.state.amplitudes).max() <= 1e-12
         seen.add(tuple(ref.cregs))
     assert len(seen) > 2
+
+
+@pytest.mark.parametrize("kind,p", [("depolarizing", 0.2), ("bitflip", 0.7), ("phaseflip", 0.6),
+                                    ("bitphaseflip", 0.9)])
+def test_presampled_mixed_unitary_run_full_on_cpu(fake_native, kind, p):
+    """run_full under a mixed-unitary channel draws its branches up front and stays
+    fused: same draws (MEASURE interleaved) and amplitudes as the oracle's reference
+    sampling; one qsv_run per MEASURE-separated segment."""
+    from oracle import oracle as O
+    from paper_2008_07140_b200.statevector import run_full
+
+    text = generate_rqc(RqcConfig(2, 3, depth=5, seed=8)).replace("QINIT 6", "QINIT 6\nCREG 2")
+    prog = parse_program(text + "MEASURE 2,$0\nCNOT 2,3\nH 4\nMEASURE 4,$1\nCZ 0,5\nPMEASURE 1,3\n")
+    for s in range(6):
+        fake_native.run_calls = 0
+        res = run_full(prog, np.random.default_rng(s), make_noise_model(kind, p))
+        assert res.stats.get("noise_engine") == "presampled"
+        assert fake_native.run_calls == 3  # the segments between MEASURE, MEASURE and PMEASURE
+        ref = O.run_full(prog, np.random.default_rng(s), (kind, p))
+        assert res.cregs == ref.cregs
+        assert np.abs(res.state.amplitudes - ref.state.amplitudes).max() <= 1e-12
+        assert np.abs(res.tables[0][1] - ref.tables[0][1]).max() <= 1e-12
+
+
+def test_state_dependent_channels_are_not_presampled(fake_native):
+    from paper_2008_07140_b200.statevector import _mixed_unitary
+
+    prog = parse_program("QINIT 2\nH 0\nCNOT 0,1\n")
+    assert _mixed_unitary(prog, make_noise_model("depolarizing", 0.1))
+    assert not _mixed_unitary(prog, make_noise_model("ampdamp", 0.1))
+    assert not _mixed_unitary(prog, make_noise_model("phasedamp", 0.1))
