@@ -405,13 +405,47 @@ class _Replay:
         return float(v)
 
 
+_PAULIS = (gates.I2, gates.X, gates.Y, gates.Z)
+_PLAN_CACHE: dict = {}  # (records bytes, n, options) -> qsv_plan handle (clean segments with errors)
+
+
+def _pauli_kinds(v: np.ndarray):
+    """Kinds (0 I, 1 X, 2 Y, 3 Z) per qubit, MSB first, if v is a Pauli string, else None."""
+    if v.shape[0] == 2:
+        for k, P in enumerate(_PAULIS):
+            if np.abs(v - P).max() < 1e-12:
+                return (k,)
+        return None
+    for a, Pa in enumerate(_PAULIS):
+        for b, Pb in enumerate(_PAULIS):
+            if np.abs(v - np.kron(Pa, Pb)).max() < 1e-12:
+                return (a, b)
+    return None
+
+
+def _cached_plan(rec: np.ndarray, n: int, opts):
+    key = (rec.tobytes(), n, opts.fuse, opts.tile_qubits, opts.reg_qubits, opts.low_qubits, opts.jit)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        plan = C.c_void_p()
+        N.check(N.lib().qsv_plan_create(rec.ctypes.data, len(rec), n, C.byref(opts), C.byref(plan)))
+        if len(_PLAN_CACHE) >= 8:
+            old = next(iter(_PLAN_CACHE))
+            N.lib().qsv_plan_destroy(_PLAN_CACHE.pop(old))
+        _PLAN_CACHE[key] = plan
+    return plan
+
+
 def _run_presampled(program, rng, noise, *, state, device, stream, max_qubits, chunk_log2, initial_index,
                     initial_state, opts) -> RunResult:
     """run_full for mixed-unitary noise (the reference trajectory, noise.py:188-222): one
     uniform per noisy gate and per MEASURE, in program order, drawn up front (the same
-    stream); noisy gate j becomes the dense gate U.K_c / sqrt(w_c) (the reference's
-    renormalised result, K_c = sqrt(w_c) x unitary), and the whole program runs through
-    the fused scheduler between MEASUREs — as many HBM passes as the noiseless run."""
+    stream); noisy gate j's branch is picked with the reference's cumulative rule.  K_c /
+    sqrt(w_c) is a Pauli string for the flip and depolarising channels, so the reference's
+    renormalised U.K_c/sqrt(w_c) is "Pauli error(s) before U": each MEASURE-separated
+    segment runs the CLEAN gates' fused plan with the errors handed to
+    `qsv_plan_execute_paulis` (no new kernels to compile; error-free runs are the
+    noiseless run).  A branch that is not a Pauli string falls back to the dense gate."""
     n = program.qubit_count
     infos = [_noisy_kraus(i, noise) for i in program.instructions]
     n_draws = sum(1 for i, x in zip(program.instructions, infos) if x is not None or i.name == "MEASURE")
@@ -425,16 +459,45 @@ def _run_presampled(program, rng, noise, *, state, device, stream, max_qubits, c
     else:
         state.set_basis(initial_index)
     result = RunResult(cregs=[0] * program.creg_count, state=state)
-    pending: list = []
+    L = N.lib()
+    seg: list = []      # clean gate triplets of the current segment
+    errs: list = []     # (gate index in seg, qubit, kind)
+    dense = [False]     # a non-Pauli branch forces a plain run with explicit gates
+
+    def account(st):
+        for k, v in st.as_dict().items():
+            result.stats[k] = result.stats.get(k, 0) + v
 
     def flush():
-        if pending:
-            rec = N.gate_records(pending)
-            st = N.qsv_run_stats()
-            N.check(N.lib().qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(st)))
-            for k, v in st.as_dict().items():
-                result.stats[k] = result.stats.get(k, 0) + v
-            pending.clear()
+        if not seg:
+            return
+        rec = N.gate_records(seg)
+        st = N.qsv_run_stats()
+        rc = None  # None: no Pauli-plan attempt (no errors, or a dense branch in the segment)
+        if errs and not dense[0]:
+            pa = np.zeros(len(errs), dtype=N.PAULI_DTYPE)
+            for k, e in enumerate(errs):
+                pa[k] = e
+            rc = L.qsv_plan_execute_paulis(state.handle, _cached_plan(rec, n, opts), pa.ctypes.data, len(errs),
+                                           C.byref(opts), C.byref(st))
+            if rc not in (0, N.QSV_E_UNSUPPORTED):
+                N.check(rc)
+        if rc != 0:
+            if errs:  # the plan cannot take Pauli errors (or a dense branch is present): explicit gates
+                items = []
+                by_gate: dict = {}
+                for g, q, kind in errs:
+                    by_gate.setdefault(g, []).append((q, kind))
+                for g, t in enumerate(seg):
+                    for q, kind in by_gate.get(g, ()):
+                        items.append((_PAULIS[kind], (q,), ()))
+                    items.append(t)
+                rec = N.gate_records(items)
+            N.check(L.qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(st)))
+        account(st)
+        seg.clear()
+        errs.clear()
+        dense[0] = False
 
     for inst, nk in zip(program.instructions, infos):
         if nk is not None:
@@ -447,12 +510,20 @@ def _run_presampled(program, rng, noise, *, state, device, stream, max_qubits, c
                 if r < acc:
                     choice = i
                     break
-            m = u @ kraus[choice]
-            if abs(w[choice] - 1.0) > 1e-12:
-                m = m / math.sqrt(w[choice])
-            pending.append((m, qubits, ()))
+            kinds = _pauli_kinds(kraus[choice] / math.sqrt(w[choice]))
+            if kinds is None:
+                m = u @ kraus[choice]
+                if abs(w[choice] - 1.0) > 1e-12:
+                    m = m / math.sqrt(w[choice])
+                seg.append((m, qubits, ()))
+                dense[0] = True
+                continue
+            for q, kind in zip(qubits, kinds):
+                if kind:
+                    errs.append((len(seg), q, kind))
+            seg.append(_gate_triplet(inst))
         elif inst.is_gate:
-            pending.append(_gate_triplet(inst))
+            seg.append(_gate_triplet(inst))
         else:
             flush()
             apply_instruction(state, inst, None, replay, None, result)

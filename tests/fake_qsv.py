@@ -124,5 +124,15 @@ class FakeLib:
         psi *= scale
         return 0
 
+    def qsv_plan_create(self, rec_ptr, n_rec, n, opts, out):
+        out._obj.value = next(self._ids)
+        return 0
+
+    def qsv_plan_destroy(self, plan):
+        return 0
+
+    def qsv_plan_execute_paulis(self, h, plan, paulis, n_paulis, opts, stats):
+        return N.QSV_E_UNSUPPORTED  # the host then inserts the Paulis as explicit gates
+
     def qsv_last_error(self):
         return b""

@@ -169,8 +169,11 @@ def test_noisy_projectors_renormalise_like_reference(engine):
 def fake_native(monkeypatch):
     from fake_qsv import FakeLib
 
+    from paper_2008_07140_b200 import statevector as SV
+
     fake = FakeLib()
     monkeypatch.setattr(N, "lib", lambda: fake)
+    monkeypatch.setattr(SV, "_PLAN_CACHE", {})  # fake plan handles never reach the real library
     return fake
 
 
