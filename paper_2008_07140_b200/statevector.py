@@ -473,8 +473,8 @@ def _run_presampled(program, rng, noise, *, state, device, stream, max_qubits, c
             return
         rec = N.gate_records(seg)
         st = N.qsv_run_stats()
-        rc = None  # None: no Pauli-plan attempt (no errors, or a dense branch in the segment)
-        if errs and not dense[0]:
+        rc = None  # None: no Pauli-plan attempt (a dense branch in the segment)
+        if not dense[0]:  # error-free segments use the same cached plan (and its compiled kernels)
             pa = np.zeros(len(errs), dtype=N.PAULI_DTYPE)
             for k, e in enumerate(errs):
                 pa[k] = e
