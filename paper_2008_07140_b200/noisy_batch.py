@@ -56,6 +56,8 @@ class NoisyBatchResult:
     group_log2: int = 0  # trajectories per group = 2^group_log2
 
     def amplitudes(self, t: int) -> np.ndarray:
+        if not self.states:
+            raise ValueError("no device states kept (chunked or closed batch)")
         out = np.empty(1 << self.qubit_count, dtype=np.complex128)
         g, k = divmod(t, 1 << self.group_log2)
         return self.states[g].download(out, k << self.qubit_count)
@@ -112,20 +114,49 @@ class _Group:
             self.inflight = False
 
 
+DEFAULT_MAX_BATCH_BYTES = 96 << 30  # device memory one batch of trajectory states may take
+
+
 def run_noisy_batch(program: Program, noise, rngs, *, device: int = 0, max_qubits: int = 30,
-                    fuse: bool = True, groups: int = 2) -> NoisyBatchResult:
+                    fuse: bool = True, groups: int = 2,
+                    max_batch_bytes: int = DEFAULT_MAX_BATCH_BYTES) -> NoisyBatchResult:
     """Run len(rngs) = 2^b trajectories of `program` under `noise`.
+
+    When 2^b trajectory states exceed `max_batch_bytes` they run in consecutive
+    power-of-two chunks; the result then carries cregs, tables and choices for
+    every trajectory but no device states (each chunk's states are freed once its
+    tables are read), so `amplitudes(t)` is unavailable.
 
     rngs[t] plays the role of the `rng` argument of the reference `run_full` for
     trajectory t (e.g. `np.random.default_rng(seed_t)`); draws happen in program
     order, one per noisy gate and per MEASURE, as in the reference.  The batch is
     split into `groups` (1 or 2) batched states on their own streams: while one
     group's pass runs, the host samples the other group's branches."""
-    from .statevector import init_state
-
     B = len(rngs)
     if B < 1 or B & (B - 1):
         raise ValueError("the batch holds a power-of-two number of trajectories")
+    per = 16 << program.qubit_count
+    if B > 1 and B * per > max_batch_bytes:
+        chunk = 1 << max(0, (max(1, max_batch_bytes // per)).bit_length() - 1)
+        out = NoisyBatchResult(cregs=[], tables=[], choices=[], qubit_count=program.qubit_count)
+        out.stats = {"noisy_steps": 0, "trajectories": B, "chunks": B // chunk}
+        for c0 in range(0, B, chunk):
+            part = _run_noisy_batch(program, noise, rngs[c0:c0 + chunk], device=device, max_qubits=max_qubits,
+                                    fuse=fuse, groups=groups)
+            part.close()
+            out.cregs += part.cregs
+            out.tables += part.tables
+            out.choices += part.choices
+            out.stats["noisy_steps"] += part.stats["noisy_steps"]
+        return out
+    return _run_noisy_batch(program, noise, rngs, device=device, max_qubits=max_qubits, fuse=fuse, groups=groups)
+
+
+def _run_noisy_batch(program: Program, noise, rngs, *, device: int, max_qubits: int, fuse: bool,
+                     groups: int) -> NoisyBatchResult:
+    from .statevector import init_state
+
+    B = len(rngs)
     b = B.bit_length() - 1
     n = program.qubit_count
     if n > max_qubits:

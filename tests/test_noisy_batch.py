@@ -242,3 +242,22 @@ def test_state_dependent_channels_are_not_presampled(fake_native):
     assert _mixed_unitary(prog, make_noise_model("depolarizing", 0.1))
     assert not _mixed_unitary(prog, make_noise_model("ampdamp", 0.1))
     assert not _mixed_unitary(prog, make_noise_model("phasedamp", 0.1))
+
+
+def test_chunked_batches_match_one_batch_on_cpu(fake_native):
+    """Batches above max_batch_bytes run in power-of-two chunks with identical
+    per-trajectory draws, outcomes and tables."""
+    from paper_2008_07140_b200.noisy_batch import run_noisy_batch
+
+    prog = parse_program(generate_rqc(RqcConfig(2, 3, depth=4, seed=6)).replace("QINIT 6", "QINIT 6\nCREG 1")
+                         + "MEASURE 3,$0\nPMEASURE 0,2\n")
+    model = make_noise_model("ampdamp", 0.25)
+    whole = run_noisy_batch(prog, model, [np.random.default_rng(900 + t) for t in range(8)])
+    parts = run_noisy_batch(prog, model, [np.random.default_rng(900 + t) for t in range(8)],
+                            max_batch_bytes=2 * (16 << 6))
+    assert parts.stats["chunks"] == 4
+    assert parts.cregs == whole.cregs and parts.choices == whole.choices
+    for a, b in zip(parts.tables, whole.tables):
+        assert np.abs(a[0][1] - b[0][1]).max() <= 1e-14
+    with pytest.raises(ValueError):
+        parts.amplitudes(0)
