@@ -1627,6 +1627,7 @@ int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int3
                                const double *mats, int nk, const int32_t *next_qubits) {
     const int nsub = st->n - batch_log2;
     if (batch_log2 < 0 || nsub < 1 || batch_log2 > 16) return fail(QSV_E_PARSE, "bad batch size");
+    if (nsub > 31) return fail(QSV_E_UNSUPPORTED, "trajectories of at most 31 qubits per batch block");
     if (gk < 0 || gk > 2 || nk < 0 || nk > 2) return fail(QSV_E_UNSUPPORTED, "noisy step acts on 0..2 qubits");
     if (gk == 0 && nk == 0) return QSV_OK;
     NoisyArgs a{};

@@ -874,36 +874,34 @@ __global__ void __launch_bounds__(256, noisy_min_blocks<NU, NK>()) noisy_batch_k
     double acc[A];
 #pragma unroll
     for (int k = 0; k < A; ++k) acc[k] = 0.0;
-    const uint64_t groups = 1ull << (a.nsub - NU);
-    const uint64_t base = (uint64_t)b << a.nsub;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
-        uint64_t i = g;
+    // 32-bit offsets inside this trajectory's block (nsub <= 31): the 2^NU loop-invariant
+    // union masks then cost one register each instead of two
+    const uint32_t groups = 1u << (a.nsub - NU);
+    double2 *__restrict__ pb = psi + ((uint64_t)b << a.nsub);
+    uint32_t um[L];
 #pragma unroll
-        for (int p = 0; p < NU; ++p) i = insert_zero(i, a.uq[p]);
-        i |= base;
+    for (int l = 0; l < L; ++l) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int p = 0; p < NU; ++p)
+            if ((l >> p) & 1) o |= 1u << a.uq[p];
+        um[l] = o;
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        uint32_t i = g;
+#pragma unroll
+        for (int p = 0; p < NU; ++p) i = ((i >> a.uq[p]) << (a.uq[p] + 1)) | (i & ((1u << a.uq[p]) - 1));
         double2 x[L];
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-            uint64_t o = i;
-#pragma unroll
-            for (int p = 0; p < NU; ++p)
-                if ((l >> p) & 1) o |= 1ull << a.uq[p];
-            x[l] = psi[o];
-        }
+        for (int l = 0; l < L; ++l) x[l] = pb[i | um[l]];
         if (a.gk) {
             if (a.gk == 1)
                 noisy_mat1<NU>(x, m, a.gpos[0]);
             else
                 noisy_mat2<NU>(x, m, a.gpos[0], a.gpos[1]);
 #pragma unroll
-            for (int l = 0; l < L; ++l) {
-                uint64_t o = i;
-#pragma unroll
-                for (int p = 0; p < NU; ++p)
-                    if ((l >> p) & 1) o |= 1ull << a.uq[p];
-                psi[o] = x[l];
-            }
+            for (int l = 0; l < L; ++l) pb[i | um[l]] = x[l];
         }
         if (NK) noisy_rdm<NU, NK>(x, acc, a.npos[0], a.npos[1]);
     }
