@@ -21,6 +21,12 @@ scaling); see paper_2008_07140_b200/distributed.py.
 `--impl reference` times the reference CPU algorithm (the oracle port,
 oracle/qsv_oracle.c, a restatement of qcsim/statevector.py) on the host
 cores over a bounded sample of the same workload.
+
+Other lines (not the driver's headline): `--workload qft` (C4), `traj` (C5,
+pre-sampled depolarising trajectories), `partial` (partial-amplitude mode,
+partition.py: n=36 RQC cut at 18), `noisy` (1024 general-channel trajectories,
+noisy_batch.py: C1-shape RQC under amplitude damping), `--qubits 32` (C3's
+single-GPU point).
 """
 
 from __future__ import annotations
