@@ -262,13 +262,19 @@ def _slices(st, m: int, cb: int, rows) -> dict:
 def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
                 branch_budget: int = DEFAULT_BRANCH_BUDGET, max_qubits: int = 30,
                 batch_qubits: int = DEFAULT_BATCH_QUBITS, device: int = 0,
-                fuse: bool = True) -> dict[str, complex]:
+                fuse: bool = True, rank: int = 0, world: int = 1, group=None) -> dict[str, complex]:
     """Amplitudes of the requested basis strings (reference `partition.py:151-192`).
 
     `workers` is accepted and ignored (the GPU runs each batched half as one
     fused program).  `max_qubits` bounds each half like the reference's
     per-branch `run_full`; `batch_qubits` bounds a batched half-state
-    (half qubits + branch qubits)."""
+    (half qubits + branch qubits).
+
+    Sharded (world > 1, one process per GPU under torch.distributed): the
+    selector runs (values of the selector bits that are not branch qubits) are
+    dealt round-robin over the ranks — with at least `world` runs, taking bits
+    from the branch qubits if needed — and the per-target sums are added with
+    one all-reduce; every rank returns the full dict."""
     plan = plan_partition(program, cut, branch_budget)
     n = program.qubit_count
     wanted = [(t, parse_target(t, n)) for t in targets]
@@ -277,12 +283,15 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
     if m_half > max_qubits:
         raise TooManyQubits(f"{m_half} qubits in one half exceed the limit of {max_qubits}")
     cb = batch_bits(plan, max(batch_qubits, m_half))
+    if world > 1:
+        need = (world - 1).bit_length()  # selector runs >= world where the branch count allows
+        cb = max(0, min(cb, plan.c - need))
     low = (1 << cut) - 1
     rows_lo = [i & low for _, i in wanted]
     rows_up = [i >> cut for _, i in wanted]
     opts = N.options(fuse=fuse)
     acc = {t: 0j for t, _ in wanted}
-    for fixed in range(1 << (plan.c - cb)):
+    for fixed in range(rank, 1 << (plan.c - cb), world):
         (tl, ml), (tu, mu) = branch_streams(plan, cb, fixed)
         lo = _run_half(tl, ml, cb, device, max_qubits, opts)  # each state runs on its own stream:
         up = _run_half(tu, mu, cb, device, max_qubits, opts)  # the two halves overlap
@@ -294,4 +303,16 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
             _give_state(up, device)
         for (t, _), rl, ru in zip(wanted, rows_lo, rows_up):
             acc[t] += complex(np.dot(up_rows[ru], lo_rows[rl]))  # branch order b = 0 .. 2^cb - 1
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        vec = np.array([acc[t] for t, _ in wanted], dtype=np.complex128)
+        buf = torch.from_numpy(vec.view(np.float64).copy())
+        backend = dist.get_backend(group)
+        if backend == "nccl":
+            buf = buf.cuda(device)
+        dist.all_reduce(buf, group=group)
+        vec = buf.cpu().numpy().view(np.complex128)
+        acc = {t: complex(v) for (t, _), v in zip(wanted, vec)}
     return acc

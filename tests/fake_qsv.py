@@ -52,6 +52,18 @@ class FakeLib:
         self._psi(h)[offset:offset + count * stride:stride] = _arr(host, np.complex128, count)
         return 0
 
+    def qsv_upload(self, h, host, offset, count):
+        self._psi(h)[offset:offset + count] = _arr(host, np.complex128, count)
+        return 0
+
+    def qsv_gather_rows(self, h, offs_ptr, n_rows, row_len, host_out):
+        psi = self._psi(h)
+        offs = _arr(offs_ptr, np.uint64, n_rows)
+        out = _arr(host_out, np.complex128, n_rows * row_len).reshape(n_rows, row_len)
+        for r, o in enumerate(offs):
+            out[r] = psi[int(o):int(o) + row_len]
+        return 0
+
     def qsv_download(self, h, host, offset, count):
         _arr(host, np.complex128, count)[:] = self._psi(h)[offset:offset + count]
         return 0

@@ -188,3 +188,44 @@ def test_run_partial_gpu_edge_cases():
     amps = run_partial(prog, 2, ["0000", "0000", "1111"])
     assert list(amps) == ["0000", "1111"]
     assert abs(amps["0000"] - 0.5) < 1e-12 and abs(amps["1111"] - 0.5) < 1e-12
+
+
+def _sharded_partial_worker(rank, world, port, name, batch_qubits, out):
+    import os
+    import sys
+
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from fake_qsv import FakeLib
+
+        fake = FakeLib()
+        N.lib = lambda: fake  # numpy stand-in for the native steps (this process only)
+        g = GOLD[name]
+        amps = run_partial(parse_program(g["text"]), g["cut"], g["targets"], batch_qubits=batch_qubits,
+                           rank=rank, world=world)
+        if rank == 0:
+            np.save(out, np.array([amps[t] for t in g["targets"]]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,batch_qubits", [("rqc_1x8_s0", 64), ("rqc_1x16_s4", 0), ("rqc_2x7_s2", 12)])
+def test_sharded_partial_over_gloo(name, batch_qubits, tmp_path):
+    """Selector runs dealt over 2 ranks + one all-reduce of the per-target sums
+    reproduce the reference's partial amplitudes (host logic over gloo)."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "amps.npy")
+    mp.spawn(_sharded_partial_worker, args=(2, port, name, batch_qubits, out), nprocs=2, join=True)
+    g = GOLD[name]
+    want = np.array(g["re"]) + 1j * np.array(g["im"])
+    assert np.abs(np.load(out) - want).max() <= 1e-12
