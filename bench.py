@@ -367,8 +367,12 @@ def run_noisy_bench(args) -> None:
     from paper_2008_07140_b200.noisy_batch import run_noisy_batch
     from paper_2008_07140_b200.program import parse_program
 
-    rank, _, local = dist_env()
+    rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    if world > 1:  # replicas: each rank runs its B/world trajectories, no collective but the timing
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     prog = parse_program(workloads.rqc_text(*NOISY, seed=SEED))
     n = prog.qubit_count
     G = len(prog.gate_instructions())
@@ -376,8 +380,10 @@ def run_noisy_bench(args) -> None:
     kind, p = "ampdamp", 1e-3
     model = make_noise_model(kind, p)
 
+    mine = range(rank * B // world, (rank + 1) * B // world)
+
     def once(step):
-        rngs = [np.random.default_rng((SEED, step, t)) for t in range(B)]
+        rngs = [np.random.default_rng((SEED, step, t)) for t in mine]
         r = run_noisy_batch(prog, model, rngs, device=local)
         r.close()
         return r
@@ -388,10 +394,16 @@ def run_noisy_bench(args) -> None:
     times = []
     with ClockSampler(local) as clk:
         for k in range(args.steps):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             r = once(k)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
+    if world > 1:  # max over ranks
+        tt = torch.tensor(times, dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        times = tt.cpu().tolist()
     dt = statistics.median(times)
     work = float(B) * G * float(1 << n)
     cpu = None
@@ -409,9 +421,9 @@ def run_noisy_bench(args) -> None:
                          f"({cdt:.1f} s, {threads} threads; #Kraus + 2 state sweeps per noisy gate as "
                          f"reference noise.py:188-222)"}
     if rank == 0:
-        line = {"metric": METRIC, "value": work / dt, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        line = {"metric": METRIC, "value": work / dt, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
                 "config": {"workload": f"general-channel trajectories: RQC {NOISY[0]}x{NOISY[1]} "
                                        f"{NOISY[2]} cycles, n={n}, {kind} p={p} on every gate",
                            "trajectories": B, "gates": G, "noisy_steps": r.stats["noisy_steps"],
@@ -422,7 +434,8 @@ def run_noisy_bench(args) -> None:
                         "d2h_bytes_per_step": None},
                 "cpu_baseline": cpu, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
-
+    if world > 1:
+        dist.destroy_process_group()
 
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
