@@ -437,6 +437,7 @@ def run_noisy_bench(args) -> None:
     if world > 1:
         dist.destroy_process_group()
 
+
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
     if args.workload == "traj":
