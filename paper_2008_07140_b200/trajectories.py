@@ -50,10 +50,44 @@ class TrajectoryReport:
     seconds: float = 0.0
 
 
+def _run_clean_batches(slots, clean_gates, n, b, pq, tables, device, opts) -> int:
+    """Error-free trajectories, 2^b per (n + b)-qubit state (the last batch is padded
+    with extra copies so every batch reuses one plan and its compiled kernels); fills
+    tables[slot] from one PMEASURE over (batch qubits, probe qubits) per batch."""
+    L = N.lib()
+    B = 1 << b
+    rec = SV.compile_gates(clean_gates)
+    st = SV.init_state(n + b, max_qubits=n + b, device=device)
+    ones = np.ones(B, dtype=np.complex128)
+    qs = np.array([n + j for j in range(b - 1, -1, -1)] + list(pq), dtype=np.int32)
+    table = np.zeros(1 << len(qs), dtype=np.float64)
+    runs = 0
+    try:
+        for s0 in range(0, len(slots), B):
+            part = slots[s0:s0 + B]
+            st.set_basis(0)
+            N.check(L.qsv_upload_strided(st.handle, ones.ctypes.data, 0, B, 1 << n))
+            stats = N.qsv_run_stats()
+            N.check(L.qsv_run(st.handle, rec.ctypes.data, len(rec), C.byref(opts), C.byref(stats)))
+            N.check(L.qsv_pmeasure(st.handle, qs.ctypes.data, len(qs), table.ctypes.data))
+            per = table.reshape(B, -1)
+            for j, k in enumerate(part):
+                tables[k] = per[j]
+            runs += len(part)
+    finally:
+        st.close()
+    return runs
+
+
 def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0, *,
                      probe_qubits=(0, 1, 2), keep=(), dedup: bool = False, device: int = 0,
                      stream=None, rank: int = 0, world: int = 1, state: SV.StateVector | None = None,
-                     options=None, streams: int = 2) -> TrajectoryReport:
+                     options=None, streams: int = 2, batch_clean: int = 6) -> TrajectoryReport:
+    """`batch_clean` = b > 0: the error-free trajectories (not kept, not deduplicated) run
+    2^b at a time as ONE (n + b)-qubit state - trajectory index = top qubits - through
+    the clean circuit's fused plan (every trajectory block is simulated; the passes are
+    2^b times larger, so they run nearer the HBM roofline than 256 MiB passes), and
+    their probe tables come from one PMEASURE over (batch qubits, probe qubits)."""
     n = program.qubit_count
     mine = list(range(rank, n_traj, world))
     if state is None:
@@ -95,13 +129,22 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     updates = 0
     unique = 0
     t0 = time.perf_counter()
+    sampled = []
+    for t in mine:
+        ins = sample_pauli_insertions(program, p, trajectory_seed(base_seed, t))
+        sampled.append((ins, sum(len(v) for v in ins.values())))
+    batched = set()
+    if batch_clean > 0 and not dedup and n + batch_clean <= 34:
+        batched = {k for k, t in enumerate(mine) if sampled[k][1] == 0 and t not in keep}
     try:
+        if batched:
+            unique += _run_clean_batches(sorted(batched), clean_gates, n, batch_clean, pq, tables, device, opts_clean)
         for k, t in enumerate(mine):
-            seed = trajectory_seed(base_seed, t)
-            ins = sample_pauli_insertions(program, p, seed)
-            n_err = sum(len(v) for v in ins.values())
+            ins, n_err = sampled[k]
             errors.append(n_err)
             updates += (len(clean_gates) + n_err) << n
+            if k in batched:
+                continue
             if n_err == 0 and dedup and clean_cache is not None and t not in keep:
                 dedup_from[k] = clean_cache
                 continue
@@ -141,7 +184,10 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
         if async_tables and mine:
             for st_ in states:
                 N.check(L.qsv_synchronize(st_.handle))
-            tables[:] = dev_tables.cpu().numpy()[: len(mine)]
+            rows = dev_tables.cpu().numpy()[: len(mine)]
+            for k in range(len(mine)):
+                if k not in batched:
+                    tables[k] = rows[k]
         for k, src in dedup_from.items():
             tables[k] = tables[src]
         norms[:] = tables.sum(axis=1)  # the probe table sums to ||psi||^2

@@ -418,3 +418,17 @@ def gates_mod_instruction(name, q):
     from paper_2008_07140_b200.program import Instruction
 
     return Instruction(name, (q,))
+
+
+def test_trajectories_clean_batches_match_single_runs():
+    """Error-free trajectories run 2^b per batched state give the same probe tables
+    as one-by-one runs (and the noisy ones are untouched)."""
+    from paper_2008_07140_b200.trajectories import run_trajectories
+
+    prog = parse_program(workloads.rqc_text(3, 4, 8, seed=5))
+    a = run_trajectories(prog, 0.01, 100, base_seed=3, probe_qubits=(0, 6, 11), batch_clean=3)
+    b = run_trajectories(prog, 0.01, 100, base_seed=3, probe_qubits=(0, 6, 11), batch_clean=0)
+    assert sum(e == 0 for e in a.errors) >= 20 and sum(e > 0 for e in a.errors) >= 5
+    assert a.errors == b.errors
+    assert np.abs(a.tables - b.tables).max() <= 1e-12
+    assert np.abs(a.norms - 1).max() <= 1e-10
