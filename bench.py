@@ -230,12 +230,14 @@ def run_traj(args) -> None:
     torch.cuda.set_device(local)
     prog = parse_program(workloads.rqc_text(4, 6, 20, seed=SEED))
     n_traj = args.trajectories
-    run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world)  # warm-up
+    bc = args.batch_clean
+    run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world,
+                     batch_clean=bc)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
                            streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")),
-                           dedup=args.dedup)
+                           dedup=args.dedup, batch_clean=bc)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     tot = torch.tensor([float(rep.gate_updates), float(rep.unique_runs), dt], dtype=torch.float64)
@@ -253,7 +255,7 @@ def run_traj(args) -> None:
                 "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
                 "config": {"workload": f"C5: {n_traj} depolarising trajectories, RQC 4x6 20 cycles, p=1e-3",
                            "n_qubits": 24, "trajectories": n_traj, "unique_simulations": unique,
-                           "dedup": bool(args.dedup), "timing": "host wall clock around the batch"}}
+                           "dedup": bool(args.dedup), "batch_clean": bc, "timing": "host wall clock around the batch"}}
         print(json.dumps(line), flush=True)
 
 
@@ -608,6 +610,8 @@ def main():
     ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj", "partial", "noisy"))
     ap.add_argument("--trajectories", type=int, default=1024)
     ap.add_argument("--dedup", action="store_true")
+    ap.add_argument("--batch-clean", type=int, default=0,
+                    help="traj: run error-free trajectories 2^b per (n+b)-qubit state (0 = one by one)")
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--regs", type=int, default=0)
     ap.add_argument("--low", type=int, default=0)
