@@ -231,13 +231,19 @@ def run_traj(args) -> None:
     prog = parse_program(workloads.rqc_text(4, 6, 20, seed=SEED))
     n_traj = args.trajectories
     bc = args.batch_clean
+    topts = None
+    if args.tile or args.regs or args.low or args.super:
+        from paper_2008_07140_b200 import _native as N
+
+        topts = N.options(tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low,
+                          super_qubits=args.super)
     run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world,
-                     batch_clean=bc)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
+                     batch_clean=bc, options=topts)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
                            streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")),
-                           dedup=args.dedup, batch_clean=bc)
+                           dedup=args.dedup, batch_clean=bc, options=topts)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     tot = torch.tensor([float(rep.gate_updates), float(rep.unique_runs), dt], dtype=torch.float64)

@@ -432,3 +432,23 @@ def test_trajectories_clean_batches_match_single_runs():
     assert a.errors == b.errors
     assert np.abs(a.tables - b.tables).max() <= 1e-12
     assert np.abs(a.norms - 1).max() <= 1e-10
+
+
+def test_trajectories_fallback_when_plan_cannot_take_paulis(monkeypatch):
+    """When the clean plan cannot carry a trajectory's Paulis (QSV_E_UNSUPPORTED, e.g. a
+    super-pass plan) the trajectory runs as its explicit noisy program; states and probe
+    tables still match the oracle with the same seeds."""
+    from paper_2008_07140_b200 import _native as N
+    from paper_2008_07140_b200.trajectories import run_trajectories
+    from paper_2008_07140_b200.workloads import trajectory_seed
+
+    lib = N.lib()
+    monkeypatch.setattr(lib, "qsv_plan_execute_probe", lambda *a: N.QSV_E_UNSUPPORTED)
+    prog = parse_program(workloads.rqc_text(3, 4, 8, seed=2))
+    keep = tuple(range(6))
+    rep = run_trajectories(prog, 0.05, 6, base_seed=7, probe_qubits=(0, 5, 11), keep=keep)
+    assert sum(e > 0 for e in rep.errors) >= 1
+    for t in keep:
+        ref = O.run_full(prog, np.random.default_rng(trajectory_seed(7, t)), noise=("depolarizing", 0.05))
+        assert_parity(rep.kept[t], ref.state.amplitudes)
+        assert np.abs(rep.tables[t] - O.pmeasure(ref.state, (0, 5, 11))).max() <= 1e-12
