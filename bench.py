@@ -231,12 +231,7 @@ def run_traj(args) -> None:
     prog = parse_program(workloads.rqc_text(4, 6, 20, seed=SEED))
     n_traj = args.trajectories
     bc = args.batch_clean
-    topts = None
-    if args.tile or args.regs or args.low or args.super:
-        from paper_2008_07140_b200 import _native as N
-
-        topts = N.options(tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low,
-                          super_qubits=args.super)
+    topts = planner_options(args)
     run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world,
                      batch_clean=bc, options=topts)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
     torch.cuda.synchronize()
@@ -263,6 +258,16 @@ def run_traj(args) -> None:
                            "n_qubits": 24, "trajectories": n_traj, "unique_simulations": unique,
                            "dedup": bool(args.dedup), "batch_clean": bc, "timing": "host wall clock around the batch"}}
         print(json.dumps(line), flush=True)
+
+
+def planner_options(args):
+    """--tile/--regs/--low/--super for the traj and partial workloads (None = their defaults)."""
+    if not (args.tile or args.regs or args.low or args.super):
+        return None
+    from paper_2008_07140_b200 import _native as N
+
+    return N.options(tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low,
+                     super_qubits=args.super)
 
 
 PARTIAL = (6, 6, 12)  # partial-mode workload: n=36 RQC, cut 18
@@ -313,14 +318,15 @@ def run_partial_bench(args) -> None:
     torch.cuda.set_device(local)
     prog, cut, plan, targets = partial_workload()
     work = partial_updates(plan)
+    popts = planner_options(args)
     for _ in range(args.warmup):
-        run_partial(prog, cut, targets, device=local)
+        run_partial(prog, cut, targets, device=local, options=popts)
     torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             t0 = time.perf_counter()
-            run_partial(prog, cut, targets, device=local)
+            run_partial(prog, cut, targets, device=local, options=popts)
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
     dt = statistics.median(times)

@@ -262,7 +262,8 @@ def _slices(st, m: int, cb: int, rows) -> dict:
 def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
                 branch_budget: int = DEFAULT_BRANCH_BUDGET, max_qubits: int = 30,
                 batch_qubits: int = DEFAULT_BATCH_QUBITS, device: int = 0,
-                fuse: bool = True, rank: int = 0, world: int = 1, group=None) -> dict[str, complex]:
+                fuse: bool = True, rank: int = 0, world: int = 1, group=None,
+                options=None) -> dict[str, complex]:
     """Amplitudes of the requested basis strings (reference `partition.py:151-192`).
 
     `workers` is accepted and ignored (the GPU runs each batched half as one
@@ -289,7 +290,7 @@ def run_partial(program: Program, cut: int, targets, *, workers: int = 1,
     low = (1 << cut) - 1
     rows_lo = [i & low for _, i in wanted]
     rows_up = [i >> cut for _, i in wanted]
-    opts = N.options(fuse=fuse)
+    opts = options or N.options(fuse=fuse)  # `options`: planner tile/register/low qubits
     acc = {t: 0j for t, _ in wanted}
     for fixed in range(rank, 1 << (plan.c - cb), world):
         (tl, ml), (tu, mu) = branch_streams(plan, cb, fixed)
