@@ -235,12 +235,13 @@ def run_traj(args) -> None:
     run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world,
                      batch_clean=bc, options=topts)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
-                           streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")),
-                           dedup=args.dedup, batch_clean=bc, options=topts)
-    torch.cuda.synchronize()
-    dt = time.perf_counter() - t0
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        rep = run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
+                               streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")),
+                               dedup=args.dedup, batch_clean=bc, options=topts)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
     tot = torch.tensor([float(rep.gate_updates), float(rep.unique_runs), dt], dtype=torch.float64)
     if world > 1:
         import torch.distributed as dist
@@ -256,7 +257,8 @@ def run_traj(args) -> None:
                 "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
                 "config": {"workload": f"C5: {n_traj} depolarising trajectories, RQC 4x6 20 cycles, p=1e-3",
                            "n_qubits": 24, "trajectories": n_traj, "unique_simulations": unique,
-                           "dedup": bool(args.dedup), "batch_clean": bc, "timing": "host wall clock around the batch"}}
+                           "dedup": bool(args.dedup), "batch_clean": bc, "timing": "host wall clock around the batch"},
+                "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 
 
