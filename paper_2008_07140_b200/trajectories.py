@@ -25,6 +25,7 @@ replicas: rank r takes t = r, r+P, ... and results are gathered on rank 0.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -48,6 +49,10 @@ class TrajectoryReport:
     gate_updates: int = 0       # sum over trajectories of (gates incl. Paulis) * 2^n
     unique_runs: int = 0
     seconds: float = 0.0
+
+
+_PLANS: dict = {}  # (gate records, n, options, device) -> qsv_plan of the clean circuit
+_MAX_PLANS = 8
 
 
 def _run_clean_batches(slots, clean_gates, n, b, pq, tables, device, opts) -> int:
@@ -112,9 +117,17 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
         if inst.is_gate:
             gate_index[j] = len(gate_index)
     clean_rec = SV.compile_gates(clean_gates)
-    clean_plan = C.c_void_p()
-    N.check(L.qsv_plan_create(clean_rec.ctypes.data, len(clean_rec), n, C.byref(opts_clean),
-                              C.byref(clean_plan)))
+    # the clean circuit's plan is built once per (circuit, options) and kept, as
+    # qsv_run keeps its plans: repeated batches of one circuit skip the planner
+    key = (clean_rec.tobytes(), n, bytes(opts_clean), device)
+    clean_plan = _PLANS.get(key)
+    if clean_plan is None:
+        clean_plan = C.c_void_p()
+        N.check(L.qsv_plan_create(clean_rec.ctypes.data, len(clean_rec), n, C.byref(opts_clean),
+                                  C.byref(clean_plan)))
+        while len(_PLANS) >= _MAX_PLANS:
+            L.qsv_plan_destroy(_PLANS.pop(next(iter(_PLANS))))
+        _PLANS[key] = clean_plan
     pq = np.asarray(probe_qubits, dtype=np.int32)
     tables = np.zeros((len(mine), 1 << len(pq)))
     norms = np.zeros(len(mine))
@@ -133,18 +146,29 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     updates = 0
     unique = 0
     t0 = time.perf_counter()
-    sampled = []
-    for t in mine:
-        ins = sample_pauli_insertions(program, p, trajectory_seed(base_seed, t))
-        sampled.append((ins, sum(len(v) for v in ins.values())))
+    # QSV_TRAJ_TRACE=<file>: per-trajectory host launch times (diagnostic)
+    trace = [] if os.environ.get("QSV_TRAJ_TRACE") else None
+    # errors are sampled inside the launch loop, so the host sampling of one
+    # trajectory overlaps the GPU passes of the earlier ones (sampling all 1024
+    # C5 trajectories up front left the GPU idle for ~78 ms); only the batched
+    # clean mode needs them all first, to know which trajectories are error-free
+    sampled = {}
+
+    def draws(k, t):
+        if k not in sampled:
+            ins = sample_pauli_insertions(program, p, trajectory_seed(base_seed, t))
+            sampled[k] = (ins, sum(len(v) for v in ins.values()))
+        return sampled[k]
+
     batched = set()
     if batch_clean > 0 and not dedup and n + batch_clean <= 34:
-        batched = {k for k, t in enumerate(mine) if sampled[k][1] == 0 and t not in keep}
+        batched = {k for k, t in enumerate(mine) if draws(k, t)[1] == 0 and t not in keep}
     try:
         if batched:
             unique += _run_clean_batches(sorted(batched), clean_gates, n, batch_clean, pq, tables, device, opts_clean)
         for k, t in enumerate(mine):
-            ins, n_err = sampled[k]
+            ins, n_err = draws(k, t)
+            sampled.pop(k, None)
             errors.append(n_err)
             updates += (len(clean_gates) + n_err) << n
             if k in batched:
@@ -178,6 +202,8 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
                     rc = L.qsv_pmeasure_async(state.handle, pq.ctypes.data, len(pq),
                                               C.c_void_p(dev_tables[k].data_ptr()))
             N.check(rc)
+            if trace is not None:
+                trace.append((k, n_err, time.perf_counter() - t0))
             unique += 1
             if not async_tables:
                 tables[k] = SV.pmeasure(state, pq)
@@ -192,11 +218,14 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             for k in range(len(mine)):
                 if k not in batched:
                     tables[k] = rows[k]
+        if trace is not None:
+            trace.append((-1, 0, time.perf_counter() - t0))
+            with open(os.environ["QSV_TRAJ_TRACE"], "a") as fh:
+                fh.write(" ".join(f"{a}:{b}:{c:.5f}" for a, b, c in trace) + "\n")
         for k, src in dedup_from.items():
             tables[k] = tables[src]
         norms[:] = tables.sum(axis=1)  # the probe table sums to ||psi||^2
     finally:
-        L.qsv_plan_destroy(clean_plan)
         for st_ in states[1:]:
             st_.close()
     return TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
