@@ -57,14 +57,57 @@ SEED = 0
 FP64_PEAK_GINSTR = 18050.0  # DFMA lane-instructions/s (36.1 TFLOP/s measured)
 
 
-def measured_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
-    for p in sorted((ROOT / "profiles").glob("r*/traffic.json"), reverse=True):
+def ncu_traffic(args, passes: int):
+    """DRAM bytes per pass-kernel launch, MEASURED: re-runs this bench (one warm-up +
+    one timed step of the same workload) under `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum` and keeps the last step's `passes` launches.  Returns
+    ({mean, per_launch, ...}, None) or (None, reason).  The child's own numbers are
+    discarded (a number printed under ncu is never a bench value)."""
+    import csv
+    import shutil
+    import tempfile
+
+    if os.environ.get("QSV_BENCH_UNDER_NCU"):
+        return None, "running under ncu"
+    exe = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(exe):
+        return None, "ncu not found"
+    fwd = ["--workload", args.workload]
+    for flag, v in (("--qubits", args.qubits), ("--tile", args.tile), ("--regs", args.regs),
+                    ("--low", args.low), ("--super", args.super)):
+        if v:
+            fwd += [flag, str(v)]
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "traffic.csv")
+        cmd = [exe, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+               "--clock-control", "none", "--csv", "-k", "regex:qsv_pass|pass_kernel", "--log-file", log,
+               sys.executable, str(ROOT / "bench.py"), "--steps", "1", "--warmup", "1", "--no-e2e",
+               "--no-cpu-baseline", "--traffic", "off", *fwd]
         try:
-            return json.loads(p.read_text())["dram_bytes_per_launch"]
-        except (KeyError, ValueError):
-            continue
-    return None
+            proc = subprocess.run(cmd, env=dict(os.environ, QSV_BENCH_UNDER_NCU="1"), capture_output=True,
+                                  text=True, timeout=args.traffic_timeout)
+        except subprocess.TimeoutExpired:
+            return None, f"ncu run exceeded {args.traffic_timeout} s"
+        if proc.returncode != 0 or not os.path.exists(log):
+            return None, f"ncu exit {proc.returncode}: {(proc.stderr or proc.stdout)[-200:]}"
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                 "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
+        rows = [r for r in csv.reader(open(log)) if len(r) > 10]
+    if len(rows) < 2:
+        return None, "ncu produced no launches"
+    ix = {k: i for i, k in enumerate(rows[0])}
+    per = {}
+    for r in rows[1:]:
+        rid = int(r[ix["ID"]])
+        v = float(r[ix["Metric Value"]].replace(",", "")) * scale.get(r[ix["Metric Unit"]], 1.0)
+        per.setdefault(rid, {})[r[ix["Metric Name"]]] = v
+    ids = sorted(per)[-passes:]
+    dram = [per[i].get("dram__bytes_read.sum", 0.0) + per[i].get("dram__bytes_write.sum", 0.0) for i in ids]
+    return {"mean": sum(dram) / len(dram), "per_launch": dram,
+            "read": [per[i].get("dram__bytes_read.sum", 0.0) for i in ids],
+            "ncu_ms": [per[i].get("gpu__time_duration.sum", 0.0) for i in ids],
+            "src": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none, "
+                   "run by this bench on the same workload (last step's pass launches)"}, None
 
 
 def peaks() -> dict:
@@ -525,33 +568,42 @@ def run_gpu(args) -> None:
     ms_step = total_ms / args.steps
     value = G * float(1 << n) / (ms_step / 1e3)
 
-    # roofline of the dominant kernel (fused pass kernel): algorithmic bytes per
-    # launch = 2 * 16 * 2^n (read + write every amplitude once)
+    # roofline of the dominant kernel (the fused pass kernel).  Algorithmic bytes
+    # per launch as libqsv counts them: 2 x 16 x 2^n for a pass (read + write every
+    # amplitude once), 16 x 2^n for the first pass after set_basis (it synthesises
+    # |0..0> and only writes); unfused: 2 x 16 x 2^(n - #controls) per gate.
+    # achieved = sum(bytes) / sum(event-timed launch ms) over the K timed steps
+    # = mean bytes per launch / mean launch duration.
     launches = stats.launches
     avg_launch_ms = stats.kernel_ms / max(1, launches)
     pk = peaks()
-    # fused passes: every pass reads + writes all 2^n amplitudes; unfused: each
-    # gate touches the amplitudes whose controls are set (libqsv counts them)
-    bytes_per_launch = (stats.algorithmic_bytes / max(1, launches)) if args.unfused else 32.0 * float(1 << n)
+    bytes_per_launch = stats.algorithmic_bytes / max(1, launches)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
-    # the specialised passes are FP64-issue-bound as much as HBM-bound: report
-    # the FP64 side too (generator's FP64 instruction count per amplitude per
-    # pass x 2^n, against the measured DFMA rate)
-    fp64_per_amp = 0.0
-    if not args.unfused:
-        for pi in range(int(info.passes)):
-            f = C.c_double()
-            if L.qsv_plan_pass_cost(plan, pi, C.byref(f)) == 0:
-                fp64_per_amp += f.value
+    # per pass of the last timed step: ms, algorithmic bytes, HBM fraction and the
+    # generator's FP64 instructions per amplitude (the heavy passes are FP64-issue
+    # bound: against the measured DFMA rate)
+    pass_ms, pass_bytes = N.last_launches(state.handle)
+    per_pass, fp64_per_amp = [], 0.0
+    for pi in range(len(pass_ms)):
+        f = C.c_double(0.0)
+        if not args.unfused:
+            L.qsv_plan_pass_cost(plan, pi, C.byref(f))
+            fp64_per_amp += f.value
+        if args.unfused and pi >= 8:
+            continue
+        gbs = pass_bytes[pi] / (pass_ms[pi] / 1e3) / 1e9
+        per_pass.append({"pass": pi, "ms": round(float(pass_ms[pi]), 3), "algorithmic_bytes": float(pass_bytes[pi]),
+                         "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / pk["hbm_gbs"], 3),
+                         "fp64_per_amp": round(f.value, 1),
+                         "fp64_frac": round(f.value * float(1 << n) / (pass_ms[pi] / 1e3) / 1e9 / FP64_PEAK_GINSTR, 3)})
     fp64_rate = fp64_per_amp * float(1 << n) / (ms_step / 1e3)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"],
-                "traffic": args.traffic if args.traffic is not None else (
-                    measured_traffic() if (n == N_BASE and args.workload == "rqc") else None),
+                "frac": achieved / pk["hbm_gbs"], "traffic": None,
                 "peak_src": pk["src"],
                 "kernel": "qsv_pass (specialised fused pass)" if not args.unfused else "gate_kernel",
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
                 "kernel_share_of_step": stats.kernel_ms / total_ms,
+                "per_pass": per_pass,
                 "fp64": None if args.unfused else {
                     "instr_per_amplitude": fp64_per_amp, "achieved_ginstr_s": fp64_rate / 1e9,
                     "peak_ginstr_s": FP64_PEAK_GINSTR, "frac": fp64_rate / 1e9 / FP64_PEAK_GINSTR,
@@ -592,6 +644,18 @@ def run_gpu(args) -> None:
         cpu.pop("gates", None)
 
     clocks = clk.summary()
+    L.qsv_plan_destroy(plan)
+    state.close()
+    if args.traffic == "auto" and not args.unfused:
+        tr, why = ncu_traffic(args, len(pass_ms))
+        if tr is None:
+            roofline["traffic_note"] = why
+        else:
+            roofline["traffic"] = tr["mean"]
+            roofline["traffic_src"] = tr["src"]
+            for row, b, rd in zip(per_pass, tr["per_launch"], tr["read"]):
+                row["dram_bytes"] = b
+                row["dram_read_bytes"] = rd
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -609,8 +673,6 @@ def run_gpu(args) -> None:
         "gpu_launches": int(launches),  # fused pass kernels (|0..0> is synthesised by the first pass)
         "clocks": clocks,
     }
-    L.qsv_plan_destroy(plan)
-    state.close()
     print(json.dumps(line), flush=True)
 
 
@@ -636,8 +698,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=12.0)
-    ap.add_argument("--traffic", type=float, default=None,
-                    help="dram bytes per pass_kernel launch from an ncu --set full capture")
+    ap.add_argument("--traffic", default="auto", choices=("auto", "off"),
+                    help="auto: measure DRAM bytes per pass launch with an ncu child run of this workload")
+    ap.add_argument("--traffic-timeout", type=float, default=240.0)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

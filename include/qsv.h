@@ -29,7 +29,9 @@
  * are a bit mask and act on the all-ones block only (gates.py:162-168).
  *
  * Every call returns 0 on success or a negative status whose class mirrors
- * qcsim/errors.py (see QSV_E_*); qsv_last_error() gives the message.  Calls are
+ * qcsim/errors.py (see QSV_E_*); qsv_state_last_error(st) gives the message of the
+ * last failed call on that handle (qsv_last_error() the calling thread's last one,
+ * for calls without a handle).  Calls are
  * asynchronous on the state's stream except readouts, which synchronise.
  * There is no CPU execution path: without a CUDA device, state calls fail
  * with QSV_E_DEVICE.  The planning calls (qsv_plan_*) are pure host code.
@@ -123,6 +125,13 @@ typedef struct qsv_op_info {
 
 const char *qsv_version(void);
 const char *qsv_last_error(void);
+/* message of the last failed call made on `st` (per handle: calls on other handles or
+ * threads in between do not overwrite it); "" when none failed */
+const char *qsv_state_last_error(const qsv_state *st);
+/* per-launch event times (ms) and algorithmic bytes of the last call on `st` that ran
+ * with qsv_options.profile = 1 (bytes: 2 x 16 x 2^n per pass, 16 x 2^n for a pass that
+ * synthesises its basis-state input); copies min(count, cap) entries */
+int qsv_last_launches(const qsv_state *st, double *ms, double *bytes, int64_t cap, int64_t *count);
 int qsv_device_count(int *out);
 
 /* ---- state lifetime and data movement ---- */

@@ -69,6 +69,8 @@ _P = C.c_void_p
 _SIGNATURES = {
     "qsv_version": ([], C.c_char_p),
     "qsv_last_error": ([], C.c_char_p),
+    "qsv_state_last_error": ([C.c_void_p], C.c_char_p),
+    "qsv_last_launches": ([_P, _P, _P, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "qsv_create": ([C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),
     "qsv_create_on": ([C.c_int, C.c_int, _P, _P, C.POINTER(_P)], C.c_int),
@@ -144,9 +146,25 @@ def lib():
     return _lib
 
 
-def check(rc: int) -> None:
+def check(rc: int, handle=None) -> None:
+    """Raise the errors.py class of a failed status; the message comes from the
+    handle the call acted on when given (qsv_state_last_error), else from the
+    calling thread's last failure."""
     if rc != 0:
-        raise_for_status(rc, lib().qsv_last_error().decode(errors="replace"))
+        L = lib()
+        msg = L.qsv_state_last_error(handle) if handle is not None else L.qsv_last_error()
+        raise_for_status(rc, (msg or b"").decode(errors="replace"))
+
+
+def last_launches(handle):
+    """(ms, algorithmic bytes) per launch of the last profiled call on `handle`."""
+    L = lib()
+    n = C.c_int64()
+    check(L.qsv_last_launches(handle, None, None, 0, C.byref(n)), handle)
+    ms = np.zeros(n.value)
+    by = np.zeros(n.value)
+    check(L.qsv_last_launches(handle, ms.ctypes.data, by.ctypes.data, n.value, C.byref(n)), handle)
+    return ms, by
 
 
 def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0,

@@ -25,11 +25,23 @@ using namespace qsv;
 namespace {
 
 thread_local std::string g_error;
+// the state handle the current C-ABI call acts on (ErrBind): failures are also
+// recorded on that handle, so qsv_state_last_error(st) survives calls made on
+// other handles or threads in between
+thread_local qsv_state *g_bound = nullptr;
+void record_state_error(qsv_state *st, const std::string &msg);
 
 int fail(int code, const std::string &msg) {
     g_error = msg;
+    if (g_bound) record_state_error(g_bound, msg);
     return code;
 }
+
+struct ErrBind {
+    qsv_state *prev;
+    explicit ErrBind(qsv_state *st) : prev(g_bound) { g_bound = st; }
+    ~ErrBind() { g_bound = prev; }
+};
 
 #define CUDA_TRY(expr)                                                                           \
     do {                                                                                         \
@@ -65,8 +77,15 @@ struct qsv_state {
     double2 *nb_mats = nullptr;  // batched noisy step: per-trajectory gate matrices + rdm out
     size_t nb_bytes = 0;
     double2 *nb_host = nullptr;  // pinned staging of the same two regions (async steps)
+    std::string last_error;      // message of the last failed call on this handle
+    // per-launch event times / algorithmic bytes of the last profiled plan execution
+    std::vector<double> launch_ms, launch_bytes;
     uint64_t size() const { return 1ull << n; }
 };
+
+namespace {
+void record_state_error(qsv_state *st, const std::string &msg) { st->last_error = msg; }
+}  // namespace
 
 struct qsv_plan {
     Plan p;
@@ -113,7 +132,9 @@ int set_device(int dev) {
 struct LaunchTimer {
     bool on = false;
     cudaStream_t s = nullptr;
+    qsv_state *st = nullptr;  // receives per-launch times and bytes (qsv_last_launches)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    std::vector<double> bytes;
     void begin() {
         if (!on) return;
         cudaEvent_t a, b;
@@ -122,22 +143,32 @@ struct LaunchTimer {
         cudaEventRecord(a, s);
         ev.push_back({a, b});
     }
-    void end() {
-        if (on) cudaEventRecord(ev.back().second, s);
+    // algorithmic bytes of the launch just ended (2 x 16 x 2^n for a pass, 16 x 2^n
+    // for a pass that synthesises its basis-state input and only writes)
+    void end(double algorithmic_bytes = 0.0) {
+        if (!on) return;
+        cudaEventRecord(ev.back().second, s);
+        bytes.push_back(algorithmic_bytes);
     }
     void collect(qsv_run_stats *stats) {
         if (!on) return;
         cudaStreamSynchronize(s);
         double tot = 0, mx = 0;
+        if (st) {
+            st->launch_ms.clear();
+            st->launch_bytes = bytes;
+        }
         for (auto &p : ev) {
             float ms = 0;
             cudaEventElapsedTime(&ms, p.first, p.second);
             tot += ms;
             mx = std::max(mx, (double)ms);
+            if (st) st->launch_ms.push_back(ms);
             cudaEventDestroy(p.first);
             cudaEventDestroy(p.second);
         }
         ev.clear();
+        bytes.clear();
         if (stats) {
             stats->kernel_ms += tot;
             stats->max_launch_ms = std::max(stats->max_launch_ms, mx);
@@ -271,7 +302,10 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
     LaunchTimer tm;
     tm.on = profile;
     tm.s = st->stream;
+    tm.st = st;
     int64_t hbm_passes = 0, launches = 0;
+    double alg_bytes = 0.0;
+    const double full = 32.0 * (double)st->size();
     for (size_t si = 0; si < P.supers.size(); ++si) {
         const SuperPass &sp = P.supers[si];
         if (use_jit && use_supers(P) && P.jit_super_funcs[si]) {
@@ -283,28 +317,33 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
             std::string err;
             tm.begin();
             rc = jit_launch_super(P, (int)si, st->amps, st->barrier, st->stream, err);
-            tm.end();
+            tm.end(full);
             if (rc) return fail(rc, err);
             ++hbm_passes;
             ++launches;
+            alg_bytes += full;
             continue;
         }
         for (int i = sp.pass_begin; i < sp.pass_end; ++i) {
             tm.begin();
             int rc;
+            // a specialised pass launched on a pending basis state synthesises it: no read
+            double b = full;
             if (use_jit) {
                 std::string err;
                 const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+                if (st->pending_basis >= 0) b = 0.5 * full;
                 rc = jit_launch(P, i, st->amps, st->n, st->stream, err, basis);
                 if (rc) return fail(rc, err);
                 st->pending_basis = -1;
             } else {
                 rc = launch_pass(st, P, i, dp, ds, dop);
             }
-            tm.end();
+            tm.end(b);
             if (rc) return rc;
             ++hbm_passes;
             ++launches;
+            alg_bytes += b;
         }
     }
     tm.collect(stats);
@@ -314,7 +353,7 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
         stats->inner_passes += (int64_t)P.passes.size();
         stats->stages += (int64_t)P.stages.size();
         stats->launches += launches;
-        stats->algorithmic_bytes += (double)hbm_passes * 32.0 * (double)st->size();
+        stats->algorithmic_bytes += alg_bytes;
     }
     return QSV_OK;
 }
@@ -373,6 +412,19 @@ extern "C" {
 const char *qsv_version(void) { return "qsv 0.1.0 (sm_100a)"; }
 
 const char *qsv_last_error(void) { return g_error.c_str(); }
+
+const char *qsv_state_last_error(const qsv_state *st) { return st ? st->last_error.c_str() : g_error.c_str(); }
+
+int qsv_last_launches(const qsv_state *st, double *ms, double *bytes, int64_t cap, int64_t *count) {
+    if (!st || !count) return fail(QSV_E_PARSE, "qsv_last_launches: null argument");
+    const int64_t n = (int64_t)st->launch_ms.size();
+    *count = n;
+    for (int64_t i = 0; i < std::min(n, cap); ++i) {
+        if (ms) ms[i] = st->launch_ms[i];
+        if (bytes) bytes[i] = i < (int64_t)st->launch_bytes.size() ? st->launch_bytes[i] : 0.0;
+    }
+    return QSV_OK;
+}
 
 int qsv_device_count(int *out) {
     int c = 0;
@@ -447,12 +499,14 @@ int qsv_destroy(qsv_state *st) {
 }
 
 int qsv_device_ptr(qsv_state *st, void **out) {
+    ErrBind eb_(st);
     *out = st->amps;
     const int rc = set_device(st->device);
     return rc ? rc : materialize(st);
 }
 
 int qsv_set_basis(qsv_state *st, uint64_t index) {
+    ErrBind eb_(st);
     if (index >= st->size()) return fail(QSV_E_PARSE, "basis index out of range");
     st->pending_basis = (int64_t)index;  // materialised lazily (see qsv_state)
     return QSV_OK;
@@ -461,6 +515,7 @@ int qsv_set_basis(qsv_state *st, uint64_t index) {
 constexpr uint64_t kCopyChunk = 1ull << 22;  // amplitudes per host<->device copy (64 MiB)
 
 int qsv_upload(qsv_state *st, const void *host, uint64_t offset, uint64_t count) {
+    ErrBind eb_(st);
     if (offset + count > st->size()) return fail(QSV_E_PARSE, "upload range out of bounds");
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -477,6 +532,7 @@ int qsv_upload(qsv_state *st, const void *host, uint64_t offset, uint64_t count)
 }
 
 int qsv_download_async(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
+    ErrBind eb_(st);
     if (offset + count > st->size()) return fail(QSV_E_PARSE, "download range out of bounds");
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -492,6 +548,7 @@ int qsv_download_async(qsv_state *st, void *host, uint64_t offset, uint64_t coun
 }
 
 int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
+    ErrBind eb_(st);
     const int rc = qsv_download_async(st, host, offset, count);
     if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(st->stream));
@@ -499,6 +556,7 @@ int qsv_download(qsv_state *st, void *host, uint64_t offset, uint64_t count) {
 }
 
 int qsv_synchronize(qsv_state *st) {
+    ErrBind eb_(st);
     const int rc = materialize(st);
     if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(st->stream));
@@ -506,6 +564,7 @@ int qsv_synchronize(qsv_state *st) {
 }
 
 int qsv_apply_gate(qsv_state *st, const qsv_gate *gate) {
+    ErrBind eb_(st);
     std::vector<GateRec> recs;
     std::string msg;
     int rc = to_records(gate, 1, st->n, recs, msg);
@@ -675,6 +734,7 @@ int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out
 }
 
 int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats) {
+    ErrBind eb_(st);
     Plan &P = plan->p;
     if (P.n != st->n) return fail(QSV_E_PARSE, "plan built for a different qubit count");
     int rc = set_device(st->device);
@@ -739,6 +799,7 @@ std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, 
 }
 
 int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt, qsv_run_stats *stats) {
+    ErrBind eb_(st);
     int rc = set_device(st->device);
     if (rc) return rc;
     std::vector<GateRec> recs;
@@ -752,10 +813,11 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
         LaunchTimer tm;
         tm.on = opt && opt->profile;
         tm.s = st->stream;
+        tm.st = st;
         for (const GateRec &g : recs) {
             tm.begin();
             rc = launch_gate(st, g);
-            tm.end();
+            tm.end(32.0 * std::ldexp(1.0, st->n - std::popcount(g.cmask)));
             if (rc) return rc;
         }
         tm.collect(stats);
@@ -1148,8 +1210,11 @@ int launch_pauli(qsv_state *st, const PauliString &ps) {
 int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_t n_paulis, const qsv_options *opt,
                         qsv_run_stats *stats, const int32_t *probe, int probe_m, double *probe_table) {
     std::string msg;
+    // the error placement runs on the plan's specialised kernels: without them (jit = -1,
+    // or NVRTC unavailable) report UNSUPPORTED so callers take the explicit-gate qsv_run path
+    if (opt && opt->jit < 0) return fail(QSV_E_UNSUPPORTED, "Pauli placement needs specialised kernels (jit = -1)");
     int rc = jit_prepare(P, st->device, msg);
-    if (rc) return fail(rc, msg);
+    if (rc) return fail(QSV_E_UNSUPPORTED, "specialised kernels unavailable: " + msg);
     const std::vector<double> &sc = pass_scales(P);
     const int np = (int)P.passes.size();
     const bool has_pl = !pl.modified.empty();
@@ -1166,19 +1231,25 @@ int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_
     LaunchTimer tm;
     tm.on = opt && opt->profile;
     tm.s = st->stream;
+    tm.st = st;
     int64_t launches = 0;
+    double alg_bytes = 0.0;
+    const double full = 32.0 * (double)st->size();
     for (int j = 0; j <= np; ++j) {
         if (has_pl && pl.bnd[j].any) {
             tm.begin();
             rc = launch_pauli(st, pl.bnd[j]);
-            tm.end();
+            tm.end(full);
             if (rc) return rc;
             ++launches;
+            alg_bytes += full;
         }
         if (j == np) break;
         tm.begin();
+        double b = full;
         if (!has_pl || !pl.modified[j]) {
             const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+            if (st->pending_basis >= 0) b = 0.5 * full;
             if (fused_probe && j == np - 1)
                 rc = jit_launch_probe(P, j, pfn, pgrid, st->amps, st->n, st->stream, msg, basis, st->work);
             else
@@ -1223,8 +1294,9 @@ int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_
             if (!rc) rc = launch_pass(st, Q, 0, dp, ds, dop);
             if (rc) return rc;
         }
-        tm.end();
+        tm.end(b);
         ++launches;
+        alg_bytes += b;
     }
     tm.collect(stats);
     if (stats) {
@@ -1233,7 +1305,7 @@ int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_
         stats->inner_passes += np;
         stats->stages += (int64_t)P.stages.size();
         stats->launches += launches;
-        stats->algorithmic_bytes += (double)launches * 32.0 * (double)st->size();
+        stats->algorithmic_bytes += alg_bytes;
     }
     if (probe) {
         if (fused_probe) {
@@ -1248,6 +1320,7 @@ int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_
 
 int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
                             const qsv_options *opt, qsv_run_stats *stats) {
+    ErrBind eb_(st);
     if (n_paulis <= 0) return qsv_plan_execute(st, plan, opt, stats);
     Plan &P = plan->p;
     if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
@@ -1263,6 +1336,7 @@ int qsv_plan_execute_paulis(qsv_state *st, qsv_plan *plan, const qsv_pauli *paul
 int qsv_plan_execute_probe(qsv_state *st, qsv_plan *plan, const qsv_pauli *paulis, int64_t n_paulis,
                            const int32_t *probe_qubits_msb_first, int m, double *device_table, const qsv_options *opt,
                            qsv_run_stats *stats) {
+    ErrBind eb_(st);
     Plan &P = plan->p;
     if (P.n != st->n) return fail(QSV_E_PARSE, "plan and state sizes differ");
     if (m < 1 || m > 4) return fail(QSV_E_UNSUPPORTED, "probe tables take 1..4 qubits");
@@ -1338,6 +1412,7 @@ int qsv_plan_pauli_stream(const qsv_plan *plan, const qsv_pauli *paulis, int64_t
 
 int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
                          uint64_t positions, int *out) {
+    ErrBind eb_(st);
     *out = 0;
     std::vector<GateRec> recs;
     std::string msg;
@@ -1359,6 +1434,7 @@ int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, 
 
 int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_options *opt,
                      const qsv_exchange *ex, qsv_run_stats *stats) {
+    ErrBind eb_(st);
     int rc = set_device(st->device);
     if (rc) return rc;
     const int s = std::popcount(ex->positions);
@@ -1386,15 +1462,20 @@ int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, cons
     LaunchTimer tm;
     tm.on = opt && opt->profile;
     tm.s = st->stream;
+    tm.st = st;
+    const double full = 32.0 * (double)st->size();
+    double alg_bytes = 0.0;
     for (int i = 0; i <= last; ++i) {
         const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+        const double b = st->pending_basis >= 0 ? 0.5 * full : full;
         tm.begin();
         if (i < last) rc = jit_launch(P, i, st->amps, st->n, st->stream, msg, basis);
         else rc = jit_launch_exchange(P, i, xfn, xgrid, st->amps, st->n, st->stream, msg, basis,
                                       (const unsigned long long *)ex->dst, ex->self_bits);
-        tm.end();
+        tm.end(b);
         if (rc) return fail(rc, msg);
         st->pending_basis = -1;
+        alg_bytes += b;
     }
     tm.collect(stats);
     if (stats) {
@@ -1403,7 +1484,7 @@ int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, cons
         stats->inner_passes += last + 1;
         stats->stages += (int64_t)P.stages.size();
         stats->launches += last + 1;
-        stats->algorithmic_bytes += (double)(last + 1) * 32.0 * (double)st->size();
+        stats->algorithmic_bytes += alg_bytes;
     }
     return QSV_OK;
 }
@@ -1466,6 +1547,7 @@ int qsv_jit_compile(const char *src, int64_t *cubin_bytes) {
 }
 
 int qsv_norm_sq(qsv_state *st, double *out) {
+    ErrBind eb_(st);
     double r[2];
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -1475,6 +1557,7 @@ int qsv_norm_sq(qsv_state *st, double *out) {
 }
 
 int qsv_prob_bit0(qsv_state *st, int k, double *out) {
+    ErrBind eb_(st);
     if (k < 0 || k >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
     double r[2];
     int rc = set_device(st->device);
@@ -1485,6 +1568,7 @@ int qsv_prob_bit0(qsv_state *st, int k, double *out) {
 }
 
 int qsv_inner(qsv_state *st, const void *other, double *re, double *im) {
+    ErrBind eb_(st);
     double r[2];
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -1495,6 +1579,7 @@ int qsv_inner(qsv_state *st, const void *other, double *re, double *im) {
 }
 
 int qsv_max_abs_diff(qsv_state *st, const void *other, double *out) {
+    ErrBind eb_(st);
     double r[2];
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -1504,6 +1589,7 @@ int qsv_max_abs_diff(qsv_state *st, const void *other, double *out) {
 }
 
 int qsv_collapse(qsv_state *st, int k, int outcome, double scale) {
+    ErrBind eb_(st);
     if (k < 0 || k >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
     int rc = set_device(st->device);
     if (rc) return rc;
@@ -1516,6 +1602,7 @@ int qsv_collapse(qsv_state *st, int k, int outcome, double scale) {
 }
 
 int qsv_scale(qsv_state *st, double scale) {
+    ErrBind eb_(st);
     int rc = set_device(st->device);
     if (rc) return rc;
     rc = materialize(st);
@@ -1527,6 +1614,7 @@ int qsv_scale(qsv_state *st, double scale) {
 }
 
 int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
+    ErrBind eb_(st);
     if (m < 1 || m > st->n) return fail(QSV_E_PARSE, "pmeasure qubit count out of range");
     for (int p = 0; p < m; ++p)
         if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "pmeasure qubit out of range");
@@ -1570,6 +1658,7 @@ int qsv_pmeasure(qsv_state *st, const int32_t *qubits, int m, double *table) {
 }
 
 int qsv_pmeasure_async(qsv_state *st, const int32_t *qubits, int m, double *device_table) {
+    ErrBind eb_(st);
     if (m < 1 || m > 4) return fail(QSV_E_UNSUPPORTED, "asynchronous pmeasure takes 1..4 qubits");
     for (int p = 0; p < m; ++p)
         if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "pmeasure qubit out of range");
@@ -1597,6 +1686,7 @@ int qsv_pmeasure_async(qsv_state *st, const int32_t *qubits, int m, double *devi
 }
 
 int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *out) {
+    ErrBind eb_(st);
     if (nq < 1 || nq > 2) return fail(QSV_E_UNSUPPORTED, "reduced density of 1 or 2 qubits only");
     for (int p = 0; p < nq; ++p)
         if (qubits[p] < 0 || qubits[p] >= st->n) return fail(QSV_E_PARSE, "qubit out of range");
@@ -1625,6 +1715,7 @@ int qsv_reduced_density(qsv_state *st, int nq, const int32_t *qubits, double *ou
 
 int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits,
                                const double *mats, int nk, const int32_t *next_qubits) {
+    ErrBind eb_(st);
     const int nsub = st->n - batch_log2;
     if (batch_log2 < 0 || nsub < 1 || batch_log2 > 16) return fail(QSV_E_PARSE, "bad batch size");
     if (nsub > 31) return fail(QSV_E_UNSUPPORTED, "trajectories of at most 31 qubits per batch block");
@@ -1716,6 +1807,7 @@ int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int3
 }
 
 int qsv_noisy_batch_wait(qsv_state *st, int batch_log2, double *rdm_out) {
+    ErrBind eb_(st);
     int rc = set_device(st->device);
     if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(st->stream));
@@ -1727,12 +1819,14 @@ int qsv_noisy_batch_wait(qsv_state *st, int batch_log2, double *rdm_out) {
 
 int qsv_noisy_batch_step(qsv_state *st, int batch_log2, int gk, const int32_t *gate_qubits, const double *mats,
                          int nk, const int32_t *next_qubits, double *rdm_out) {
+    ErrBind eb_(st);
     const int rc = qsv_noisy_batch_step_async(st, batch_log2, gk, gate_qubits, mats, nk, next_qubits);
     if (rc) return rc;
     return qsv_noisy_batch_wait(st, batch_log2, nk ? rdm_out : nullptr);
 }
 
 int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint64_t row_len, void *host_out) {
+    ErrBind eb_(st);
     if (n_rows < 0 || n_rows > 65535) return fail(QSV_E_PARSE, "1..65535 rows per gather");
     if (n_rows == 0 || row_len == 0) return QSV_OK;
     for (int r = 0; r < n_rows; ++r)
@@ -1757,6 +1851,7 @@ int qsv_gather_rows(qsv_state *st, const uint64_t *row_offsets, int n_rows, uint
 }
 
 int qsv_upload_strided(qsv_state *st, const void *host, uint64_t offset, uint64_t count, uint64_t stride) {
+    ErrBind eb_(st);
     if (count == 0) return QSV_OK;
     if (stride == 0 || offset + (count - 1) * stride >= st->size()) return fail(QSV_E_PARSE, "strided upload out of bounds");
     int rc = set_device(st->device);

@@ -1583,8 +1583,8 @@ Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int 
     Plan P5 = build_plan(recs, n, m, r, L, s);
     static const bool off = std::getenv("QSV_MIXED_R") && std::atoi(std::getenv("QSV_MIXED_R")) == 0;
     if (off || !auto_r || r != 5 || P5.s != P5.m || P5.passes.empty()) return P5;
-    Plan P4 = build_plan(recs, n, m, 4, L, s);
-    if (P4.pass_gates != P5.pass_gates || P4.passes.size() != P5.passes.size()) return P5;
+    // the same tiles and gate sets re-staged with r = 4 (no second tile planning)
+    Plan P4 = rebuild_with_pass_r(P5, std::vector<int>(P5.passes.size(), 4));
     const int np = (int)P5.passes.size();
     std::vector<int> rs(np, 5);
     int n4 = 0;

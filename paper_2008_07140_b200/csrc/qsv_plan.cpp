@@ -17,6 +17,8 @@
 #include "qsv_plan.h"
 
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <bit>
 #include <cstdlib>
 #include <cstring>
@@ -462,16 +464,39 @@ uint64_t lookahead_tile(const std::vector<GateRec> &recs, const std::vector<int>
     }
     std::stable_sort(cands.begin() + 1, cands.end(), [](auto &x, auto &y) { return x.first > y.first; });
     if ((int)cands.size() > K) cands.resize(K);
+    // the rollouts are independent: run them on up to 16 host threads, each capped
+    // by the best completion found so far (a capped rollout returns cap + 1, which
+    // never wins), then pick in candidate order - the same choice as a serial scan
+    std::vector<int> passes(cands.size(), 1 << 30);
+    std::atomic<int> best_so_far{1 << 30};
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t k; (k = next.fetch_add(1)) < cands.size();) {
+            std::vector<int> t, d;
+            scan_fixed_tile(recs, rem, cands[k].second, &t, &d);
+            const int p = rollout_passes(recs, d, fixed, all, n, m, best_so_far.load());
+            passes[k] = p;
+            for (int cur = best_so_far.load(); p < cur && !best_so_far.compare_exchange_weak(cur, p);) {
+            }
+        }
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t nt = std::min<size_t>(hw, cands.size());
+    if (nt <= 1) {
+        work();
+    } else {
+        std::vector<std::thread> pool;
+        for (size_t t = 0; t < nt; ++t) pool.emplace_back(work);
+        for (auto &th : pool) th.join();
+    }
     uint64_t choice = best;
     int best_passes = 1 << 30, choice_count = -1;
-    for (auto &c : cands) {
-        std::vector<int> t, d;
-        scan_fixed_tile(recs, rem, c.second, &t, &d);
-        const int p = rollout_passes(recs, d, fixed, all, n, m, best_passes);
-        if (p < best_passes || (p == best_passes && c.first > choice_count)) {
+    for (size_t k = 0; k < cands.size(); ++k) {
+        const int p = passes[k];
+        if (p < best_passes || (p == best_passes && cands[k].first > choice_count)) {
             best_passes = p;
-            choice = c.second;
-            choice_count = c.first;
+            choice = cands[k].second;
+            choice_count = cands[k].first;
         }
     }
     return choice;

@@ -74,7 +74,7 @@ class StateVector:
     @property
     def device_ptr(self) -> int:
         p = C.c_void_p()
-        N.check(N.lib().qsv_device_ptr(self._h, C.byref(p)))
+        N.check(N.lib().qsv_device_ptr(self._h, C.byref(p)), self._h)
         return p.value
 
     @property
@@ -93,34 +93,34 @@ class StateVector:
         values = np.ascontiguousarray(values, dtype=np.complex128)
         if values.size != 1 << self.qubit_count:
             raise ValueError(f"expected {1 << self.qubit_count} amplitudes, got {values.size}")
-        N.check(N.lib().qsv_upload(self._h, values.ctypes.data, 0, values.size))
+        N.check(N.lib().qsv_upload(self._h, values.ctypes.data, 0, values.size), self._h)
 
     def download(self, out: np.ndarray, offset: int = 0) -> np.ndarray:
         assert out.dtype == np.complex128 and out.flags.c_contiguous
-        N.check(N.lib().qsv_download(self._h, out.ctypes.data, offset, out.size))
+        N.check(N.lib().qsv_download(self._h, out.ctypes.data, offset, out.size), self._h)
         return out
 
     def set_basis(self, index: int) -> None:
-        N.check(N.lib().qsv_set_basis(self._h, int(index)))
+        N.check(N.lib().qsv_set_basis(self._h, int(index)), self._h)
 
     def synchronize(self) -> None:
-        N.check(N.lib().qsv_synchronize(self._h))
+        N.check(N.lib().qsv_synchronize(self._h), self._h)
 
     # -- readout ------------------------------------------------------------
     def norm_sq(self) -> float:
         out = C.c_double()
-        N.check(N.lib().qsv_norm_sq(self._h, C.byref(out)))
+        N.check(N.lib().qsv_norm_sq(self._h, C.byref(out)), self._h)
         return out.value
 
     def inner(self, other: "StateVector") -> complex:
         """<self|other> computed on the device."""
         re, im = C.c_double(), C.c_double()
-        N.check(N.lib().qsv_inner(self._h, C.c_void_p(other.device_ptr), C.byref(re), C.byref(im)))
+        N.check(N.lib().qsv_inner(self._h, C.c_void_p(other.device_ptr), C.byref(re), C.byref(im)), self._h)
         return complex(re.value, im.value)
 
     def max_abs_diff(self, other: "StateVector") -> float:
         out = C.c_double()
-        N.check(N.lib().qsv_max_abs_diff(self._h, C.c_void_p(other.device_ptr), C.byref(out)))
+        N.check(N.lib().qsv_max_abs_diff(self._h, C.c_void_p(other.device_ptr), C.byref(out)), self._h)
         return out.value
 
     def reduced_density(self, qubits) -> np.ndarray:
@@ -128,7 +128,7 @@ class StateVector:
         d = 1 << len(qubits)
         out = np.empty((d, d), dtype=np.complex128)
         q = np.asarray(qubits, dtype=np.int32)
-        N.check(N.lib().qsv_reduced_density(self._h, len(qubits), q.ctypes.data, out.ctypes.data))
+        N.check(N.lib().qsv_reduced_density(self._h, len(qubits), q.ctypes.data, out.ctypes.data), self._h)
         return out
 
 
@@ -151,7 +151,7 @@ def init_state(n: int, *, chunk_log2: int | None = None, max_qubits: int = DEFAU
 
 def _apply_gate(state: StateVector, u, targets, controls=()) -> None:
     rec = N.gate_records([(np.asarray(u, dtype=np.complex128), tuple(targets), tuple(controls))])
-    N.check(N.lib().qsv_apply_gate(state.handle, rec.ctypes.data))
+    N.check(N.lib().qsv_apply_gate(state.handle, rec.ctypes.data), state.handle)
 
 
 def apply_single_qubit(state, u, k, pool=None) -> None:
@@ -181,7 +181,7 @@ def apply_projector(state, p, k, pool=None) -> None:
 
 def probability_bit0(state: StateVector, k: int) -> float:
     out = C.c_double()
-    N.check(N.lib().qsv_prob_bit0(state.handle, int(k), C.byref(out)))
+    N.check(N.lib().qsv_prob_bit0(state.handle, int(k), C.byref(out)), state.handle)
     return out.value
 
 
@@ -201,7 +201,7 @@ def pmeasure(state: StateVector, qubits) -> np.ndarray:
     """Probability table over the listed qubits, first listed = MSB; state untouched."""
     q = np.asarray(tuple(qubits), dtype=np.int32)
     table = np.empty(1 << q.size, dtype=np.float64)
-    N.check(N.lib().qsv_pmeasure(state.handle, q.ctypes.data, int(q.size), table.ctypes.data))
+    N.check(N.lib().qsv_pmeasure(state.handle, q.ctypes.data, int(q.size), table.ctypes.data), state.handle)
     return table
 
 
@@ -274,7 +274,7 @@ def _flush(state, batch, options, stats) -> None:
         return
     rec = compile_gates(batch)
     st = N.qsv_run_stats()
-    N.check(N.lib().qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(options), C.byref(st)))
+    N.check(N.lib().qsv_run(state.handle, rec.ctypes.data, len(rec), C.byref(options), C.byref(st)), state.handle)
     for k, v in st.as_dict().items():
         stats[k] = stats.get(k, 0) + v
     batch.clear()

@@ -76,10 +76,24 @@ def gaussian_state(n: int, seed: int = 0, chunk: int = 1 << 24) -> np.ndarray:
         for s in range(0, size, chunk):
             e = min(size, s + chunk)
             view[s:e, part] = rng.standard_normal(e - s)
-    # pairwise (numpy) sum of squares, then one scale
-    norm = math.sqrt(float(np.sum(view * view, dtype=np.float64)))
-    out /= norm
+    # pairwise (numpy) sum of squares per chunk, chunks added exactly (fsum): no
+    # state-sized temporary at n = 30 (a single chunk below 2^24 amplitudes)
+    big = 1 << 26
+    norm = math.sqrt(math.fsum(float(np.sum(view[s:s + big] * view[s:s + big], dtype=np.float64))
+                               for s in range(0, size, big)))
+    for s in range(0, size, big):
+        out[s:s + big] /= norm
     return out
+
+
+def mirror_text(text: str) -> str:
+    """C followed by DAGGER C ENDDAGGER (program.py:328-333): the identity circuit
+    used as a size-independent known answer (|0..0> -> |0..0>)."""
+    lines = [ln for ln in text.splitlines() if ln.strip() and not ln.lstrip().startswith("%")]
+    head, body = lines[0], lines[1:]
+    if not head.startswith("QINIT"):
+        raise ValueError("mirror_text: program must start with QINIT")
+    return "\n".join([head] + body + ["DAGGER"] + body + ["ENDDAGGER"]) + "\n"
 
 
 # --------------------------------------------------------------------------

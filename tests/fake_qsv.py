@@ -148,3 +148,6 @@ class FakeLib:
 
     def qsv_last_error(self):
         return b""
+
+    def qsv_state_last_error(self, h):
+        return b""
