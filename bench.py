@@ -5,18 +5,22 @@
 Metric: amplitude-gate updates/s = G * 2^n / time, G = gate instructions of
 the expanded program.  Workload at N=1: BASELINE config 2 -
 the 30-qubit 5x6 grid RQC, 24 cycles, eight cycled CZ patterns, seed 0
-(16 GiB complex128 state, fused schedule).  A step = reset to |0..0> and run
-the whole circuit.  Inputs (the 16 GiB state) are far larger than the 126 MB
-L2, so no explicit flush is needed between steps.
+(16 GiB complex128 state, fused schedule with the product-state start).  A
+step = reset to |0..0> and run the whole circuit.  Inputs (the 16 GiB state)
+are far larger than the 126 MB L2, so no explicit flush is needed between steps.
 
 `value` is device-timed with the state resident in HBM (CUDA events on the
 engine's stream, barrier + synchronize around the K timed steps, max over
-ranks).  `e2e` is the same metric through the public API `run_full(program)`
-with the gate records uploaded and the full 2^n amplitude vector downloaded
-to pinned host memory inside the timed region.
+ranks).  `e2e` is the same metric through the public API (statevector.run_batch:
+program text in, the full 2^n amplitude vector downloaded to pinned host memory
+inside the timed region); `e2e.cold` is the first call on an unseen circuit
+(planning + kernel compilation included).
 
-N > 1 (torchrun): the path is sharded by global qubits (n = 30 + log2 N, weak
-scaling); see paper_2008_07140_b200/distributed.py.
+N > 1 (torchrun): the state is sharded by global qubits (distributed.py).
+Weak scaling (default): 2^30 amplitudes per GPU, n = 30 + log2 N (N = 1 is C2
+itself, so `--gpus 1,2,4,8` is one ladder); `--local-qubits 32` gives BASELINE
+C3's 64 GiB shards (n = 32 + log2 N); `--strong` fixes n (= --qubits, 32) for
+every N, its N = 1 point being `--gpus 1 --strong`.
 
 `--impl reference` times the reference CPU algorithm (the oracle port,
 oracle/qsv_oracle.c, a restatement of qcsim/statevector.py) on the host
@@ -72,7 +76,7 @@ def ncu_traffic(args, passes: int):
     exe = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
     if not os.path.exists(exe):
         return None, "ncu not found"
-    fwd = ["--workload", args.workload]
+    fwd = ["--workload", args.workload, "--product", str(args.product), "--jit", str(args.jit)]
     for flag, v in (("--qubits", args.qubits), ("--tile", args.tile), ("--regs", args.regs),
                     ("--low", args.low), ("--super", args.super)):
         if v:
@@ -176,7 +180,15 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("QSV_SHARE_GPU"):  # tests: every rank on GPU 0 (no kernel waits on another rank)
+        local = 0
     return rank, world, local
+
+
+def workloads_rqc(n: int, seed: int) -> str:
+    from paper_2008_07140_b200 import workloads
+
+    return workloads.rqc_text(*C2, seed=seed) if n == N_BASE else workloads.rqc_for_qubits(n, C2[2], seed)
 
 
 def workload(n: int, kind: str = "rqc"):
@@ -197,7 +209,33 @@ def workload(n: int, kind: str = "rqc"):
 # --------------------------------------------------------------------------
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def gate_sample(prog, stride: int):
+    """Every stride-th gate of the whole circuit: the sample keeps the circuit's gate
+    mix (H layer, CZ patterns, RX/RY/T) instead of its first cycle only."""
+    insts = [i for i in prog.instructions if i.is_gate]
+    return insts[::max(1, stride)], len(insts)
+
+
+def _mix(insts) -> str:
+    from collections import Counter
+
+    return ", ".join(f"{k} {v}" for k, v in sorted(Counter(i.name for i in insts).items()))
+
+
 def cpu_reference_sample(prog, budget_s: float, threads: int | None = None) -> dict:
+    """The oracle port (oracle/qsv_oracle.c, restating qcsim/statevector.py:73-247
+    with pthreads = WorkerPool) on a strided gate sample of the whole circuit, the
+    stride chosen from a 3-gate calibration so the sample takes about `budget_s`."""
     from oracle import oracle as O
 
     threads = threads or O.cpu_threads()
@@ -205,20 +243,61 @@ def cpu_reference_sample(prog, budget_s: float, threads: int | None = None) -> d
     st = O.init_state(n, workers=threads, max_qubits=n)
     st.amplitudes[:] = 0  # first touch outside the timed region
     st.amplitudes[0] = 1
-    insts = [i for i in prog.instructions if i.is_gate]
-    done = 0
+    allg = [i for i in prog.instructions if i.is_gate]
+    t0 = time.perf_counter()
+    for inst in (allg[0], allg[len(allg) // 2], allg[-1]):
+        O.apply_instruction(st, inst, workers=threads)
+    per_gate = (time.perf_counter() - t0) / 3
+    stride = max(1, math.ceil(len(allg) * per_gate / max(budget_s, 1e-3)))
+    sample, total = gate_sample(prog, stride)
+    t0 = time.perf_counter()
+    for inst in sample:
+        O.apply_instruction(st, inst, workers=threads)
+    dt = time.perf_counter() - t0
+    del st
+    return {"value": len(sample) * float(1 << n) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"gates at stride {stride} over the whole n={n} circuit: {len(sample)} of {total} gates ({_mix(sample)}), "
+                      f"{dt:.1f} s, oracle/qsv_oracle.c restating qcsim/statevector.py:73-247, "
+                      f"{threads} threads = WorkerPool({threads}) on {cpu_model()}",
+            "seconds": dt, "gates": len(sample), "stride": stride}
+
+
+def qcsim_reference_sample(text: str, stride: int, threads: int) -> dict | None:
+    """The reference itself (qcsim, numba kernels, installed unmodified in
+    baseline/_ref) on the same strided gate sample: its `apply_instruction`
+    (statevector.py:360-394) over a WorkerPool(threads) state, after a small warm-up
+    run that JIT-compiles the numba kernels.  None when it cannot be imported."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "qcsim").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/qsv_numba_cache")
+    sys.path.insert(0, str(ref))
+    try:
+        from qcsim import statevector as QS
+        from qcsim.parallel import WorkerPool
+        from qcsim.program import parse_program as qparse
+    except Exception as e:  # noqa: BLE001 - report why the second figure is missing
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    finally:
+        sys.path.remove(str(ref))
+    prog = qparse(text)
+    n = prog.qubit_count
+    pool = WorkerPool(threads)
+    small = qparse("QINIT 12\n" + "\n".join(f"H {q}\nCZ {q},{(q + 1) % 12}\nRX {q},\"pi/2\"\nT {q}\n"
+                                             f"SWAP {q},{(q + 5) % 12}" for q in range(12)) + "\n")
+    QS.run_full(small, pool=pool, workers=threads)  # numba JIT outside the timed region
+    st = QS.init_state(n, chunk_log2=QS.default_chunk_log2(n, threads), max_qubits=n)
+    st.amplitudes[:] = 0
+    st.amplitudes[0] = 1
+    insts = [i for i in prog.instructions if i.name not in ("MEASURE", "PMEASURE")][::max(1, stride)]
     t0 = time.perf_counter()
     for inst in insts:
-        O.apply_instruction(st, inst, workers=threads)
-        done += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
+        QS.apply_instruction(st, inst, pool)
     dt = time.perf_counter() - t0
-    return {"value": done * float(1 << n) / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {done} of {len(insts)} gates of the n={n} config-2 RQC "
-                      f"({dt:.1f} s, oracle/qsv_oracle.c restating qcsim/statevector.py:73-247, "
-                      f"{threads} threads = WorkerPool({threads}))",
-            "seconds": dt, "gates": done}
+    del st
+    return {"value": len(insts) * float(1 << n) / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"qcsim (baseline/_ref, numba) apply_instruction on the same stride-{stride} gate sample: "
+                      f"{len(insts)} gates, {dt:.1f} s, WorkerPool({threads})"}
 
 
 def run_reference(args) -> None:
@@ -228,7 +307,7 @@ def run_reference(args) -> None:
     from oracle import oracle as O
 
     n = N_BASE
-    _, prog = workload(n)
+    text, prog = workload(n)
     threads = O.cpu_threads()
     per_step = args.ref_step_seconds
     vals = []
@@ -238,13 +317,16 @@ def run_reference(args) -> None:
             vals.append(r)
     value = statistics.median(v["value"] for v in vals)
     ms = statistics.median(v["seconds"] for v in vals) * 1e3
+    qc = None if args.no_qcsim else qcsim_reference_sample(text, vals[-1]["stride"], threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
         "config": {"workload": f"C2: RQC 5x6 grid, 24 cycles, n={n}, seed {SEED} (bounded CPU sample)",
-                   "n_qubits": n, "gates": len(prog.gate_instructions())},
+                   "n_qubits": n, "gates": len(prog.gate_instructions()), "cpu_model": cpu_model(),
+                   "workers": threads},
         "cpu_baseline": {k: vals[-1][k] for k in ("kind", "cores", "sample")} | {"value": value, "unit": UNIT},
+        "qcsim_numba": qc,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -285,15 +367,15 @@ def run_traj(args) -> None:
                                dedup=args.dedup, batch_clean=bc, options=topts)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-    tot = torch.tensor([float(rep.gate_updates), float(rep.unique_runs), dt], dtype=torch.float64)
+    # rank 0's report holds the whole batch (run_trajectories gathers the per-trajectory
+    # tables there); the time is the max over ranks
     if world > 1:
         import torch.distributed as dist
 
-        tt = tot.cuda()
-        dist.all_reduce(tt[:2])
-        dist.all_reduce(tt[2:], op=dist.ReduceOp.MAX)
-        tot = tt.cpu()
-    updates, unique, dt = float(tot[0]), int(tot[1]), float(tot[2])
+        tt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    updates, unique = float(rep.gate_updates), int(rep.unique_runs)
     if rank == 0:
         line = {"metric": METRIC, "value": updates / dt, "unit": UNIT, "n_gpus": world, "steps": 1,
                 "warmup": 1, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -497,6 +579,175 @@ def run_noisy_bench(args) -> None:
         dist.destroy_process_group()
 
 
+def sharded_qubits(args, world: int) -> int:
+    """Workload ladder.  Weak scaling (default): n_local = --local-qubits (30) on every
+    GPU, n = n_local + log2 N - N = 1 is C2 itself.  Strong scaling (--strong): n =
+    --qubits (32) on every N."""
+    g = world.bit_length() - 1
+    if args.strong:
+        return args.qubits or 32
+    return (args.local_qubits or N_BASE) + g
+
+
+def run_sharded(args) -> None:
+    """`bench.py --gpus N` under torchrun (N > 1): the state sharded over N GPUs by its
+    top log2 N qubits (paper_2008_07140_b200/distributed.py), global<->local qubit
+    swaps fused into the last pass's stores over CUDA-IPC-mapped peer memory (NVLink).
+    Timed steps: set_basis(0) + the whole circuit, CUDA events on each rank's
+    compute stream between barriers + synchronize, max over ranks.  One extra
+    profiled step (after the timed region) gives the per-GPU HBM roofline and the
+    exchange-out pass time; e2e = the same run through ShardedSimulator.run plus
+    every rank's download of its shard into pinned host memory."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2008_07140_b200 import _native as N
+    from paper_2008_07140_b200.distributed import CudaShard, ShardedSimulator, make_transport
+    from paper_2008_07140_b200.program import parse_program
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    # QSV_DIST_BACKEND=gloo (tests: several ranks sharing one GPU, which NCCL refuses);
+    # the bookkeeping tensors then live on the host
+    backend = os.environ.get("QSV_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    else:
+        dist.init_process_group(backend)
+    dev = f"cuda:{local}" if backend == "nccl" else "cpu"
+    g = world.bit_length() - 1
+    n = sharded_qubits(args, world)
+    nl = n - g
+    text = workloads_rqc(n, SEED)
+    prog = parse_program(text)
+    G = len(prog.gate_instructions())
+    opts = N.options(tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low)
+    shard = CudaShard(nl, local, options=opts)
+    shard.reduce_device = dev
+    kind = os.environ.get("QSV_TRANSPORT", "p2p")
+    transport = make_transport(kind, dist, shard)
+    sim = ShardedSimulator(n, shard, transport=transport)
+
+    def step(stats=None):
+        sim.set_basis(0)
+        sim.run(prog, stats)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sim.stats.swaps.clear()
+    timed = {}
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record(shard.stream)
+        for _ in range(args.steps):
+            step(timed)
+        ev1.record(shard.stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms.item())
+    swaps = list(sim.stats.swaps)
+    # profiled step: per-launch times -> per-GPU HBM roofline and the exchange-out pass
+    shard.options.profile = 1
+    prof = {}
+    step(prof)
+    torch.cuda.synchronize()
+    shard.options.profile = 0
+    pk = peaks()
+    mine = torch.tensor([prof.get("algorithmic_bytes", 0.0), prof.get("kernel_ms", 0.0),
+                         float(timed.get("launches", 0))], dtype=torch.float64, device=dev)
+    allr = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allr, mine)
+    per_gpu = [(float(a[0]) / (float(a[1]) / 1e3) / 1e9) if float(a[1]) > 0 else None for a in allr]
+    xfer = {"swaps_per_step": len(swaps) / max(1, args.steps),
+            "fused_exchanges_per_step": sum(x.fused for x in swaps) / max(1, args.steps),
+            "swap_bytes_per_rank_per_step": sum(x.bytes_sent for x in swaps) / max(1, args.steps),
+            "nvlink_peak_gbs": 900.0}
+    lf = getattr(transport, "last_fused", None)
+    if lf is not None:
+        x_ms, others = lf
+        t = torch.tensor([x_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sent = next((x.bytes_sent for x in reversed(swaps) if x.fused), None)
+        if sent:
+            gbs = sent / (float(t.item()) / 1e3) / 1e9
+            xfer |= {"exchange_pass_ms": float(t.item()),
+                     "other_pass_ms_median": statistics.median(others) if others else None,
+                     "exchange_bytes_per_rank": sent, "nvlink_gbs_per_rank": gbs, "nvlink_frac": gbs / 900.0,
+                     "nvlink_note": "remote bytes of the fused exchange-out pass / that pass's duration "
+                                    "(the pass also computes: a lower bound on the link rate)"}
+    elif kind == "p2p" and swaps and not all(x.fused for x in swaps):
+        t = torch.tensor([transport.exchange_ms()], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        last = swaps[-1].bytes_sent
+        xfer |= {"last_exchange_ms": float(t.item()), "last_exchange_bytes_per_rank": last,
+                 "nvlink_gbs_per_rank": last / (float(t.item()) / 1e3) / 1e9,
+                 "nvlink_frac": last / (float(t.item()) / 1e3) / 1e9 / 900.0}
+    # end to end through the public API: run + every rank downloads its shard (pinned)
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(1 << nl, dtype=torch.complex128, pin_memory=True)
+        times = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            step()
+            with torch.cuda.stream(shard.stream):
+                host.copy_(shard.buf, non_blocking=True)
+            shard.stream.synchronize()
+            times.append(time.perf_counter() - t0)
+        tt = torch.tensor([min(times)], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": G * float(1 << n) / float(tt.item()), "unit": UNIT, "ms_per_step": float(tt.item()) * 1e3,
+               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": (1 << nl) * 16 * world,
+               "api": "ShardedSimulator.run(program) + every rank's shard -> pinned host (host wall clock, max over ranks)"}
+        del host
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        _, cprog = workload(N_BASE)
+        cpu = cpu_reference_sample(cprog, min(args.cpu_seconds, 10.0))
+        cpu.pop("seconds", None)
+        cpu.pop("gates", None)
+    dist.barrier()
+    clocks = clk.summary()
+    if rank == 0:
+        ok = [x for x in per_gpu if x]
+        line = {
+            "metric": METRIC, "value": G * float(1 << n) / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "c128 (f64)",
+            "data": "synthetic",
+            "config": {"workload": (f"C3 {'strong' if args.strong else 'weak'} scaling: RQC n={n} on grid "
+                                    f"{workloads_grid(n)}, 24 cycles, seed {SEED}"),
+                       "n_qubits": n, "n_local": nl, "gates": G, "parallelism": f"sharded x{world} (top {g} qubits global)",
+                       "transport": kind, "chunks": 1 << sim.chunk_log2, **xfer,
+                       "l2": f"shard ({16 << nl >> 30} GiB) >> 126 MB L2: no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": statistics.mean(ok) if ok else None, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": statistics.mean(ok) / pk["hbm_gbs"] if ok else None,
+                         "per_gpu_gbs": per_gpu, "traffic": None, "peak_src": pk["src"],
+                         "kernel": "qsv_pass (specialised fused pass, incl. exchange-out passes)",
+                         "note": "per GPU: algorithmic bytes / event-timed kernel ms of one profiled step"},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(max(float(a[2]) for a in allr)),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    transport.close() if hasattr(transport, "close") else None
+    dist.destroy_process_group()
+
+
+def workloads_grid(n: int):
+    from paper_2008_07140_b200 import workloads
+
+    return workloads.grid_shape(n)
+
+
 def run_gpu(args) -> None:
     rank, world, local = dist_env()
     if args.workload == "traj":
@@ -509,9 +760,7 @@ def run_gpu(args) -> None:
         run_noisy_bench(args)
         return
     if world > 1:
-        from paper_2008_07140_b200 import distributed
-
-        distributed.bench_main(args)
+        run_sharded(args)
         return
 
     import torch
@@ -520,14 +769,19 @@ def run_gpu(args) -> None:
     from paper_2008_07140_b200 import statevector as SV
 
     torch.cuda.set_device(local)
-    n = args.qubits or N_BASE
+    n = (args.qubits or 32) if args.strong else (args.qubits or N_BASE)
     text, prog = workload(n, args.workload)
     gates_list = prog.gate_instructions()
     G = len(gates_list)
     rec = SV.compile_gates(gates_list)
     L = N.lib()
+    # RQC steps start from |0..0> (set_basis): the plan takes the product-state start
+    # (leading single-qubit gates synthesised by the first pass), as qsv_run does for
+    # run_full; the QFT round trip starts from an uploaded state
+    product = 1 if (args.product and args.workload == "rqc" and not args.unfused and args.jit >= 0) else -1
     opts = N.options(fuse=not args.unfused, tile_qubits=args.tile, reg_qubits=args.regs,
-                     low_qubits=args.low, profile=True, super_qubits=args.super)
+                     low_qubits=args.low, profile=True, super_qubits=args.super, jit=args.jit,
+                     product_start=product)
 
     stream = torch.cuda.Stream(device=local)
     state = SV.init_state(n, max_qubits=n, device=local, stream=stream.cuda_stream)
@@ -618,7 +872,7 @@ def run_gpu(args) -> None:
         hosts = [torch.empty(1 << n, dtype=torch.complex128, pin_memory=True) for _ in range(2)]
         outs = [h.numpy() for h in hosts]
         states = [state, SV.init_state(n, max_qubits=n, device=local)]
-        kw = dict(max_qubits=n, tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low,
+        kw = dict(max_qubits=n, tile_qubits=args.tile, reg_qubits=args.regs, low_qubits=args.low, jit=args.jit,
                   fuse=not args.unfused, initial_state=psi0, device=local, states=states)
         SV.run_batch([text, text], outs, **kw)  # warm-up: plan cache, specialised kernels
         K = args.e2e_steps
@@ -635,6 +889,29 @@ def run_gpu(args) -> None:
                         "gates reach the device as specialised-kernel code (cached per circuit), the "
                         "|0..0> input is synthesised by the first pass (no host buffer to copy); "
                         "downloads overlap the next step's passes (host wall clock over K steps)")}
+        # COLD end to end: the first call on a circuit this process has never seen (same
+        # C2 construction, another seed; the on-disk kernel cache is off, QSV_CACHE_DIR=0):
+        # parse + look-ahead planning + kernel specialisation/NVRTC + passes + download
+        if args.workload == "rqc" and not args.unfused:
+            cold = []
+            for k in range(args.cold_steps):
+                ctext = workloads_rqc(n, SEED + 1000 + k)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = SV.run_batch([ctext], [outs[0]], **kw)
+                torch.cuda.synchronize()
+                cold.append((time.perf_counter() - t0) * 1e3)
+                st = res[0].stats
+                cold_plan = st.get("plan_ms", 0.0)
+                cold_jit = st.get("jit_ms", 0.0)
+            cms = statistics.median(cold)
+            e2e["cold"] = {"value": G * float(1 << n) / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
+                           "ms_each": [round(c, 1) for c in cold], "plan_ms_last": cold_plan,
+                           "jit_ms_last": cold_jit, "vs_warm": cms / e2e_t,
+                           "h2d_bytes_per_step": 0, "d2h_bytes_per_step": (1 << n) * 16,
+                           "note": "first run_batch call on an unseen circuit (C2 construction, seeds "
+                                   f"{SEED + 1000}..{SEED + 999 + args.cold_steps}), QSV_CACHE_DIR=0: parse, "
+                                   "planning, kernel specialisation + NVRTC, passes, 16 GiB download"}
         states[1].close()
         del hosts, outs
     cpu = None
@@ -668,6 +945,7 @@ def run_gpu(args) -> None:
                    "stages": int(info.stages), "tile_qubits": int(info.tile_qubits),
                    "super_passes": int(info.super_passes), "super_qubits": int(info.super_qubits),
                    "reg_qubits": int(info.reg_qubits), "low_qubits": int(info.low_qubits),
+                   "product_start": bool(info.product_start),
                    "l2": f"state ({16 << n >> 30} GiB) >> 126 MB L2: no flush needed", "parallelism": "single GPU"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(launches),  # fused pass kernels (|0..0> is synthesised by the first pass)
@@ -677,12 +955,17 @@ def run_gpu(args) -> None:
 
 
 def main():
+    # the on-disk kernel cache stays off in the bench: every specialised kernel of a
+    # circuit is compiled by this process (the cold e2e number depends on it)
+    os.environ.setdefault("QSV_CACHE_DIR", "0")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--qubits", type=int, default=0)
+    ap.add_argument("--qubits", type=int, default=0, help="total qubits (N=1, or with --strong)")
+    ap.add_argument("--local-qubits", type=int, default=0, help="weak scaling: qubits per GPU (default 30)")
+    ap.add_argument("--strong", action="store_true", help="fixed total n (--qubits, default 32) for every N")
     ap.add_argument("--workload", default="rqc", choices=("rqc", "qft", "traj", "partial", "noisy"))
     ap.add_argument("--trajectories", type=int, default=1024)
     ap.add_argument("--dedup", action="store_true")
@@ -693,15 +976,21 @@ def main():
     ap.add_argument("--low", type=int, default=0)
     ap.add_argument("--super", type=int, default=0, help="L2 super-tile qubits (0 = default)")
     ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--jit", type=int, default=0, help="pass kernels: 0 auto, 1 specialised, -1 interpreted")
+    ap.add_argument("--cold-steps", type=int, default=3)
+    ap.add_argument("--product", type=int, default=1, help="1: product-state start for basis-state runs, 0: off")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=12.0)
+    ap.add_argument("--no-qcsim", action="store_true", help="reference arm: skip the qcsim (numba) figure")
     ap.add_argument("--traffic", default="auto", choices=("auto", "off"),
                     help="auto: measure DRAM bytes per pass launch with an ncu child run of this workload")
     ap.add_argument("--traffic-timeout", type=float, default=240.0)
     args = ap.parse_args()
+    if not args.product:
+        os.environ["QSV_PRODUCT_START"] = "0"  # run_full / run_batch (qsv_run's automatic choice)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -77,6 +77,11 @@ typedef struct qsv_options {
     int32_t jit;         /* pass kernels: 0 auto (specialise when n >= 16), 1 always, -1 never
                             (specialised = runtime-generated CUDA compiled with NVRTC for sm_100a) */
     int32_t super_qubits; /* s: qubits of an L2-resident super-tile (2^s amplitudes; default 21) */
+    int32_t product_start; /* 1: absorb every qubit's leading single-qubit gates into a product-state
+                              start that the first pass synthesises (the plan then runs only on a
+                              state holding a pending basis index, qsv_set_basis); -1: never;
+                              0: auto - qsv_run uses it for a pending basis state with specialised
+                              kernels, qsv_plan_create does not */
 } qsv_options;
 
 typedef struct qsv_run_stats {
@@ -87,14 +92,16 @@ typedef struct qsv_run_stats {
     int64_t launches;      /* kernels launched by this call */
     double kernel_ms;      /* sum of event-timed launch durations (profile=1 only) */
     double max_launch_ms;  /* longest single launch (profile=1 only) */
-    double algorithmic_bytes; /* passes * 2 * 16 * 2^n_local */
+    double algorithmic_bytes; /* per pass 2 * 16 * 2^n_local (16 * 2^n_local when it synthesises a basis input) */
+    double plan_ms;        /* host time building schedules for this call (0 when the plan was cached) */
+    double jit_ms;         /* host time specialising + compiling (NVRTC) / loading pass kernels */
 } qsv_run_stats;
 
 typedef struct qsv_plan_info {
     int32_t n_qubits, tile_qubits, reg_qubits, low_qubits;
     int64_t gates, passes, stages, ops;
     int32_t super_qubits;
-    int32_t reserved;
+    int32_t product_start; /* 1: the plan starts from a product state (qsv_options.product_start) */
     int64_t super_passes; /* HBM passes: each streams the state once through L2 */
 } qsv_plan_info;
 
@@ -165,6 +172,9 @@ int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out);
 int qsv_plan_pass(const qsv_plan *plan, int64_t pass, qsv_pass_info *out);
 int qsv_plan_op(const qsv_plan *plan, int64_t pass, int64_t op, qsv_op_info *out);
 int qsv_plan_execute(qsv_state *st, qsv_plan *plan, const qsv_options *opt, qsv_run_stats *stats);
+/* factor tables a product-start plan's first pass reads for basis index `basis` (complex,
+ * interleaved re/im; count = entries): host code, used to run the host rendering in tests */
+int qsv_plan_product_tables(const qsv_plan *plan, uint64_t basis, double *out, int64_t cap, int64_t *count);
 
 /* source of the specialised (runtime-generated) kernel of one pass; copies at most
  * buf_size bytes (NUL-terminated) and reports the full size in *needed; host=1 renders the

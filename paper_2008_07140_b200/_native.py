@@ -36,13 +36,13 @@ class qsv_exchange(C.Structure):
 class qsv_options(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
-                ("jit", C.c_int32), ("super_qubits", C.c_int32)]
+                ("jit", C.c_int32), ("super_qubits", C.c_int32), ("product_start", C.c_int32)]
 
 
 class qsv_run_stats(C.Structure):
     _fields_ = [("gates", C.c_int64), ("passes", C.c_int64), ("stages", C.c_int64),
                 ("inner_passes", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double), ("max_launch_ms", C.c_double),
-                ("algorithmic_bytes", C.c_double)]
+                ("algorithmic_bytes", C.c_double), ("plan_ms", C.c_double), ("jit_ms", C.c_double)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -52,7 +52,7 @@ class qsv_plan_info(C.Structure):
     _fields_ = [("n_qubits", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("gates", C.c_int64), ("passes", C.c_int64),
                 ("stages", C.c_int64), ("ops", C.c_int64), ("super_qubits", C.c_int32),
-                ("reserved", C.c_int32), ("super_passes", C.c_int64)]
+                ("product_start", C.c_int32), ("super_passes", C.c_int64)]
 
 
 class qsv_pass_info(C.Structure):
@@ -71,6 +71,7 @@ _SIGNATURES = {
     "qsv_last_error": ([], C.c_char_p),
     "qsv_state_last_error": ([C.c_void_p], C.c_char_p),
     "qsv_last_launches": ([_P, _P, _P, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_plan_product_tables": ([_P, C.c_uint64, _P, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "qsv_create": ([C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),
     "qsv_create_on": ([C.c_int, C.c_int, _P, _P, C.POINTER(_P)], C.c_int),
@@ -168,14 +169,17 @@ def last_launches(handle):
 
 
 def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0,
-            jit=0, super_qubits=0) -> qsv_options:
+            jit=0, super_qubits=0, product_start=0) -> qsv_options:
     """jit: 0 auto (specialised kernels for n >= 16), 1 always, -1 never;
-    super_qubits: L2 super-tile size s (0 = default 21; s <= tile_qubits disables)."""
+    super_qubits: L2 super-tile size s (0 = default 21; s <= tile_qubits disables);
+    product_start: 1 plan with a product-state start (runs only from set_basis), -1 never,
+    0 auto (qsv_run: on for basis starts with specialised kernels)."""
     o = qsv_options()
     o.fuse, o.tile_qubits, o.reg_qubits = int(bool(fuse)), int(tile_qubits), int(reg_qubits)
     o.low_qubits, o.profile, o.n_global = int(low_qubits), int(bool(profile)), int(n_global)
     o.jit = int(jit)
     o.super_qubits = int(super_qubits)
+    o.product_start = int(product_start)
     return o
 
 

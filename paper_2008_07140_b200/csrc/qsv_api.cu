@@ -6,6 +6,7 @@
 #include <map>
 
 #include <algorithm>
+#include <chrono>
 #include <bit>
 #include <cstdio>
 #include <cstring>
@@ -77,6 +78,7 @@ struct qsv_state {
     double2 *nb_mats = nullptr;  // batched noisy step: per-trajectory gate matrices + rdm out
     size_t nb_bytes = 0;
     double2 *nb_host = nullptr;  // pinned staging of the same two regions (async steps)
+    double2 *ptab = nullptr;     // factor tables of a product-start pass 0 (8 KB)
     std::string last_error;      // message of the last failed call on this handle
     // per-launch event times / algorithmic bytes of the last profiled plan execution
     std::vector<double> launch_ms, launch_bytes;
@@ -278,6 +280,21 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
             use_jit = false;  // auto mode: the interpreted pass kernel runs the same plan
         }
     }
+    const void *ptab = nullptr;
+    if (P.product) {
+        // pass 0 synthesises the product state prefix (x) e_b from the pending basis b
+        if (!use_jit) return fail(QSV_E_UNSUPPORTED, "a product-start plan needs the specialised kernels");
+        if (st->pending_basis < 0)
+            return fail(QSV_E_UNSUPPORTED, "a product-start plan runs only on a basis state (qsv_set_basis)");
+        std::vector<cd> tab;
+        product_tables(P, (uint64_t)st->pending_basis, product_regs(P), tab);
+        if (!st->ptab) CUDA_TRY(cudaMalloc(&st->ptab, 8192));
+        if (tab.size() * sizeof(cd) > 8192) return fail(QSV_E_UNSUPPORTED, "product tables too large");
+        // pageable source: staged by the driver before this call returns; stream-ordered
+        // after any earlier pass-0 launch still reading the buffer
+        CUDA_TRY(cudaMemcpyAsync(st->ptab, tab.data(), tab.size() * sizeof(cd), cudaMemcpyHostToDevice, st->stream));
+        ptab = st->ptab;
+    }
     if (!use_jit || jit_double_buffer()) {
         const int rc = materialize(st);
         if (rc) return rc;
@@ -333,7 +350,7 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
                 std::string err;
                 const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
                 if (st->pending_basis >= 0) b = 0.5 * full;
-                rc = jit_launch(P, i, st->amps, st->n, st->stream, err, basis);
+                rc = jit_launch(P, i, st->amps, st->n, st->stream, err, basis, i == 0 ? ptab : nullptr);
                 if (rc) return fail(rc, err);
                 st->pending_basis = -1;
             } else {
@@ -493,6 +510,7 @@ int qsv_destroy(qsv_state *st) {
     if (st->barrier) cudaFree(st->barrier);
     if (st->nb_mats) cudaFree(st->nb_mats);
     if (st->nb_host) cudaFreeHost(st->nb_host);
+    if (st->ptab) cudaFree(st->ptab);
     if (st->own_stream) cudaStreamDestroy(st->stream);
     delete st;
     return QSV_OK;
@@ -585,7 +603,7 @@ int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const 
     int s;
     resolve_options(opt, n_qubits, m, r, L, s);
     auto p = std::make_unique<qsv_plan>();
-    p->p = build_plan_auto(recs, n_qubits, m, r, L, s, auto_r_of(opt, n_qubits));
+    p->p = build_plan_start(recs, n_qubits, m, r, L, s, auto_r_of(opt, n_qubits), opt && opt->product_start > 0);
     *out = p.release();
     return QSV_OK;
 }
@@ -689,8 +707,22 @@ int qsv_plan_summary(const qsv_plan *plan, qsv_plan_info *out) {
     out->stages = (int64_t)P.stages.size();
     out->ops = (int64_t)P.ops.size();
     out->super_qubits = P.s;
-    out->reserved = 0;
+    out->product_start = P.product ? 1 : 0;
     out->super_passes = (int64_t)P.supers.size();
+    return QSV_OK;
+}
+
+int qsv_plan_product_tables(const qsv_plan *plan, uint64_t basis, double *out, int64_t cap, int64_t *count) {
+    if (!plan || !count) return fail(QSV_E_PARSE, "qsv_plan_product_tables: null argument");
+    const Plan &P = plan->p;
+    if (!P.product) return fail(QSV_E_UNSUPPORTED, "not a product-start plan");
+    std::vector<cd> tab;
+    product_tables(P, basis, product_regs(P), tab);
+    *count = (int64_t)tab.size();
+    for (int64_t i = 0; i < std::min(cap, *count); ++i) {
+        out[2 * i] = tab[i].real();
+        out[2 * i + 1] = tab[i].imag();
+    }
     return QSV_OK;
 }
 
@@ -771,12 +803,13 @@ struct CachedPlan {
 };
 
 std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, const std::vector<GateRec> &recs,
-                                        int n, int m, int r, int L, int s, int jit, int device, bool auto_r = false) {
+                                        int n, int m, int r, int L, int s, int jit, int device, bool auto_r = false,
+                                        bool product = false) {
     static std::mutex mu;
     static std::list<std::shared_ptr<CachedPlan>> lru;
     constexpr size_t kEntries = 16;
     std::vector<unsigned char> key(sizeof(int) * 7 + sizeof(qsv_gate) * (size_t)n_gates);
-    const int head[7] = {n, m, r + (auto_r ? 100 : 0), L, s, jit, device};
+    const int head[7] = {n, m, r + (auto_r ? 100 : 0) + (product ? 1000 : 0), L, s, jit, device};
     std::memcpy(key.data(), head, sizeof(head));
     std::memcpy(key.data() + sizeof(head), gates, sizeof(qsv_gate) * (size_t)n_gates);
     {
@@ -791,7 +824,7 @@ std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, 
     }
     auto e = std::make_shared<CachedPlan>();
     e->key.swap(key);
-    e->plan = build_plan_auto(recs, n, m, r, L, s, auto_r);
+    e->plan = build_plan_start(recs, n, m, r, L, s, auto_r, product);
     std::lock_guard<std::mutex> lk(mu);
     lru.push_front(e);
     if (lru.size() > kEntries) lru.pop_back();
@@ -836,18 +869,34 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     int m, r, L;
     int s;
     resolve_options(opt, st->n, m, r, L, s);
-    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, opt ? opt->jit : 0,
-                                                 st->device, auto_r_of(opt, st->n));
-    Plan &P = cp->plan;
+    const int jm = opt ? opt->jit : 0;
+    const bool want_jit = jm > 0 || (jm == 0 && st->n >= kJitAutoQubits);
+    // product-state start: the run begins on a pending basis state, so every qubit's
+    // leading single-qubit gates become the synthesised input of the first pass
+    static const bool product_env = !std::getenv("QSV_PRODUCT_START") || std::atoi(std::getenv("QSV_PRODUCT_START")) != 0;
+    const int ps = opt ? opt->product_start : 0;
+    const bool product = want_jit && !jit_double_buffer() && st->pending_basis >= 0 &&
+                         (ps > 0 || (ps == 0 && product_env));
+    const auto t0 = std::chrono::steady_clock::now();
+    std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, jm, st->device,
+                                                 auto_r_of(opt, st->n), product);
+    const auto t1 = std::chrono::steady_clock::now();
     bool jit_ready = false;
-    {
+    if (want_jit) {
         // first use of a cached plan: specialise its kernels once
-        const int jm = opt ? opt->jit : 0;
-        if (jm > 0 || (jm == 0 && st->n >= kJitAutoQubits)) {
-            std::lock_guard<std::mutex> lk(cp->mu);
-            std::string err;
-            jit_ready = jit_prepare(P, st->device, err) == QSV_OK;  // failures are reported by execute_plan
-        }
+        std::lock_guard<std::mutex> lk(cp->mu);
+        std::string err;
+        jit_ready = jit_prepare(cp->plan, st->device, err) == QSV_OK;  // failures are reported by execute_plan
+    }
+    if (product && !jit_ready) {
+        // no specialised kernels: the plain plan runs on the interpreted kernel
+        cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, jm, st->device, auto_r_of(opt, st->n), false);
+    }
+    Plan &P = cp->plan;
+    if (stats) {
+        const auto t2 = std::chrono::steady_clock::now();
+        stats->plan_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        stats->jit_ms += std::chrono::duration<double, std::milli>(t2 - t1).count();
     }
     // the specialised kernels carry the whole plan in their code: the device
     // op tables are only uploaded for the interpreted kernel (a pageable
@@ -1213,6 +1262,7 @@ int execute_with_paulis(qsv_state *st, Plan &P, const PauliPlacement &pl, int64_
     // the error placement runs on the plan's specialised kernels: without them (jit = -1,
     // or NVRTC unavailable) report UNSUPPORTED so callers take the explicit-gate qsv_run path
     if (opt && opt->jit < 0) return fail(QSV_E_UNSUPPORTED, "Pauli placement needs specialised kernels (jit = -1)");
+    if (P.product) return fail(QSV_E_UNSUPPORTED, "Pauli placement on a product-start plan");
     int rc = jit_prepare(P, st->device, msg);
     if (rc) return fail(QSV_E_UNSUPPORTED, "specialised kernels unavailable: " + msg);
     const std::vector<double> &sc = pass_scales(P);
@@ -1757,6 +1807,7 @@ int qsv_noisy_batch_step_async(qsv_state *st, int batch_log2, int gk, const int3
         CUDA_TRY(cudaStreamSynchronize(st->stream));
         if (st->nb_mats) cudaFree(st->nb_mats);
         if (st->nb_host) cudaFreeHost(st->nb_host);
+    if (st->ptab) cudaFree(st->ptab);
         st->nb_mats = st->nb_host = nullptr;
         st->nb_bytes = 0;
         CUDA_TRY(cudaMalloc(&st->nb_mats, need));

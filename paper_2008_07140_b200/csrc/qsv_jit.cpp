@@ -136,6 +136,12 @@ __device__ __forceinline__ double2 ldwb2(const double2 *p) {
 __device__ __forceinline__ void stwb2(double2 *p, double2 v) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+// one 128-byte line into L2 (a plain per-thread prefetch: the bulk form needs a
+// uniform address, so per-lane bulk prefetches were serialised into ~10-instruction
+// loops - 21-30 % of all issued instructions of the C2 passes, ncu r02)
+__device__ __forceinline__ void prefetch_line(const void *g) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(g));
+}
 __device__ __forceinline__ void prefetch_l2(const void *g, unsigned bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g), "r"(bytes) : "memory");
 }
@@ -1036,6 +1042,7 @@ static inline void stcs2(double2 *p, double2 v) { *p = v; }
 static inline void stwb2(double2 *p, double2 v) { *p = v; }
 static inline double2 ldwb2(const double2 *p) { return *p; }
 static inline void prefetch_l2(const void *, unsigned) {}
+static inline void prefetch_line(const void *) {}
 static inline double2 cmulc(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -1099,13 +1106,15 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
     const std::string thread_end = host ? "    }\n" : "";
     const std::string barrier = host ? "" : "    __syncthreads();\n";
     const int S = dp.stage_end - dp.stage_begin;
-    o << "  { // pass " << pi << ": " << S << " stage(s)\n";
+    // product-start plan: pass 0 synthesises its input (no read, no TMA, no prefetch)
+    const bool product = P.product && pi == 0 && !xmask;
+    o << "  { // pass " << pi << ": " << S << " stage(s)" << (product ? ", product-state input" : "") << "\n";
     o << "  const u64 ntiles = " << ntiles << ";\n";
     // gang > 1: the CTA holds `gang` tiles side by side (sub-tile `sub`), its
     // warps run every stage in lock step (one code region in flight per SM);
     // a sub-tile past the end recomputes the last tile without storing it
     const std::string guard = (!host && gang > 1) ? "if (act) " : "";
-    tma = tma && !host;
+    tma = tma && !host && !product;
     // TMA-fed tiles (QSV_JIT_TMA): the next tile (group) is brought into the
     // shared tile by bulk copies (one 2^lr-amplitude run per copy, completion
     // on an mbarrier) as soon as this tile's last shared-memory read is done,
@@ -1197,7 +1206,8 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         int run = 0;
         while (run < (int)nonreg.size() && nonreg[run] == run && tq[run] == run) ++run;
         static const int stage_min = std::getenv("QSV_JIT_STAGE_MIN") ? std::atoi(std::getenv("QSV_JIT_STAGE_MIN")) : 1;
-        const bool staged_in = !tma && first && run < stage_min, staged_out = last && run < stage_min;
+        const bool synth = product && first;  // registers synthesised from the product tables
+        const bool staged_in = !synth && !tma && first && run < stage_min, staged_out = last && run < stage_min;
         const int T = 1 << (m - R);
         std::vector<int> lowq(tq.begin(), tq.begin() + (m - R));
         std::vector<uint64_t> goffc(1u << R);
@@ -1246,14 +1256,38 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             }
             o << "    }\n" << thread_end << barrier;
         }
-        if (!staged_basis) {
+        if (synth) {
+            // product-state input: amplitude(i) = prod_q v_q[bit q of i]; the thread's
+            // factor over its non-register qubits from the 5-bit group tables (the
+            // register bits of gb are zero), then a tree over the register qubits
+            o << thread_loop;
+            if (!last || staged_out) o << "    const unsigned tsw = " << smap.tid_expr(nonreg) << ";\n";
+            o << "    const u64 gb = base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
+            if (last && !staged_out) o << "    double2 *gp = psi + gb;\n";
+            const int G = (P.n + 4) / 5;
+            o << "    double2 v0 = ptab[(unsigned)(gb & 31ull)]";
+            for (int rho = 1; rho < (1 << R); ++rho) o << ", v" << rho;
+            o << ";\n";
+            for (int gi = 1; gi < G; ++gi)
+                o << "    v0 = cmulc(v0, ptab[" << 32 * gi << "u + (unsigned)((gb >> " << 5 * gi << ") & 31ull)]);\n";
+            for (int k = 0; k < R; ++k) {
+                o << "    { const double2 w0 = ptab[" << 32 * G + 2 * k << "u], w1 = ptab[" << 32 * G + 2 * k + 1
+                  << "u];\n";
+                for (int j = 0; j < (1 << k); ++j)
+                    o << "      v" << (j + (1 << k)) << " = cmulc(v" << j << ", w1); v" << j << " = cmulc(v" << j
+                      << ", w0);\n";
+                o << "    }\n";
+            }
+            fp64 += 4.0 * (double)((G - 1) + (2 << R) - 2);
+        } else if (!staged_basis) {
         o << thread_loop;
         if (!first || !last || staged_in || staged_out)
             o << "    const unsigned tsw = " << smap.tid_expr(nonreg) << ";\n";
         if ((first && !staged_in) || (last && !staged_out))
             o << "    double2 *gp = psi + base + (" << deposit_expr("tid", nonreg_q, true) << ");\n";
         }
-        if (staged_basis) {
+        if (synth) {
+        } else if (staged_basis) {
         } else if (staged_in) {
             for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         } else if (first && tma) {
@@ -1290,7 +1324,7 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
         } else {
             for (int rho = 0; rho < (1 << R); ++rho) o << "    double2 v" << rho << " = tile[tsw ^ " << c[rho] << "u];\n";
         }
-        if (first && stream_out && !host && prefetch) {
+        if (first && stream_out && !host && prefetch && !synth) {
             // TMA bulk prefetch of this CTA's NEXT tile into L2 (contiguous runs
             // of 2^lr amplitudes), so HBM streaming overlaps this tile's math
             int lr = 0;
@@ -1305,9 +1339,13 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             else
                 o << "    { const u64 nt = t + (u64)gridDim.x * " << gang << "u;\n";
             o << "      if (nt < ntiles" << (basis_param ? " && basis == ~0ull" : "") << ")\n";
-            o << "      for (unsigned j = tid; j < " << (1u << (m - lr)) << "u; j += " << T
-              << "u) prefetch_l2(psi + (" << base_of("nt")
-              << ") + (" << deposit_expr("j", runq, true) << "), " << (16u << lr) << "u); }\n";
+            // one prefetch per 128-byte line of the next tile (runs of 2^lb amplitudes,
+            // lb = min(lr, 3): 8 amplitudes = one line when the 3 lowest qubits are resident)
+            const int lb = std::min(lr, 3);
+            std::vector<int> lineq(tq.begin() + lb, tq.end());
+            o << "      for (unsigned j = tid; j < " << (1u << (m - lb)) << "u; j += " << T
+              << "u) prefetch_line(psi + (" << base_of("nt") << ") + (" << deposit_expr("j", lineq, true)
+              << ")); }\n";
         }
         const std::string next_group = gang > 1 ? "(tg + " + step + ")" : "(t + " + step + ")";
         if (tma && last && !staged_out) {
@@ -1519,6 +1557,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
         o << "] + (((ix) & ~" << xmask << "ull) | xd.self))\n";
     }
     std::string params = host ? "double2 *__restrict__ psi, u64 n_tiles" : "double2 *__restrict__ psi, u64 n_tiles, u64 basis";
+    if (P.product && pi == 0 && !xmask) params += ", const double2 *__restrict__ ptab";
     if (xmask) params += ", XDst xd";
     if (probe) {
         gang = 1;
@@ -1610,6 +1649,32 @@ Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int 
     return rebuild_with_pass_r(P5, rs);
 }
 
+Plan build_plan_start(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r,
+                      bool product) {
+    if (product) {
+        std::vector<GateRec> kept;
+        std::vector<cd> prefix;
+        if (split_product_prefix(recs, n, kept, prefix) > 0 && !kept.empty()) {
+            Plan P = build_plan_auto(kept, n, m, r, L, s, auto_r);
+            if (P.s == P.m && !P.passes.empty()) {  // flat plans only (no L2 super-passes)
+                P.product = true;
+                P.prefix = std::move(prefix);
+                P.gates = (int64_t)recs.size();
+                return P;
+            }
+        }
+    }
+    return build_plan_auto(recs, n, m, r, L, s, auto_r);
+}
+
+std::vector<int> product_regs(const Plan &P) {
+    const DevPass &dp = P.passes[0];
+    const DevStage &st = P.stages[dp.stage_begin];
+    std::vector<int> regs(pass_r(P, 0));
+    for (int k = 0; k < (int)regs.size(); ++k) regs[k] = dp.tq[st.rb[k]];
+    return regs;
+}
+
 int super_batch(const Plan &P) {
     // super-tiles processed together: keep the batch within the L2 budget
     // (default 64 MB of the 126 MB L2; QSV_L2_BYTES overrides)
@@ -1669,6 +1734,16 @@ size_t spill_bytes(const std::string &log) {
 }
 constexpr size_t kMaxSpillBytes = 128;
 
+// QSV_NVRTC_FAST=min|mid (diagnostic): NVRTC --Ofast-compile level (cuts front-end time,
+// slightly different code); part of the disk-cache key
+const std::string &nvrtc_fast_compile() {
+    static const std::string v = [] {
+        const char *e = std::getenv("QSV_NVRTC_FAST");
+        return (e && *e) ? std::string("--Ofast-compile=") + e : std::string();
+    }();
+    return v;
+}
+
 std::string jit_compile_cubin(const std::string &src, std::string &log) {
     Nvrtc &api = nvrtc();
     if (!api.ok) {
@@ -1680,9 +1755,11 @@ std::string jit_compile_cubin(const std::string &src, std::string &log) {
         log = "nvrtcCreateProgram failed";
         return {};
     }
-    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--extra-device-vectorization",
-                          "--ptxas-options=-v", "-diag-suppress=177"};
-    const nvrtcResult rc = api.CompileProgram(prog, 7, opts);
+    std::vector<const char *> opts = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo",
+                                      "--extra-device-vectorization", "--ptxas-options=-v", "-diag-suppress=177"};
+    const std::string &fast = nvrtc_fast_compile();
+    if (!fast.empty()) opts.push_back(fast.c_str());
+    const nvrtcResult rc = api.CompileProgram(prog, (int)opts.size(), opts.data());
     size_t ls = 0;
     api.GetProgramLogSize(prog, &ls);
     log.assign(ls, '\0');
@@ -1719,7 +1796,7 @@ std::string disk_cache_path(const std::string &src) {
         int major = 0, minor = 0;
         Nvrtc &api = nvrtc();
         if (api.ok && api.Version) api.Version(&major, &minor);
-        return "sm_100a|lineinfo|xdv|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+        return "sm_100a|lineinfo|xdv|nvrtc" + std::to_string(major) + "." + std::to_string(minor) + nvrtc_fast_compile();
     }();
     uint64_t h = 1469598103934665603ull;
     for (const std::string *part : {&salt, &src})
@@ -1925,11 +2002,19 @@ int jit_variant_prepare(const Plan &P, int pass, const std::string &src, int dev
                         std::string &err);
 
 int jit_exchange_prepare(const Plan &P, int pass, uint64_t xmask, int device, void **fn, int *grid, std::string &err) {
+    if (P.product) {
+        err = "exchange-out passes of a product-start plan are not generated";
+        return QSV_E_UNSUPPORTED;
+    }
     return jit_variant_prepare(P, pass, jit_source(P, pass, false, nullptr, xmask), device, fn, grid, err);
 }
 
 int jit_probe_prepare(const Plan &P, int pass, const std::vector<int> &probe, int device, void **fn, int *grid,
                       std::string &err) {
+    if (P.product) {
+        err = "probe-out passes of a product-start plan are not generated";
+        return QSV_E_UNSUPPORTED;
+    }
     return jit_variant_prepare(P, pass, jit_source(P, pass, false, nullptr, 0, &probe), device, fn, grid, err);
 }
 
@@ -2031,7 +2116,7 @@ static int cu_fail(CUresult r, const char *what, std::string &err) {
 }
 
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
-               unsigned long long basis) {
+               unsigned long long basis, const void *ptab) {
     const DevPass &dp = P.passes[pass];
     const int m = dp.m, T = 1 << (m - pass_r(P, pass));
     unsigned long long n_tiles = 1ull << (n - m);
@@ -2044,7 +2129,11 @@ int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, s
     const bool per_tile = jit_per_tile_grid();
     const unsigned long long cap = per_tile ? 0x7fffffffull : (unsigned long long)P.jit_grids[pass];
     const unsigned grid = (unsigned)std::min<unsigned long long>((n_tiles + gang - 1) / gang, cap);
-    void *args[] = {&psi, &n_tiles, &basis};
+    if (P.product && pass == 0 && !ptab) {
+        err = "product-start pass launched without its factor tables";
+        return QSV_E_UNSUPPORTED;
+    }
+    void *args[] = {&psi, &n_tiles, &basis, &ptab};
     const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, gang * T, 1, 1,
                                              gang * (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
                                              (CUstream)stream, args, nullptr);

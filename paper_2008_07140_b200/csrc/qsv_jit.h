@@ -82,7 +82,15 @@ const std::vector<double> &pass_scales(const Plan &P);
 // ~0 means the state is the basis state |basis> and is not read (single-buffer
 // kernels synthesise the tiles; see jit_basis_fusable).
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
-               unsigned long long basis = ~0ull);
+               unsigned long long basis = ~0ull, const void *ptab = nullptr);
+
+// build_plan_auto, or with `product` a product-start plan (Plan::product) when the
+// stream has leading single-qubit gates to absorb
+Plan build_plan_start(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r,
+                      bool product);
+
+// register qubits (k = 0..R-1) of pass 0's first stage: the `regs` of product_tables
+std::vector<int> product_regs(const Plan &P);
 
 // Launches the persistent kernel of super-pass `si` (needs a 4-byte device
 // counter for the grid barrier).

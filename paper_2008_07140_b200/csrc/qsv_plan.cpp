@@ -895,6 +895,63 @@ Plan rebuild_with_pass_r(const Plan &B, const std::vector<int> &rs) {
     return P;
 }
 
+int split_product_prefix(const std::vector<GateRec> &recs, int n, std::vector<GateRec> &kept, std::vector<cd> &prefix) {
+    prefix.assign(4 * (size_t)n, cd(0.0));
+    for (int q = 0; q < n; ++q) prefix[4 * q] = prefix[4 * q + 3] = cd(1.0);
+    uint64_t blocked = 0;
+    int absorbed = 0;
+    kept.clear();
+    for (const GateRec &g : recs) {
+        const uint64_t touch = g.cmask | (1ull << g.t[0]) | (g.nt == 2 ? 1ull << g.t[1] : 0ull);
+        if (g.nt == 1 && g.cmask == 0 && !((blocked >> g.t[0]) & 1)) {
+            // A_q <- U A_q (U acts after the gates already absorbed on q)
+            cd *a = &prefix[4 * g.t[0]];
+            const cd a0 = a[0], a1 = a[1], a2 = a[2], a3 = a[3];
+            a[0] = g.u[0] * a0 + g.u[1] * a2;
+            a[1] = g.u[0] * a1 + g.u[1] * a3;
+            a[2] = g.u[2] * a0 + g.u[3] * a2;
+            a[3] = g.u[2] * a1 + g.u[3] * a3;
+            ++absorbed;
+            continue;
+        }
+        blocked |= touch;
+        kept.push_back(g);
+    }
+    return absorbed;
+}
+
+void product_tables(const Plan &P, uint64_t basis, const std::vector<int> &regs, std::vector<cd> &tab) {
+    const int n = P.n, G = (n + 4) / 5;
+    std::vector<cd> v(2 * (size_t)n);
+    for (int q = 0; q < n; ++q) {
+        const int b = (int)((basis >> q) & 1);
+        v[2 * q] = P.prefix[4 * q + b];          // column b_q of A_q
+        v[2 * q + 1] = P.prefix[4 * q + 2 + b];
+    }
+    uint64_t regmask = 0;
+    for (int q : regs) regmask |= 1ull << q;
+    tab.assign(32 * (size_t)G + 2 * regs.size(), cd(1.0));
+    for (int g = 0; g < G; ++g)
+        for (int x = 0; x < 32; ++x) {
+            cd f(1.0);
+            for (int j = 0; j < 5; ++j) {
+                const int q = 5 * g + j;
+                if (q >= n) break;
+                const int bit = (x >> j) & 1;
+                if ((regmask >> q) & 1) {
+                    if (bit) f = cd(0.0);  // register bits are zero in the thread's base index
+                } else {
+                    f *= v[2 * q + bit];
+                }
+            }
+            tab[32 * g + x] = f;
+        }
+    for (size_t k = 0; k < regs.size(); ++k) {
+        tab[32 * G + 2 * k] = v[2 * regs[k]];
+        tab[32 * G + 2 * k + 1] = v[2 * regs[k] + 1];
+    }
+}
+
 // Two-level schedule.  A SUPER-PASS selects s "super-tile" qubits S (greedy
 // absorption with capacity s); its gates are then split into ordinary passes
 // whose tiles lie inside S.  The executor runs all inner passes of a

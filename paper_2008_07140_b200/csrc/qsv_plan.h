@@ -130,7 +130,26 @@ struct Plan {
     // (+ the plan's output, always 1); filled on first use by qsv_jit.cpp
     mutable std::vector<double> jit_scale_in;
     int jit_device = -1;
+    // product-state start (qsv_options.product_start): the leading single-qubit
+    // gates of every qubit (each before any other gate touching that qubit) are
+    // not in `recs`; they map a basis state |b> to the product state
+    // (x)_q prefix_q e_{b_q}, which pass 0 synthesises from host-built factor
+    // tables instead of reading the state.  Such a plan only runs on a state
+    // holding a pending basis index (qsv_set_basis).
+    bool product = false;
+    std::vector<cd> prefix;  // 4 per qubit: row-major 2x2 product of the absorbed gates
 };
+
+// Splits `recs` into the leading uncontrolled single-qubit gates of each qubit
+// (multiplied into prefix[4q..4q+3]) and the rest (`kept`, program order).
+// Returns the number of absorbed gates.
+int split_product_prefix(const std::vector<GateRec> &recs, int n, std::vector<GateRec> &kept, std::vector<cd> &prefix);
+
+// Factor tables of a product-start plan for basis index `basis`: for every
+// group g of 5 index bits, tab[32 g + x] = prod over the group's qubits q that are
+// not in `regs` of v_q[bit of x], then for every register qubit regs[k] the pair
+// tab[32 G + 2k + b] = v_{regs[k]}[b]  (v_q = prefix_q e_{b_q}, G = ceil(n / 5)).
+void product_tables(const Plan &P, uint64_t basis, const std::vector<int> &regs, std::vector<cd> &tab);
 
 // Validates and classifies gate records; returns QSV_OK or an error status (msg set).
 int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector<GateRec> &out,

@@ -311,17 +311,23 @@ class P2PTransport:
             N.check(L.qsv_ipc_mem_handle(C.c_void_p(b.data_ptr()), hbuf, C.byref(off)))
             mine.append((hbuf.raw, off.value))
         self.events = [torch.cuda.Event(interprocess=True) for _ in range(1 << max_chunk_log2)]
+        # recorded on the compute stream before an exchange: completes when this rank is
+        # done with its receive buffer (last read by its previous exchange's sends)
+        self.free_event = torch.cuda.Event(interprocess=True)
         ev_handles = [e.ipc_handle() for e in self.events]
         allh = [None] * self.world
-        dist.all_gather_object(allh, (mine, ev_handles), group=group)
+        dist.all_gather_object(allh, (mine, ev_handles, self.free_event.ipc_handle()), group=group)
         self.peer_ptr = []  # [rank][buffer] -> device pointer (own buffers: local pointers)
         self.peer_events = []
+        self.peer_free = []
         self._opened = []
-        for r, (bufs, evh) in enumerate(allh):
+        for r, (bufs, evh, freeh) in enumerate(allh):
             if r == self.rank:
                 self.peer_ptr.append([b.data_ptr() for b in shard.bufs])
                 self.peer_events.append(self.events)
+                self.peer_free.append(self.free_event)
                 continue
+            self.peer_free.append(torch.cuda.Event.from_ipc_handle(shard.device, freeh))
             ptrs = []
             for raw, off in bufs:
                 p = C.c_void_p()
@@ -332,6 +338,7 @@ class P2PTransport:
             self.peer_events.append([torch.cuda.Event.from_ipc_handle(shard.device, h) for h in evh])
         self.max_chunk_log2 = max_chunk_log2
         self.last_exchange_ms = 0.0
+        self.last_fused = None  # (exchange-out pass ms, the run's other pass ms) when profiled
         self._t0 = torch.cuda.Event(enable_timing=True)
         self._t1 = torch.cuda.Event(enable_timing=True)
 
@@ -352,16 +359,14 @@ class P2PTransport:
         blk = chunk >> s
         src_base = shard.bufs[shard.cur].data_ptr()
         spare = 1 - shard.cur
-        # every rank's previous pushes are complete -> every receive buffer is free
-        self.copy_stream.synchronize()
-        self.dist.barrier(group=self.group)
-        self.copy_stream.wait_stream(shard.stream)  # this rank's send data is final
         partners = []
         for j in range(1 << s):
             peer = self.rank & ~gmask
             for i, b in enumerate(gbits):
                 peer |= ((j >> i) & 1) << b
             partners.append(peer)
+        self.copy_stream.wait_stream(shard.stream)  # this rank's send data is final
+        self._wait_partners_free(self.copy_stream, partners)
         self._t0.record(self.copy_stream)
         for i in range(1 << chunk_log2):
             for j, peer in enumerate(partners):
@@ -412,22 +417,45 @@ class P2PTransport:
                 peer |= ((j >> i) & 1) << b
             partners.append(peer)
             ex.dst[j] = self.peer_ptr[peer][spare]
-        # every rank's previous exchange is complete -> every receive buffer is free
-        self.copy_stream.synchronize()
-        shard.stream.synchronize()
-        self.dist.barrier(group=self.group)
+        # the partners' receive buffers are free once their streams pass their free
+        # events (no host synchronisation: only event waits on the compute stream)
+        self._wait_partners_free(shard.stream, partners)
         st = N.qsv_run_stats()
-        N.check(L.qsv_run_exchange(shard.handle(), rec.ctypes.data, len(rec), C.byref(shard.options), C.byref(ex),
-                                   C.byref(st)))
+        rc = L.qsv_run_exchange(shard.handle(), rec.ctypes.data, len(rec), C.byref(shard.options), C.byref(ex),
+                                C.byref(st))
+        if rc == 0:
+            self.events[0].record(shard.stream)
+            if shard.options.profile:
+                ms, _ = N.last_launches(shard.handle())
+                self.last_fused = (float(ms[-1]), [float(x) for x in ms[:-1]])
+        # the status vote doubles as the barrier after which every partner's event
+        # record has been enqueued; a failure on any rank raises on every rank
+        good = torch.tensor([int(rc == 0)], dtype=torch.int32,
+                            device="cpu" if self.dist.get_backend(self.group) == "gloo" else f"cuda:{shard.device}")
+        self.dist.all_reduce(good, op=self.dist.ReduceOp.MIN, group=self.group)
+        if not int(good.item()):
+            N.check(rc, shard.handle())
+            raise RuntimeError("fused exchange failed on another rank; the sharded state is invalid")
         if stats is not None:
             for k, v in st.as_dict().items():
                 stats[k] = stats.get(k, 0) + v
-        self.events[0].record(shard.stream)
-        self.dist.barrier(group=self.group)  # every partner has enqueued its event
         shard.commit_exchange()
         for peer in partners:
             shard.stream.wait_event(self.peer_events[peer][0])
         return True
+
+    def _wait_partners_free(self, stream, partners):
+        """`stream` waits until every partner is done with the receive buffer this
+        exchange writes into: each rank records its free event on its compute stream
+        (after all its work so far, including copy-stream pushes), a host barrier makes
+        every record visible, then the waits are enqueued."""
+        shard = self.shard
+        shard.stream.wait_stream(self.copy_stream)
+        self.free_event.record(shard.stream)
+        self.dist.barrier(group=self.group)
+        for peer in partners:
+            if peer != self.rank:
+                stream.wait_event(self.peer_free[peer])
 
     def exchange_ms(self) -> float:
         """Copy-stream time of the last exchange (this rank's pushes)."""
@@ -716,7 +744,13 @@ class ShardedSimulator:
 
         from .errors import DegenerateState
 
-        if rng is None and self.rank == 0:
+        import torch as _t
+
+        # the stream lives on rank 0; every rank learns whether it is there before any
+        # collective, so a missing stream raises everywhere instead of hanging the others
+        has = _t.tensor([int(rng is not None)], dtype=_t.int64, device=getattr(self.shard, "reduce_device", "cpu"))
+        self.dist.broadcast(has, src=0, group=self.group)
+        if not int(has.item()):
             raise UnsupportedGate("MEASURE needs a random stream", line)
         self._materialize()
         p = self.perm[self.dq[qubit]]
@@ -775,75 +809,3 @@ def make_transport(kind: str, dist, shard, group=None):
     if kind == "p2p":
         return P2PTransport(dist, shard, group)
     return AllToAllTransport(dist, group)
-
-
-def bench_main(args) -> None:
-    """`bench.py --gpus N` under torchrun: C3 weak scaling, RQC with
-    n = 32 + log2(N) qubits (2^32 local amplitudes = 64 GiB per GPU)."""
-    import json
-
-    import torch
-    import torch.distributed as dist
-
-    from . import workloads
-    from . import _native as N
-    from .program import parse_program
-
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    g = int(round(math.log2(world)))
-    n = (args.qubits or 32) + g
-    prog = parse_program(workloads.rqc_for_qubits(n, 24, 0))
-    G = len(prog.gate_instructions())
-    shard = CudaShard(n - g, local, options=N.options(tile_qubits=args.tile, reg_qubits=args.regs,
-                                                      low_qubits=args.low))
-    shard.reduce_device = f"cuda:{local}"
-    kind = os.environ.get("QSV_TRANSPORT", "p2p")
-    transport = make_transport(kind, dist, shard)
-    sim = ShardedSimulator(n, shard, transport=transport)
-
-    def step():
-        sim.set_basis(0)
-        sim.run(prog)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sim.stats.swaps.clear()
-    ev0.record(shard.stream)
-    for _ in range(args.steps):
-        step()
-    ev1.record(shard.stream)
-    torch.cuda.synchronize()
-    ms = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step = float(ms.item())
-    swaps = sim.stats.swaps
-    swap_bytes = sum(s.bytes_sent for s in swaps) / max(1, args.steps)
-    xfer = {"fused_exchanges_per_step": sum(s.fused for s in swaps) / max(1, args.steps)}
-    if kind == "p2p" and swaps and not all(s.fused for s in swaps):
-        t = torch.tensor([transport.exchange_ms()], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        last = swaps[-1].bytes_sent
-        xfer |= {"last_exchange_ms": float(t.item()), "last_exchange_bytes_per_rank": last,
-                "nvlink_gbs_per_rank": last / (float(t.item()) / 1e3) / 1e9, "nvlink_peak_gbs": 900.0}
-    if rank == 0:
-        line = {
-            "metric": "amplitude-gate updates/s", "value": G * float(1 << n) / (ms_step / 1e3),
-            "unit": "amp-gate/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "c128 (f64)", "data": "synthetic",
-            "config": {"workload": f"C3 weak scaling: RQC n={n} on grid {workloads.grid_shape(n)}, 24 cycles",
-                       "n_qubits": n, "n_local": n - g, "gates": G, "parallelism": f"sharded x{world}",
-                       "transport": kind, "chunks": 1 << sim.chunk_log2,
-                       "swaps_per_step": len(swaps) / max(1, args.steps),
-                       "swap_bytes_per_rank_per_step": swap_bytes, **xfer},
-            "gpu_launches": None,
-        }
-        print(json.dumps(line), flush=True)
-    transport.close() if hasattr(transport, "close") else None
-    dist.destroy_process_group()

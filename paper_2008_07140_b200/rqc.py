@@ -15,7 +15,10 @@ Two families:
   Appendix C.1-C.2, a documented extension - ref [21]'s exact prescription
   is not available).
 
-Qubits are numbered row-major, q = r * cols + c.  The pool gates are the
+Qubits are numbered row-major, q = r * cols + c.  `qubits` < rows * cols
+leaves the last row partial (qubits >= `qubits` do not exist and their edges
+are dropped): the near-square grids of qubit counts with no near-square
+rectangle.  The pool gates are the
 reference vocabulary: ``RX q,"pi/2"`` (= sqrt(X) up to a global phase),
 ``RY q,"pi/2"`` (= sqrt(Y) up to a global phase) and ``T q``.
 """
@@ -45,10 +48,13 @@ class RqcConfig:
     pmeasure: tuple[int, ...] = field(default=())
     patterns: int = 4
     no_repeat: bool = False
+    qubits: int = 0  # 0: rows * cols; else a partial last row
 
     def __post_init__(self):
         if self.rows * self.cols < 2:
             raise ValueError("grid needs at least 2 qubits")
+        if self.qubits and not ((self.rows - 1) * self.cols < self.qubits <= self.rows * self.cols):
+            raise ValueError("qubits must end inside the last grid row")
         if self.depth < 1:
             raise ValueError("depth must be at least 1")
         if self.patterns not in (4, 8):
@@ -61,14 +67,17 @@ class RqcConfig:
 
     @property
     def qubit_count(self) -> int:
-        return self.rows * self.cols
+        return self.qubits or self.rows * self.cols
 
 
-def _edges(rows, cols, orient, start, split=None):
+def _edges(rows, cols, orient, start, split=None, n=None):
     """Grid edges of one orientation; `start` = parity of the lower endpoint
-    along the edge axis, `split` = optional parity filter on the other axis."""
+    along the edge axis, `split` = optional parity filter on the other axis;
+    edges touching a qubit >= n (partial last row) are dropped."""
     q = lambda r, c: r * cols + c
     out = []
+    if n is not None and n < rows * cols:
+        return [e for e in _edges(rows, cols, orient, start, split) if e[1] < n]
     if orient == "h":
         for r in range(rows):
             if split is not None and r % 2 != split:
@@ -86,11 +95,12 @@ def _edges(rows, cols, orient, start, split=None):
 
 def layer_pairs(config: RqcConfig, layer: int) -> list[tuple[int, int]]:
     """CZ pairs of one cycle (reference pattern order for patterns=4)."""
+    n = config.qubit_count
     if config.patterns == 4:
         p = layer % 4
-        return _edges(config.rows, config.cols, "h" if p < 2 else "v", p % 2)
+        return _edges(config.rows, config.cols, "h" if p < 2 else "v", p % 2, n=n)
     orient, start, split = _EIGHT[layer % 8]
-    return _edges(config.rows, config.cols, orient, start, split)
+    return _edges(config.rows, config.cols, orient, start, split, n=n)
 
 
 _layer_pairs = layer_pairs  # reference-compatible private name
@@ -104,6 +114,8 @@ def generate_rqc(config: RqcConfig) -> str:
             f"depth={config.depth} seed={config.seed}")
     if config.patterns != 4 or config.no_repeat:
         head += f" patterns={config.patterns} no_repeat={int(config.no_repeat)}"
+    if config.qubits and config.qubits != config.rows * config.cols:
+        head += f" qubits={config.qubits}"
     lines = [head, f"QINIT {n}"] + [f"H {q}" for q in range(n)]
     last: dict[int, str] = {}
     pool = config.single_qubit_pool

@@ -19,7 +19,11 @@ compile, no per-trajectory re-planning.  Plans the Pauli path cannot take
 their qubit) fall back to running the noisy program itself.  With `dedup=True` the error-free
 trajectories are simulated once and the result reused - reported separately
 (`TrajectoryReport.unique_runs`).  Across GPUs trajectories are independent
-replicas: rank r takes t = r, r+P, ... and results are gathered on rank 0.
+replicas: rank r takes t = r, r+P, ... (no collective while they run); with
+`gather=True` (default) and an initialised process group the per-trajectory
+tables, error counts, norms and kept amplitudes are gathered on rank 0, which
+returns the whole batch in trajectory order (`gather_reports`); the other ranks
+return their own slice.
 """
 
 from __future__ import annotations
@@ -55,6 +59,25 @@ _PLANS: dict = {}  # (gate records, n, options, device) -> qsv_plan of the clean
 _MAX_PLANS = 8
 
 
+def gather_reports(rep: TrajectoryReport, dist, group=None) -> TrajectoryReport:
+    """All ranks' slices on rank 0, trajectories in id order (one all_gather_object;
+    the other ranks get their own report back).  Work counters are summed and the
+    time is the max over ranks."""
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, rep, group=group)
+    if dist.get_rank(group) != 0:
+        return rep
+    rows = sorted((t, r, i) for r, pr in enumerate(parts) for i, t in enumerate(pr.trajectories))
+    tables = np.stack([parts[r].tables[i] for _, r, i in rows]) if rows else rep.tables[:0]
+    norms = np.array([parts[r].norms[i] for _, r, i in rows])
+    kept = {}
+    for pr in parts:
+        kept.update(pr.kept)
+    return TrajectoryReport(rep.n_qubits, [t for t, _, _ in rows], [parts[r].errors[i] for _, r, i in rows],
+                            rep.probe_qubits, tables, norms, kept, sum(pr.gate_updates for pr in parts),
+                            sum(pr.unique_runs for pr in parts), max(pr.seconds for pr in parts))
+
+
 def _run_clean_batches(slots, clean_gates, n, b, pq, tables, device, opts) -> int:
     """Error-free trajectories, 2^b per (n + b)-qubit state (the last batch is padded
     with extra copies so every batch reuses one plan and its compiled kernels); fills
@@ -87,7 +110,8 @@ def _run_clean_batches(slots, clean_gates, n, b, pq, tables, device, opts) -> in
 def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0, *,
                      probe_qubits=(0, 1, 2), keep=(), dedup: bool = False, device: int = 0,
                      stream=None, rank: int = 0, world: int = 1, state: SV.StateVector | None = None,
-                     options=None, streams: int = 2, batch_clean: int = 0) -> TrajectoryReport:
+                     options=None, streams: int = 2, batch_clean: int = 0, gather: bool = True,
+                     group=None) -> TrajectoryReport:
     """`batch_clean` = b > 0: the error-free trajectories (not kept, not deduplicated) run
     2^b at a time as ONE (n + b)-qubit state - trajectory index = top qubits - through
     the clean circuit's fused plan (every trajectory block is simulated; the passes are
@@ -136,10 +160,10 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
     dedup_from = {}     # slot -> slot whose table it reuses
     # probe tables land in device memory, one row per trajectory, read once at
     # the end: the host runs ahead of the GPU (no per-trajectory synchronisation)
-    async_tables = len(pq) <= 4
-    if async_tables:
-        import torch
+    import torch
 
+    async_tables = len(pq) <= 4 and torch.cuda.is_available()
+    if async_tables:
         # no fill kernel: the libqsv streams are not ordered after torch's; every
         # simulated row is written by its pmeasure, deduplicated rows are copied below
         dev_tables = torch.empty((max(1, len(mine)), 1 << len(pq)), dtype=torch.float64, device=f"cuda:{device}")
@@ -226,7 +250,17 @@ def run_trajectories(program: Program, p: float, n_traj: int, base_seed: int = 0
             tables[k] = tables[src]
         norms[:] = tables.sum(axis=1)  # the probe table sums to ||psi||^2
     finally:
+        # every state's stream (states[0] included) is idle before dev_tables, which its
+        # kernels write, can go back to torch's allocator
+        for st_ in states:
+            L.qsv_synchronize(st_.handle)
         for st_ in states[1:]:
             st_.close()
-    return TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
-                            time.perf_counter() - t0)
+    rep = TrajectoryReport(n, mine, errors, tuple(int(q) for q in pq), tables, norms, kept, updates, unique,
+                           time.perf_counter() - t0)
+    if gather and world > 1:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            rep = gather_reports(rep, dist, group)
+    return rep

@@ -27,23 +27,30 @@ C5_SHAPE = (4, 6, 20)   # n=24, 20 cycles
 
 
 def grid_shape(n: int) -> tuple[int, int]:
-    """Most square rows x cols = n with rows <= cols (33 -> 3x11, 34 -> 2x17)."""
+    """Grid of an n-qubit RQC: the most square full rectangle rows x cols = n
+    (rows <= cols) when its aspect ratio is at most 2 (30 -> 5x6, 32 -> 4x8,
+    35 -> 5x7), else ceil(sqrt(n)) columns with a partial last row
+    (31 -> 6x6 holding 31, 33 -> 6x6 holding 33, 34 -> 6x6 holding 34;
+    SURVEY.md Appendix C.4)."""
     best = (1, n)
     for r in range(1, int(math.isqrt(n)) + 1):
         if n % r == 0:
             best = (r, n // r)
-    return best
+    if best[1] <= 2 * best[0] or n < 4:
+        return best
+    c = math.isqrt(n - 1) + 1
+    return (-(-n // c), c)
 
 
-def rqc_text(rows: int, cols: int, depth: int, seed: int = 0, pmeasure=()) -> str:
+def rqc_text(rows: int, cols: int, depth: int, seed: int = 0, pmeasure=(), qubits: int = 0) -> str:
     """BASELINE RQC: 8 cycled CZ patterns, no repeated pool gate per qubit."""
     return generate_rqc(RqcConfig(rows, cols, depth, seed, pmeasure=tuple(pmeasure),
-                                  patterns=8, no_repeat=True))
+                                  patterns=8, no_repeat=True, qubits=qubits))
 
 
 def rqc_for_qubits(n: int, depth: int = 24, seed: int = 0) -> str:
     r, c = grid_shape(n)
-    return rqc_text(r, c, depth, seed)
+    return rqc_text(r, c, depth, seed, qubits=n if r * c != n else 0)
 
 
 def qft_lines(n: int) -> list[str]:

@@ -146,6 +146,9 @@ class FakeLib:
     def qsv_plan_execute_paulis(self, h, plan, paulis, n_paulis, opts, stats):
         return N.QSV_E_UNSUPPORTED  # the host then inserts the Paulis as explicit gates
 
+    def qsv_plan_execute_probe(self, h, plan, paulis, n_paulis, probe, m, table, opts, stats):
+        return N.QSV_E_UNSUPPORTED
+
     def qsv_last_error(self):
         return b""
 

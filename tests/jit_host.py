@@ -70,6 +70,42 @@ def run_plan_host(records: np.ndarray, n: int, psi: np.ndarray, **opts) -> np.nd
         N.lib().qsv_plan_destroy(h)
 
 
+def product_tables(h, basis: int) -> np.ndarray:
+    L = N.lib()
+    cnt = C.c_int64()
+    N.check(L.qsv_plan_product_tables(h, basis, None, 0, C.byref(cnt)))
+    tab = np.zeros(cnt.value, dtype=np.complex128)
+    N.check(L.qsv_plan_product_tables(h, basis, tab.ctypes.data, cnt.value, C.byref(cnt)))
+    return tab
+
+
+def run_product_plan_host(records: np.ndarray, n: int, basis: int, **opts):
+    """A product-start plan (qsv_options.product_start = 1) through the host rendering:
+    pass 0 synthesises the product state from the plan's factor tables for `basis`
+    (the state buffer is not read), the other passes run as usual.  Returns
+    (amplitudes, plan passes) or None when the stream has nothing to absorb."""
+    h = plan_handle(records, n, product_start=1, **opts)
+    try:
+        info = N.qsv_plan_info()
+        N.check(N.lib().qsv_plan_summary(h, C.byref(info)))
+        if not info.product_start:
+            return None
+        out = np.full(1 << n, np.nan + 0j)  # never read by the synthesising pass
+        tab = product_tables(h, basis)
+        for p in range(info.passes):
+            pi = N.qsv_pass_info()
+            N.check(N.lib().qsv_plan_pass(h, p, C.byref(pi)))
+            lib = _compile(kernel_source(h, p, True))
+            if p == 0:
+                lib.qsv_pass_host.argtypes = [C.c_void_p, C.c_ulonglong, C.c_void_p]
+                lib.qsv_pass_host(out.ctypes.data, 1 << (n - pi.m), tab.ctypes.data)
+            else:
+                lib.qsv_pass_host(out.ctypes.data, 1 << (n - pi.m))
+        return out, info.passes
+    finally:
+        N.lib().qsv_plan_destroy(h)
+
+
 def super_source(h, si: int, host: bool) -> str:
     L = N.lib()
     need = C.c_int64()

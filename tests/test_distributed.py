@@ -183,7 +183,7 @@ def test_segment_planner_c3_shapes():
                 assert all((local[k] >> q) & 1 for q in t)
     # reorder validity on a small instance (the planner's order is a topological order)
     n = 10
-    prog = parse_program(workloads.rqc_for_qubits(n, 16, 3))
+    prog = parse_program(workloads.rqc_text(2, 5, 16, 3))
     items = [Gt.controlled_form(i) for i in prog.gate_instructions()]
     seg, local = plan_segments(items, n, 8, 255, False)
     assert len(local) > 2

@@ -221,3 +221,39 @@ def test_mixed_register_qubits_per_pass(pattern, monkeypatch):
         ref = O.run_full(prog, initial=psi).state.amplitudes
         out = run_plan_host(compile_gates(prog.gate_instructions()), 16, psi, tile_qubits=9, jit=1)
         assert np.abs(out - ref).max() <= 1e-12, pattern
+
+
+@pytest.mark.parametrize("basis", [0, 5, 0b101101])
+@pytest.mark.parametrize("cfg", [dict(), dict(tile_qubits=5, reg_qubits=3, low_qubits=2), dict(tile_qubits=6, reg_qubits=4)])
+def test_product_start_plan_matches_oracle(basis, cfg):
+    """Product-state start (qsv_options.product_start): every qubit's leading
+    single-qubit gates (the RQC's H layer and the idle qubits' first gates) leave the
+    stream and the first pass synthesises prefix (x) e_b from host-built factor tables
+    instead of reading the state; host rendering vs the oracle from |basis>."""
+    from jit_host import run_product_plan_host
+
+    prog = parse_program(workloads.rqc_text(3, 4, 10, seed=basis % 7))
+    n = prog.qubit_count
+    got = run_product_plan_host(compile_gates(prog.gate_instructions()), n, basis, **cfg)
+    assert got is not None
+    init = np.zeros(1 << n, complex)
+    init[basis] = 1
+    ref = O.run_full(prog, initial=init).state.amplitudes
+    assert np.abs(got[0] - ref).max() <= 1e-12
+
+
+def test_product_start_split_rules():
+    """Absorption stops at the first gate on a qubit that is not an uncontrolled
+    single-qubit gate; diagonal single-qubit gates are absorbed too; a stream with
+    nothing to absorb gives an ordinary plan."""
+    from jit_host import run_product_plan_host
+
+    text = "QINIT 4\nH 0\nT 0\nCZ 0,1\nH 1\nX 0\nRY 2,\"0.3\"\nCNOT 2,3\nH 3\nRZ 2,\"0.7\"\n"
+    prog = parse_program(text)
+    got, passes = run_product_plan_host(compile_gates(prog.gate_instructions()), 4, 0, tile_qubits=3,
+                                        reg_qubits=2, low_qubits=1)
+    ref = O.run_full(prog).state.amplitudes
+    assert np.abs(got - ref).max() <= 1e-13 and passes >= 1
+    only2q = parse_program("QINIT 3\nCZ 0,1\nCNOT 1,2\n")
+    assert run_product_plan_host(compile_gates(only2q.gate_instructions()), 3, 0, tile_qubits=3, reg_qubits=2,
+                                 low_qubits=1) is None

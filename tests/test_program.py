@@ -132,8 +132,26 @@ def test_eight_pattern_rqc_properties(rows, cols):
 
 
 def test_workload_grid_shapes():
-    assert [workloads.grid_shape(n) for n in (20, 24, 30, 32, 33, 34, 35)] == [
-        (4, 5), (4, 6), (5, 6), (4, 8), (3, 11), (2, 17), (5, 7)]
+    assert [workloads.grid_shape(n) for n in (20, 24, 30, 31, 32, 33, 34, 35)] == [
+        (4, 5), (4, 6), (5, 6), (6, 6), (4, 8), (6, 6), (6, 6), (5, 7)]
+
+
+def test_partial_row_grid_edges():
+    """31 qubits on 6 columns: the last row holds one qubit; every CZ is a grid edge
+    between existing qubits, no qubit is touched twice per cycle, and over 8 cycles
+    every existing edge appears exactly once (the 8-pattern property)."""
+    cfg = rqc.RqcConfig(6, 6, 8, 0, patterns=8, no_repeat=True, qubits=31)
+    seen = []
+    for layer in range(8):
+        pairs = rqc.layer_pairs(cfg, layer)
+        flat = [q for pr in pairs for q in pr]
+        assert len(flat) == len(set(flat)) and max(flat) < 31
+        for a, b in pairs:
+            assert b - a in (1, 6) and (b - a != 1 or a // 6 == b // 6)
+        seen += pairs
+    edges = {(a, a + 1) for a in range(31) if a % 6 != 5 and a + 1 < 31} | {(a, a + 6) for a in range(31) if a + 6 < 31}
+    assert sorted(seen) == sorted(edges)
+    assert parse_program(workloads.rqc_for_qubits(31, 4, 0)).qubit_count == 31
 
 
 def test_pauli_insertion_replays_reference_draws(golden):
