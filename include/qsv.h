@@ -95,6 +95,8 @@ typedef struct qsv_run_stats {
     double algorithmic_bytes; /* per pass 2 * 16 * 2^n_local (16 * 2^n_local when it synthesises a basis input) */
     double plan_ms;        /* host time building schedules for this call (0 when the plan was cached) */
     double jit_ms;         /* host time specialising + compiling (NVRTC) / loading pass kernels */
+    int64_t compiled_passes; /* passes of a cold call (kernels still compiling in the background) that
+                                ran compiled; the others ran on the interpreted pass kernel */
 } qsv_run_stats;
 
 typedef struct qsv_plan_info {
@@ -135,6 +137,11 @@ const char *qsv_last_error(void);
 /* message of the last failed call made on `st` (per handle: calls on other handles or
  * threads in between do not overwrite it); "" when none failed */
 const char *qsv_state_last_error(const qsv_state *st);
+/* The first qsv_run of a new circuit does not wait for NVRTC: its pass kernels compile on
+ * background host threads while the passes run (compiled once ready, interpreted before;
+ * qsv_run_stats.compiled_passes).  qsv_jit_wait blocks until no such compile is pending,
+ * so the next call runs fully compiled. */
+int qsv_jit_wait(void);
 /* per-launch event times (ms) and algorithmic bytes of the last call on `st` that ran
  * with qsv_options.profile = 1 (bytes: 2 x 16 x 2^n per pass, 16 x 2^n for a pass that
  * synthesises its basis-state input); copies min(count, cap) entries */

@@ -42,7 +42,8 @@ class qsv_options(C.Structure):
 class qsv_run_stats(C.Structure):
     _fields_ = [("gates", C.c_int64), ("passes", C.c_int64), ("stages", C.c_int64),
                 ("inner_passes", C.c_int64), ("launches", C.c_int64), ("kernel_ms", C.c_double), ("max_launch_ms", C.c_double),
-                ("algorithmic_bytes", C.c_double), ("plan_ms", C.c_double), ("jit_ms", C.c_double)]
+                ("algorithmic_bytes", C.c_double), ("plan_ms", C.c_double), ("jit_ms", C.c_double),
+                ("compiled_passes", C.c_int64)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -71,6 +72,7 @@ _SIGNATURES = {
     "qsv_last_error": ([], C.c_char_p),
     "qsv_state_last_error": ([C.c_void_p], C.c_char_p),
     "qsv_last_launches": ([_P, _P, _P, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "qsv_jit_wait": ([], C.c_int),
     "qsv_plan_product_tables": ([_P, C.c_uint64, _P, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
     "qsv_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "qsv_create": ([C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),

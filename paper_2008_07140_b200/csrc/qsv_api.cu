@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <thread>
 #include <bit>
 #include <cstdio>
 #include <cstring>
@@ -375,6 +376,151 @@ int execute_plan(qsv_state *st, Plan &P, DevPass *dp, DevStage *ds, DevOp *dop, 
     return QSV_OK;
 }
 
+// A plan the cold-call path can run pass by pass (flat, no SWAP relabelling).
+bool mixed_ok(const Plan &P) {
+    return !P.passes.empty() && !use_supers(P) && !P.relabelled && P.pass_gates.size() == P.passes.size() &&
+           !jit_double_buffer();
+}
+
+int ensure_plan_buf(qsv_state *st, size_t bytes) {
+    if (st->plan_buf_bytes >= bytes) return QSV_OK;
+    if (st->plan_buf) {
+        CUDA_TRY(cudaStreamSynchronize(st->stream));
+        cudaFree(st->plan_buf);
+    }
+    st->plan_buf = nullptr;
+    st->plan_buf_bytes = 0;
+    CUDA_TRY(cudaMalloc(&st->plan_buf, bytes));
+    st->plan_buf_bytes = bytes;
+    return QSV_OK;
+}
+
+int upload_product_tables(qsv_state *st, const Plan &P, const std::vector<int> &regs) {
+    std::vector<cd> tab;
+    product_tables(P, (uint64_t)st->pending_basis, regs, tab);
+    if (tab.size() * sizeof(cd) > 8192) return fail(QSV_E_UNSUPPORTED, "product tables too large");
+    if (!st->ptab) CUDA_TRY(cudaMalloc(&st->ptab, 8192));
+    CUDA_TRY(cudaMemcpyAsync(st->ptab, tab.data(), tab.size() * sizeof(cd), cudaMemcpyHostToDevice, st->stream));
+    return QSV_OK;
+}
+
+// Cold call of a flat plan whose specialised kernels are still compiling
+// (jit_start_async): pass j runs compiled when its kernel is ready, else on the
+// interpreted pass kernel with the same tile and gates (r <= 4) plus the scale op
+// that leaves the state as compiled pass j+1 expects (stored = true / scale, as in
+// execute_with_paulis).  Before enqueueing a pass whose kernel is not ready the
+// host waits until it is, or until the GPU has finished pass j-1 (the GPU never
+// idles for it; a late pass gets the longest time to finish compiling).  A product-start plan's interpreted first pass
+// reads the product state written by product_state_kernel.
+int execute_plan_mixed(qsv_state *st, Plan &P, const qsv_options *opt, qsv_run_stats *stats) {
+    std::string err;
+    const int np = (int)P.passes.size();
+    const std::vector<double> &sc = pass_scales(P);
+    if (P.product && st->pending_basis < 0)
+        return fail(QSV_E_UNSUPPORTED, "a product-start plan runs only on a basis state (qsv_set_basis)");
+    LaunchTimer tm;
+    tm.on = opt && opt->profile;
+    tm.s = st->stream;
+    tm.st = st;
+    const double full = 32.0 * (double)st->size();
+    double alg_bytes = 0.0;
+    int64_t launches = 0, compiled = 0;
+    std::vector<cudaEvent_t> done(np, nullptr);
+    int rc = QSV_OK;
+    for (int j = 0; j < np && rc == QSV_OK; ++j) {
+        bool ready = false;
+        rc = jit_try_pass(P, j, st->device, &ready, err);
+        while (rc == QSV_OK && !ready && j >= 1 && cudaEventQuery(done[j - 1]) == cudaErrorNotReady) {
+            std::this_thread::sleep_for(std::chrono::microseconds(100));
+            rc = jit_try_pass(P, j, st->device, &ready, err);
+        }
+        if (rc) {
+            rc = fail(rc, err);
+            break;
+        }
+        double b = full;
+        if (ready) {
+            const void *ptab = nullptr;
+            if (j == 0 && P.product) {
+                rc = upload_product_tables(st, P, product_regs(P));
+                if (rc) break;
+                ptab = st->ptab;
+            }
+            const unsigned long long basis = st->pending_basis >= 0 ? (unsigned long long)st->pending_basis : ~0ull;
+            if (st->pending_basis >= 0) b = 0.5 * full;
+            tm.begin();
+            rc = qsv::jit_ready(P, st->device) ? jit_launch(P, j, st->amps, st->n, st->stream, err, basis, ptab)
+                                               : jit_launch_partial(P, j, st->amps, st->n, st->stream, err, basis, ptab);
+            tm.end(b);
+            if (rc) {
+                rc = fail(rc, err);
+                break;
+            }
+            st->pending_basis = -1;
+            ++compiled;
+        } else {
+            if (j == 0 && P.product) {
+                rc = upload_product_tables(st, P, {});
+                if (rc) break;
+                tm.begin();
+                product_state_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(
+                    st->amps, st->size(), st->ptab, (P.n + 4) / 5);
+                tm.end(0.5 * full);
+                CUDA_TRY(cudaGetLastError());
+                st->pending_basis = -1;
+                alg_bytes += 0.5 * full;
+                ++launches;
+            } else {
+                rc = materialize(st);
+                if (rc) break;
+            }
+            std::vector<GateRec> recs = P.recs;
+            std::vector<int32_t> taken = P.pass_gates[j];
+            const double f = sc[j] / sc[j + 1];
+            if (f != 1.0) {
+                GateRec g;
+                g.nt = 1;
+                g.t[0] = P.passes[j].tq[0];
+                for (int k = 0; k < 16; ++k) g.u[k] = 0;
+                g.u[0] = g.u[3] = f;
+                g.diag = true;
+                g.dmask = 1ull << g.t[0];
+                recs.push_back(g);
+                taken.push_back((int32_t)recs.size() - 1);
+            }
+            Plan Q = build_single_pass(recs, taken, P.passes[j].tile_mask, P.n, P.m, std::min(pass_r(P, j), 4), P.L);
+            rc = ensure_plan_buf(st, plan_bytes(Q));
+            DevPass *dp;
+            DevStage *ds;
+            DevOp *dop;
+            if (!rc) rc = upload_plan(st, Q, st->plan_buf, &dp, &ds, &dop);
+            if (rc) break;
+            tm.begin();
+            rc = launch_pass(st, Q, 0, dp, ds, dop);
+            tm.end(full);
+            if (rc) break;
+        }
+        cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming);
+        cudaEventRecord(done[j], st->stream);
+        ++launches;
+        alg_bytes += b;
+    }
+    for (cudaEvent_t e : done)
+        if (e) cudaEventDestroy(e);
+    if (rc) return rc;
+    tm.collect(stats);
+    if (stats) {
+        stats->gates += P.gates;
+        stats->passes += np;
+        stats->inner_passes += np;
+        stats->stages += (int64_t)P.stages.size();
+        stats->launches += launches;
+        stats->algorithmic_bytes += alg_bytes;
+        stats->compiled_passes += compiled;
+    }
+    return QSV_OK;
+}
+
 int launch_gate(qsv_state *st, const GateRec &g) {
     const int mrc = materialize(st);
     if (mrc) return mrc;
@@ -431,6 +577,11 @@ const char *qsv_version(void) { return "qsv 0.1.0 (sm_100a)"; }
 const char *qsv_last_error(void) { return g_error.c_str(); }
 
 const char *qsv_state_last_error(const qsv_state *st) { return st ? st->last_error.c_str() : g_error.c_str(); }
+
+int qsv_jit_wait(void) {
+    jit_wait_async();
+    return QSV_OK;
+}
 
 int qsv_last_launches(const qsv_state *st, double *ms, double *bytes, int64_t cap, int64_t *count) {
     if (!st || !count) return fail(QSV_E_PARSE, "qsv_last_launches: null argument");
@@ -883,10 +1034,24 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     const auto t1 = std::chrono::steady_clock::now();
     bool jit_ready = false;
     if (want_jit) {
-        // first use of a cached plan: specialise its kernels once
-        std::lock_guard<std::mutex> lk(cp->mu);
+        std::unique_lock<std::mutex> lk(cp->mu);
         std::string err;
-        jit_ready = jit_prepare(cp->plan, st->device, err) == QSV_OK;  // failures are reported by execute_plan
+        // first call on a new circuit (auto mode): its kernels compile in the background
+        // while the passes run, each compiled one as soon as it is ready and the others
+        // on the interpreted kernel (no wait for NVRTC); later calls find them compiled
+        static const bool async_env = !std::getenv("QSV_JIT_ASYNC") || std::atoi(std::getenv("QSV_JIT_ASYNC")) != 0;
+        Plan &Pc = cp->plan;
+        if (jm == 0 && async_env && !qsv::jit_ready(Pc, st->device) && mixed_ok(Pc) &&
+            jit_start_async(Pc, st->device, err) == QSV_OK) {
+            if (stats) {
+                const auto t2 = std::chrono::steady_clock::now();
+                stats->plan_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+                stats->jit_ms += std::chrono::duration<double, std::milli>(t2 - t1).count();
+            }
+            return execute_plan_mixed(st, Pc, opt, stats);
+        }
+        // otherwise specialise the plan's kernels once (blocking)
+        jit_ready = jit_prepare(Pc, st->device, err) == QSV_OK;  // failures are reported by execute_plan
     }
     if (product && !jit_ready) {
         // no specialised kernels: the plain plan runs on the interpreted kernel

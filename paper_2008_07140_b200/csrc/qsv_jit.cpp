@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cctype>
 #include <atomic>
+#include <condition_variable>
+#include <deque>
 #include <cinttypes>
 #include <cmath>
 #include <cstdio>
@@ -1894,10 +1896,150 @@ void jit_choose_supers(Plan &P, int sms) {
     }
 }
 
+namespace {
+
+// One NVRTC compile (disk cache first); a three-CTA register cap that spills
+// (accumulator-heavy passes, e.g. QFT: 1.2 KB of local memory, +20 % time) is
+// recompiled for two CTAs per SM (the cache key stays the original source).
+void compile_unit(Unit &u) {
+    const std::string path = disk_cache_path(u.src);
+    if (disk_cache_load(path, u.cubin)) return;
+    u.cubin = jit_compile_cubin(u.src, u.log);
+    const std::string three = "__launch_bounds__(128, 3)";
+    const size_t at = u.src.find(three);
+    if (!u.cubin.empty() && at != std::string::npos && spill_bytes(u.log) > kMaxSpillBytes) {
+        std::string src2 = u.src;
+        src2.replace(at, three.size(), "__launch_bounds__(128, 2)");
+        std::string log2;
+        std::string cubin2 = jit_compile_cubin(src2, log2);
+        if (!cubin2.empty()) u.cubin.swap(cubin2);
+    }
+    disk_cache_store(path, u.cubin);
+}
+
+// ---- asynchronous compilation (the cold call of a new circuit) ----------------
+// Units submitted here compile on a small pool of host threads while the caller
+// runs the passes that are not ready yet on the interpreted kernel
+// (execute_plan_mixed in qsv_api.cu).  A blocking jit_prepare that meets a unit in
+// flight waits for it instead of compiling it again.  The pool and its maps are
+// never destroyed (threads may outlive static destruction); an atexit hook waits
+// for compiles in flight so NVRTC is not torn down under a running compile.
+struct AsyncUnit {
+    Unit u;
+    bool done = false;
+};
+struct AsyncPool {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::shared_ptr<AsyncUnit>> queue;
+    std::map<std::string, std::shared_ptr<AsyncUnit>> by_src;  // submitted, not yet loaded
+    int active = 0;
+    bool started = false;
+};
+AsyncPool &apool() {
+    static AsyncPool *p = new AsyncPool();
+    return *p;
+}
+void async_worker() {
+    AsyncPool &A = apool();
+    for (;;) {
+        std::shared_ptr<AsyncUnit> job;
+        {
+            std::unique_lock<std::mutex> lk(A.mu);
+            A.cv.wait(lk, [&] { return !A.queue.empty(); });
+            job = A.queue.front();
+            A.queue.pop_front();
+            ++A.active;
+        }
+        compile_unit(job->u);
+        {
+            std::lock_guard<std::mutex> lk(A.mu);
+            job->done = true;
+            --A.active;
+        }
+        A.cv.notify_all();
+    }
+}
+void async_drain_at_exit() {
+    AsyncPool &A = apool();
+    std::unique_lock<std::mutex> lk(A.mu);
+    A.queue.clear();
+    A.cv.wait(lk, [&] { return A.active == 0; });
+}
+std::shared_ptr<AsyncUnit> async_submit(const Unit &u) {
+    AsyncPool &A = apool();
+    std::lock_guard<std::mutex> lk(A.mu);
+    auto it = A.by_src.find(u.src);
+    if (it != A.by_src.end()) return it->second;
+    if (!A.started) {
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        for (unsigned t = 0; t < hw; ++t) std::thread(async_worker).detach();
+        std::atexit(async_drain_at_exit);
+        A.started = true;
+    }
+    auto job = std::make_shared<AsyncUnit>();
+    job->u = u;
+    A.by_src[u.src] = job;
+    A.queue.push_back(job);
+    A.cv.notify_all();
+    return job;
+}
+// the finished async unit for `src` (removed from the pool), waiting for it when
+// `wait`; nullptr when none was submitted (or it is still running and !wait)
+std::shared_ptr<AsyncUnit> async_take(const std::string &src, bool wait) {
+    AsyncPool &A = apool();
+    std::unique_lock<std::mutex> lk(A.mu);
+    auto it = A.by_src.find(src);
+    if (it == A.by_src.end()) return nullptr;
+    auto job = it->second;
+    if (!job->done) {
+        if (!wait) return nullptr;
+        A.cv.wait(lk, [&] { return job->done; });
+    }
+    A.by_src.erase(src);
+    return job;
+}
+
+// Loads a compiled unit for `device` (module, dynamic smem, occupancy) into the
+// in-process cache.  Caller holds g_cache_mu.
+int load_unit(const Plan &P, Unit &u, int device, CacheEntry &out, std::string &err) {
+    Driver &drv = driver();
+    if (u.cubin.empty()) {
+        err = "NVRTC failed for " + u.name + " " + std::to_string(u.index) + ": " + u.log;
+        return QSV_E_DEVICE;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    CUmodule mod;
+    CUfunction fn;
+    CUresult r = drv.ModuleLoadData(&mod, u.cubin.data());
+    if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&fn, mod, u.name.c_str());
+    const int gang = u.super ? 1 : source_gang(u.src);
+    const int smem = gang * (int)((size_t)(jit_double_buffer() ? 32 : 16) << u.m);  // tile buffer(s)
+    if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
+    int per_sm = 0;
+    if (r == CUDA_SUCCESS)
+        r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn,
+                                                          gang << (u.m - (u.super ? P.r : pass_r(P, u.index))),
+                                                          (size_t)smem);
+    if (r != CUDA_SUCCESS || per_sm < 1) {
+        const char *s = nullptr;
+        if (r != CUDA_SUCCESS) drv.GetErrorString(r, &s);
+        err = std::string("loading specialised kernel: ") + (s ? s : "zero occupancy");
+        return QSV_E_DEVICE;
+    }
+    // QSV_JIT_CTAS_PER_SM (diagnostic): cap the persistent grid's CTAs per SM
+    if (const char *c = std::getenv("QSV_JIT_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(c)));
+    out = CacheEntry{fn, per_sm * sms, gang};
+    g_cache[{device, u.src}] = out;
+    return QSV_OK;
+}
+
+}  // namespace
+
 int jit_prepare(Plan &P, int device, std::string &err) {
     if (P.jit_device == device && P.jit_funcs.size() == P.passes.size()) return QSV_OK;
     if (!jit_available(err)) return QSV_E_DEVICE;
-    Driver &drv = driver();
     std::vector<Unit> units;
     for (size_t i = 0; i < P.passes.size(); ++i)
         units.push_back(Unit{jit_source(P, (int)i), "qsv_pass", {}, {}, P.passes[i].m, false, (int)i});
@@ -1917,32 +2059,20 @@ int jit_prepare(Plan &P, int device, std::string &err) {
             else todo.push_back((int)i);
         }
     }
-    // compile the missing kernels concurrently (independent NVRTC programs)
+    // units compiling asynchronously (an earlier cold call) are awaited, the others are
+    // compiled here concurrently (independent NVRTC programs)
+    std::vector<int> local;
+    for (int i : todo) {
+        if (auto job = async_take(units[i].src, true)) units[i].cubin.swap(job->u.cubin), units[i].log.swap(job->u.log);
+        else local.push_back(i);
+    }
     {
         std::vector<std::thread> pool;
         const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
         std::atomic<size_t> next{0};
-        for (unsigned t = 0; t < std::min<size_t>(hw, todo.size()); ++t)
+        for (unsigned t = 0; t < std::min<size_t>(hw, local.size()); ++t)
             pool.emplace_back([&] {
-                for (size_t k; (k = next.fetch_add(1)) < todo.size();) {
-                    Unit &u = units[todo[k]];
-                    const std::string path = disk_cache_path(u.src);
-                    if (disk_cache_load(path, u.cubin)) continue;
-                    u.cubin = jit_compile_cubin(u.src, u.log);
-                    // a three-CTA register cap that spills (accumulator-heavy
-                    // passes, e.g. QFT: 1.2 KB of local memory, +20 % time) is
-                    // recompiled for two CTAs per SM (cache key stays u.src)
-                    const std::string three = "__launch_bounds__(128, 3)";
-                    const size_t at = u.src.find(three);
-                    if (!u.cubin.empty() && at != std::string::npos && spill_bytes(u.log) > kMaxSpillBytes) {
-                        std::string src2 = u.src;
-                        src2.replace(at, three.size(), "__launch_bounds__(128, 2)");
-                        std::string log2;
-                        std::string cubin2 = jit_compile_cubin(src2, log2);
-                        if (!cubin2.empty()) u.cubin.swap(cubin2);
-                    }
-                    disk_cache_store(path, u.cubin);
-                }
+                for (size_t k; (k = next.fetch_add(1)) < local.size();) compile_unit(units[local[k]]);
             });
         for (auto &th : pool) th.join();
     }
@@ -1950,33 +2080,8 @@ int jit_prepare(Plan &P, int device, std::string &err) {
     cudaFree(nullptr);  // make the primary context current for the driver API
     std::lock_guard<std::mutex> lk(g_cache_mu);
     for (int i : todo) {
-        Unit &u = units[i];
-        if (u.cubin.empty()) {
-            err = "NVRTC failed for " + u.name + " " + std::to_string(u.index) + ": " + u.log;
-            return QSV_E_DEVICE;
-        }
-        CUmodule mod;
-        CUfunction fn;
-        CUresult r = drv.ModuleLoadData(&mod, u.cubin.data());
-        if (r == CUDA_SUCCESS) r = drv.ModuleGetFunction(&fn, mod, u.name.c_str());
-        const int gang = u.super ? 1 : source_gang(u.src);
-        const int smem = gang * (int)((size_t)(jit_double_buffer() ? 32 : 16) << u.m);  // tile buffer(s)
-        if (r == CUDA_SUCCESS) r = drv.FuncSetAttribute(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem);
-        int per_sm = 0;
-        if (r == CUDA_SUCCESS)
-            r = drv.OccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn,
-                                                              gang << (u.m - (u.super ? P.r : pass_r(P, u.index))),
-                                                              (size_t)smem);
-        if (r != CUDA_SUCCESS || per_sm < 1) {
-            const char *s = nullptr;
-            if (r != CUDA_SUCCESS) drv.GetErrorString(r, &s);
-            err = std::string("loading specialised kernel: ") + (s ? s : "zero occupancy");
-            return QSV_E_DEVICE;
-        }
-        // QSV_JIT_CTAS_PER_SM (diagnostic): cap the persistent grid's CTAs per SM
-        if (const char *c = std::getenv("QSV_JIT_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(c)));
-        found[i] = CacheEntry{fn, per_sm * sms, gang};
-        g_cache[{device, u.src}] = found[i];
+        const int rc = load_unit(P, units[i], device, found[i], err);
+        if (rc) return rc;
     }
     P.jit_funcs.assign(P.passes.size(), nullptr);
     P.jit_grids.assign(P.passes.size(), 0);
@@ -1994,6 +2099,83 @@ int jit_prepare(Plan &P, int device, std::string &err) {
         }
     }
     P.jit_device = device;
+    return QSV_OK;
+}
+
+void jit_wait_async() {
+    AsyncPool &A = apool();
+    std::unique_lock<std::mutex> lk(A.mu);
+    A.cv.wait(lk, [&] { return A.queue.empty() && A.active == 0; });
+}
+
+bool jit_ready(const Plan &P, int device) { return P.jit_device == device && P.jit_funcs.size() == P.passes.size(); }
+
+int jit_start_async(Plan &P, int device, std::string &err) {
+    if (jit_ready(P, device)) return QSV_OK;
+    if (!jit_available(err)) return QSV_E_DEVICE;
+    if (P.jit_part_src.size() != P.passes.size()) {
+        P.jit_part_src.clear();
+        for (size_t i = 0; i < P.passes.size(); ++i) P.jit_part_src.push_back(jit_source(P, (int)i));
+        P.jit_part_funcs.assign(P.passes.size(), nullptr);
+        P.jit_part_grids.assign(P.passes.size(), 0);
+    }
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    // last passes first: the first ones run interpreted on a cold call anyway, the
+    // late (often light, quick to compile) ones may be ready when the GPU gets there
+    for (size_t i = P.passes.size(); i-- > 0;) {
+        if (P.jit_part_funcs[i]) continue;
+        auto it = g_cache.find({device, P.jit_part_src[i]});
+        if (it != g_cache.end()) {
+            P.jit_part_funcs[i] = it->second.fn;
+            P.jit_part_grids[i] = it->second.grid;
+            continue;
+        }
+        async_submit(Unit{P.jit_part_src[i], "qsv_pass", {}, {}, P.passes[i].m, false, (int)i});
+    }
+    return QSV_OK;
+}
+
+int jit_try_pass(Plan &P, int pass, int device, bool *ready, std::string &err) {
+    *ready = false;
+    if (jit_ready(P, device)) {
+        *ready = true;
+        return QSV_OK;
+    }
+    if ((int)P.jit_part_funcs.size() <= pass) return QSV_OK;
+    if (!P.jit_part_funcs[pass]) {
+        auto job = async_take(P.jit_part_src[pass], false);
+        if (!job) {
+            // compiled by another caller (blocking jit_prepare) in the meantime?
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            auto it = g_cache.find({device, P.jit_part_src[pass]});
+            if (it == g_cache.end()) return QSV_OK;
+            P.jit_part_funcs[pass] = it->second.fn;
+            P.jit_part_grids[pass] = it->second.grid;
+        } else {
+            cudaSetDevice(device);
+            cudaFree(nullptr);
+            std::lock_guard<std::mutex> lk(g_cache_mu);
+            CacheEntry e;
+            const int rc = load_unit(P, job->u, device, e, err);
+            if (rc) return rc;
+            P.jit_part_funcs[pass] = e.fn;
+            P.jit_part_grids[pass] = e.grid;
+        }
+    }
+    *ready = true;
+    // every pass loaded: the plan becomes an ordinary prepared plan
+    bool all = true;
+    for (void *f : P.jit_part_funcs) all = all && f;
+    if (all && !use_supers(P)) {
+        P.jit_funcs = P.jit_part_funcs;
+        P.jit_grids = P.jit_part_grids;
+        P.jit_gangs.assign(P.passes.size(), 1);
+        for (size_t i = 0; i < P.passes.size(); ++i) P.jit_gangs[i] = source_gang(P.jit_part_src[i]);
+        P.jit_super_funcs.assign(P.supers.size(), nullptr);
+        P.jit_super_grids.assign(P.supers.size(), 0);
+        P.super_use.assign(P.supers.size(), 0);
+        P.jit_device = device;
+    }
     return QSV_OK;
 }
 
@@ -2115,30 +2297,48 @@ static int cu_fail(CUresult r, const char *what, std::string &err) {
     return QSV_E_DEVICE;
 }
 
+namespace {
+int launch_fn(const Plan &P, int pass, void *fnp, int grid_cap_in, int gang, void *psi, int n, cudaStream_t stream,
+              std::string &err, unsigned long long basis, const void *ptab);
+}
+
 int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
                unsigned long long basis, const void *ptab) {
+    const int gang = pass < (int)P.jit_gangs.size() ? P.jit_gangs[pass] : 1;
+    return launch_fn(P, pass, P.jit_funcs[pass], P.jit_grids[pass], gang, psi, n, stream, err, basis, ptab);
+}
+
+int jit_launch_partial(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
+                       unsigned long long basis, const void *ptab) {
+    return launch_fn(P, pass, P.jit_part_funcs[pass], P.jit_part_grids[pass], source_gang(P.jit_part_src[pass]), psi,
+                     n, stream, err, basis, ptab);
+}
+
+namespace {
+int launch_fn(const Plan &P, int pass, void *fnp, int grid_cap_in, int gang, void *psi, int n, cudaStream_t stream,
+              std::string &err, unsigned long long basis, const void *ptab) {
     const DevPass &dp = P.passes[pass];
     const int m = dp.m, T = 1 << (m - pass_r(P, pass));
     unsigned long long n_tiles = 1ull << (n - m);
-    const int gang = pass < (int)P.jit_gangs.size() ? P.jit_gangs[pass] : 1;
     // One CTA per tile (group) by default: measured faster than the persistent
     // grid (C2 70.7 -> 67.5 ms, QFT 48.5 -> 48.0, C5 1.03 -> 1.00 s) - freshly
     // scheduled CTAs keep the tiles in flight adjacent, and a kernel sharing the
     // GPU with another stream's kernels is not stuck with its early residents.
     // QSV_JIT_GRID_TILES=0 restores the persistent grid.
     const bool per_tile = jit_per_tile_grid();
-    const unsigned long long cap = per_tile ? 0x7fffffffull : (unsigned long long)P.jit_grids[pass];
+    const unsigned long long cap = per_tile ? 0x7fffffffull : (unsigned long long)grid_cap_in;
     const unsigned grid = (unsigned)std::min<unsigned long long>((n_tiles + gang - 1) / gang, cap);
     if (P.product && pass == 0 && !ptab) {
         err = "product-start pass launched without its factor tables";
         return QSV_E_UNSUPPORTED;
     }
     void *args[] = {&psi, &n_tiles, &basis, &ptab};
-    const CUresult r = driver().LaunchKernel((CUfunction)P.jit_funcs[pass], grid, 1, 1, gang * T, 1, 1,
+    const CUresult r = driver().LaunchKernel((CUfunction)fnp, grid, 1, 1, gang * T, 1, 1,
                                              gang * (unsigned)((size_t)(jit_double_buffer() ? 32 : 16) << m),
                                              (CUstream)stream, args, nullptr);
     return r == CUDA_SUCCESS ? QSV_OK : cu_fail(r, "cuLaunchKernel", err);
 }
+}  // namespace
 
 int jit_launch_super(const Plan &P, int si, void *psi, unsigned *bar, cudaStream_t stream, std::string &err) {
     const int m = P.m, T = 1 << (m - P.r), s = popc64(P.supers[si].mask), lb = super_batch(P);

@@ -89,6 +89,18 @@ int jit_launch(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, s
 Plan build_plan_start(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r,
                       bool product);
 
+// Cold calls (a plan whose kernels are not compiled yet): jit_start_async queues
+// every missing pass kernel on a background NVRTC pool and returns at once;
+// jit_try_pass loads pass `pass` if its kernel has finished compiling (*ready);
+// jit_launch_partial launches such a loaded pass.  Once every pass is loaded
+// the plan is an ordinary prepared plan (jit_ready).  Flat plans only.
+bool jit_ready(const Plan &P, int device);
+void jit_wait_async();  // blocks until no background compile is queued or running
+int jit_start_async(Plan &P, int device, std::string &err);
+int jit_try_pass(Plan &P, int pass, int device, bool *ready, std::string &err);
+int jit_launch_partial(const Plan &P, int pass, void *psi, int n, cudaStream_t stream, std::string &err,
+                       unsigned long long basis, const void *ptab);
+
 // register qubits (k = 0..R-1) of pass 0's first stage: the `regs` of product_tables
 std::vector<int> product_regs(const Plan &P);
 

@@ -430,6 +430,21 @@ __global__ void set_basis_kernel(double2 *psi, uint64_t size, uint64_t index) {
         psi[i] = make_double2(i == index ? 1.0 : 0.0, 0.0);
 }
 
+// Product state (x)_q v_q from 5-bit group tables (product_tables with no register
+// qubits): amplitude(i) = prod_g tab[32 g + ((i >> 5 g) & 31)].  The interpreted
+// first pass of a product-start plan reads this state (cold calls, execute_plan_mixed).
+__global__ void product_state_kernel(double2 *psi, uint64_t size, const double2 *__restrict__ tab, int groups) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < size; i += stride) {
+        double2 a = tab[i & 31];
+        for (int g = 1; g < groups; ++g) {
+            const double2 b = tab[32 * g + ((i >> (5 * g)) & 31)];
+            a = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+        }
+        psi[i] = a;
+    }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

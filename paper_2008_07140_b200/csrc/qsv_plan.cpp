@@ -22,6 +22,7 @@
 #include <bit>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 namespace qsv {
 
@@ -443,6 +444,44 @@ int rollout_passes(const std::vector<GateRec> &recs, std::vector<int> cur, uint6
     return cur.empty() ? passes : cap + 1;
 }
 
+// Modeled time of one pass in FP64-instructions-per-amplitude units: a pass costs
+// max(HBM floor, FP64 work); the floor (~65 FP64/amp on B200: 32 B/amp at ~6.9 TB/s
+// vs ~78 % of the DFMA rate) and the work (gate_work ~ 1.5 units per FP64/amp).
+double modeled_pass_time(const std::vector<GateRec> &recs, const std::vector<int> &taken) {
+    double w = 0;
+    for (int gi : taken) w += gate_work(recs[gi]);
+    return std::max(65.0, w / 1.5);
+}
+
+// QSV_PLAN_OBJECTIVE=time: the look-ahead minimises the summed modeled pass time of
+// the completion instead of the number of passes (heavy front passes + light tail
+// passes cost more than balanced ones of the same count)
+bool objective_time() {
+    static const bool v = [] {
+        const char *e = std::getenv("QSV_PLAN_OBJECTIVE");
+        return e && std::string(e) == "time";
+    }();
+    return v;
+}
+
+// Summed modeled time of the greedy completion of `cur` (stops above `cap`).
+double rollout_time(const std::vector<GateRec> &recs, std::vector<int> cur, uint64_t low, uint64_t all, int n, int m,
+                    double cap) {
+    double t = 0;
+    while (!cur.empty() && t <= cap) {
+        Absorber tile;
+        tile.resident = low;
+        tile.capacity = m;
+        for (int gi : cur) tile.offer(recs[gi]);
+        const uint64_t res = search_tile(recs, cur, padded_tile(tile.resident, all, n, m), low, n);
+        std::vector<int> tk, d;
+        scan_fixed_tile(recs, cur, res, &tk, &d);
+        t += modeled_pass_time(recs, tk);
+        cur.swap(d);
+    }
+    return cur.empty() ? t : cap + 1.0;
+}
+
 // Look-ahead tile choice (QSV_PLAN_ROLLOUT=K): among the best tile and its
 // single-swap neighbours absorbing at least 70 % as many gates, the K with the
 // most gates are completed greedily; the tile whose completion needs the fewest
@@ -470,11 +509,20 @@ uint64_t lookahead_tile(const std::vector<GateRec> &recs, const std::vector<int>
     std::vector<int> passes(cands.size(), 1 << 30);
     std::atomic<int> best_so_far{1 << 30};
     std::atomic<size_t> next{0};
+    const bool by_time = objective_time();
     auto work = [&] {
         for (size_t k; (k = next.fetch_add(1)) < cands.size();) {
             std::vector<int> t, d;
             scan_fixed_tile(recs, rem, cands[k].second, &t, &d);
-            const int p = rollout_passes(recs, d, fixed, all, n, m, best_so_far.load());
+            int p;
+            if (by_time) {
+                // modeled time in 1/16 units (ints keep the atomic pruning bound)
+                const double now = modeled_pass_time(recs, t);
+                const double rest = rollout_time(recs, d, fixed, all, n, m, best_so_far.load() / 16.0 - now);
+                p = (int)std::min(1e9, 16.0 * (now + rest));
+            } else {
+                p = rollout_passes(recs, d, fixed, all, n, m, best_so_far.load());
+            }
             passes[k] = p;
             for (int cur = best_so_far.load(); p < cur && !best_so_far.compare_exchange_weak(cur, p);) {
             }

@@ -130,6 +130,11 @@ struct Plan {
     // (+ the plan's output, always 1); filled on first use by qsv_jit.cpp
     mutable std::vector<double> jit_scale_in;
     int jit_device = -1;
+    // kernels of a plan still compiling asynchronously (jit_start_async): per-pass
+    // sources and the passes loaded so far
+    std::vector<std::string> jit_part_src;
+    std::vector<void *> jit_part_funcs;
+    std::vector<int> jit_part_grids;
     // product-state start (qsv_options.product_start): the leading single-qubit
     // gates of every qubit (each before any other gate touching that qubit) are
     // not in `recs`; they map a basis state |b> to the product state
