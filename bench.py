@@ -476,6 +476,12 @@ def run_partial_bench(args) -> None:
     popts = planner_options(args)
     for _ in range(args.warmup):
         run_partial(prog, cut, targets, device=local, options=popts)
+    # the first call's kernels compile in the background (interpreted meanwhile): the timed
+    # calls are warm
+    from paper_2008_07140_b200 import _native as N
+
+    N.check(N.lib().qsv_jit_wait())
+    run_partial(prog, cut, targets, device=local, options=popts)
     torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clk:
@@ -559,6 +565,10 @@ def run_noisy_bench(args) -> None:
 
     for w in range(args.warmup):
         once(10_000 + w)
+    from paper_2008_07140_b200 import _native as N
+
+    N.check(N.lib().qsv_jit_wait())  # background compiles of the first call done: timed calls are warm
+    once(10_100)
     torch.cuda.synchronize()
     times = []
     with ClockSampler(local) as clk:

@@ -1492,6 +1492,23 @@ constexpr double kPrefetchMinFp64 = 55.0;
 
 // The uniform scale each pass's kernel finds the state stored with (chained
 // through dry runs of the generator: pass i's last stage decides pass i+1's).
+// FP64 instructions per amplitude of every pass (the specialiser's cost model) from
+// one dry emission per pass, filling the uniform-scale chain on the way (the same
+// emission pass_scales runs; jit_source's own dry run gives the same numbers).
+std::vector<double> pass_costs(const Plan &P) {
+    const size_t np = P.passes.size();
+    std::vector<double> sc(np + 1, 1.0), cost(np, 0.0);
+    for (size_t pi = 0; pi < np; ++pi) {
+        std::ostringstream dry;
+        const double f = emit_tile_loop(
+            dry, P, (int)pi, false, "n", [](const std::string &) { return std::string("0"); }, true, false, false,
+            sc[pi], pi + 1 == np, &sc[pi + 1]);
+        cost[pi] = f / (double)(1 << pass_r(P, (int)pi));
+    }
+    P.jit_scale_in = sc;
+    return cost;
+}
+
 const std::vector<double> &pass_scales(const Plan &P) {
     const size_t np = P.passes.size();
     if (P.jit_scale_in.size() != np + 1) {
@@ -1629,11 +1646,13 @@ Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int 
     const int np = (int)P5.passes.size();
     std::vector<int> rs(np, 5);
     int n4 = 0;
+    // both stagings' cost models at once (one dry emission per pass each)
+    std::vector<double> c4;
+    std::thread t4([&] { c4 = pass_costs(P4); });
+    const std::vector<double> c5 = pass_costs(P5);
+    t4.join();
     for (int i = 0; i < np; ++i) {
-        double c5 = 0, c4 = 0;
-        jit_source(P5, i, false, &c5);
-        jit_source(P4, i, false, &c4);
-        if (c4 <= kR4CostRatio * c5) {
+        if (c4[i] <= kR4CostRatio * c5[i]) {
             rs[i] = 4;
             ++n4;
         }

@@ -26,7 +26,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 def test_c3_mirror_returns_basis_state(n):
     need_device_gib(66)
     prog = parse_program(workloads.mirror_text(workloads.rqc_for_qubits(n, 24, 0)))
-    res = SV.run_full(prog, max_qubits=n)
+    res = SV.run_full(prog, max_qubits=n, jit=1)  # specialised kernels (product start)
     st = res.state
     try:
         a0 = np.empty(1, np.complex128)

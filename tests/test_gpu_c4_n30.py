@@ -28,8 +28,8 @@ def test_c4_n30_forward_and_round_trip():
     fwd_prog = parse_program(workloads.qft_text(N))
     rt_prog = parse_program(workloads.qft_text(N, round_trip=True))
     assert len(fwd_prog.gate_instructions()) == 480 and len(rt_prog.gate_instructions()) == 960
-    fwd = SV.run_full(fwd_prog, initial_state=psi0).state
-    rt = SV.run_full(rt_prog, initial_state=psi0).state
+    fwd = SV.run_full(fwd_prog, initial_state=psi0, jit=1).state
+    rt = SV.run_full(rt_prog, initial_state=psi0, jit=1).state
     check = SV.StateVector(N, psi0)
     try:
         assert_device_parity(rt, check, "C4 n=30 QFT + DAGGER-QFT round trip vs psi0")

@@ -463,3 +463,27 @@ def test_trajectories_fallback_when_plan_cannot_take_paulis(monkeypatch):
         ref = O.run_full(prog, np.random.default_rng(trajectory_seed(7, t)), noise=("depolarizing", 0.05))
         assert_parity(rep.kept[t], ref.state.amplitudes)
         assert np.abs(rep.tables[t] - O.pmeasure(ref.state, (0, 5, 11))).max() <= 1e-12
+
+
+def test_cold_call_runs_while_kernels_compile():
+    """The first run of a new circuit (jit auto) does not wait for NVRTC: passes whose
+    specialised kernel is still compiling run on the interpreted kernel (plus the scale op
+    the compiled chain expects), the product-start plan's first pass reads the state of
+    product_state_kernel; after qsv_jit_wait every pass runs compiled.  Both vs the oracle."""
+    from paper_2008_07140_b200 import _native as N
+
+    prog = parse_program(workloads.rqc_for_qubits(22, 16, 977))  # a circuit no other test compiles
+    ref = O.run_full(prog, workers=O.cpu_threads()).state.amplitudes
+    cold = SV.run_full(prog)
+    assert cold.stats["compiled_passes"] < cold.stats["passes"]
+    assert_parity(cold.state.amplitudes, ref)
+    cold.state.close()
+    N.check(N.lib().qsv_jit_wait())
+    warm = SV.run_full(prog)
+    assert warm.stats["compiled_passes"] in (0, warm.stats["passes"])  # 0: the plan was already fully loaded
+    assert_parity(warm.state.amplitudes, ref)
+    # an uploaded (non-basis) start: no product start, the same mixed/compiled machinery
+    psi0 = workloads.gaussian_state(22, 5)
+    prog2 = parse_program(workloads.rqc_for_qubits(22, 12, 978))
+    ref2 = O.run_full(prog2, initial=psi0).state.amplitudes
+    assert_parity(SV.run_full(prog2, initial_state=psi0).state.amplitudes, ref2)

@@ -33,7 +33,7 @@ def _worker(rank, world, port, out, transport):
     try:
         prog = parse_program(workloads.rqc_for_qubits(N_QUBITS, 24, 3))
         g = world.bit_length() - 1
-        shard = CudaShard(N_QUBITS - g, 0, options=N.options())
+        shard = CudaShard(N_QUBITS - g, 0, options=N.options(jit=1))
         tr = make_transport(transport, dist, shard)
         sim = ShardedSimulator(N_QUBITS, shard, transport=tr)
         sim.set_basis(0)
@@ -46,7 +46,7 @@ def _worker(rank, world, port, out, transport):
         dist.barrier()
         shard.close()
         if rank == 0:
-            ref = SV.run_full(prog)
+            ref = SV.run_full(prog, jit=1)
             diff, dot, nn, rr = 0.0, 0.0j, 0.0, 0.0
             want = np.empty(1 << 24, np.complex128)
             for s in range(0, amps.size, want.size):

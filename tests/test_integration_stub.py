@@ -34,7 +34,8 @@ class _HostLib:
     def __init__(self):
         self.states = {}
         self.next = 1
-        for name in ("qsv_create", "qsv_run", "qsv_download", "qsv_destroy", "qsv_last_error"):
+        for name in ("qsv_create", "qsv_run", "qsv_download", "qsv_destroy", "qsv_last_error",
+                     "qsv_state_last_error"):
             # plain functions (the stub sets .argtypes / .restype on them, as on ctypes symbols)
             bound = getattr(self, "_" + name)
             setattr(self, name, (lambda f: lambda *a: f(*a))(bound))
@@ -65,6 +66,9 @@ class _HostLib:
         return 0
 
     def _qsv_last_error(self):
+        return b""
+
+    def _qsv_state_last_error(self, h):
         return b""
 
 
