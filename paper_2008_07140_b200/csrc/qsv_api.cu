@@ -197,7 +197,7 @@ int configure_pass_kernel(int *per_sm, size_t smem, int threads) {
 
 template <int R>
 int launch_pass_r(qsv_state *st, const Plan &P, int pass_idx, const DevPass *pp, const DevStage *d_st,
-                  const DevOp *d_ops, uint64_t n_tiles, int threads) {
+                  const DevOp *d_ops, uint64_t n_tiles, int threads, const double2 *ptab) {
     const DevPass &hp = P.passes[pass_idx];
     const size_t n_ops = (size_t)(P.stages[hp.stage_end - 1].op_end - P.stages[hp.stage_begin].op_begin);
     const size_t ops_bytes = n_ops * sizeof(DevOp);
@@ -212,23 +212,28 @@ int launch_pass_r(qsv_state *st, const Plan &P, int pass_idx, const DevPass *pp,
     // early leave their tiles to a few; the op records come from L2)
     (void)per_sm;
     const uint64_t grid = std::min<uint64_t>(n_tiles, 0x7fffffffull);
-    if (so) pass_kernel<R, true><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles);
-    else pass_kernel<R, false><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles);
+    const int groups = (st->n + 4) / 5;
+    if (so)
+        pass_kernel<R, true><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles, ptab,
+                                                                          groups);
+    else
+        pass_kernel<R, false><<<(unsigned)grid, threads, smem, st->stream>>>(st->amps, pp, d_st, d_ops, n_tiles, ptab,
+                                                                           groups);
     return QSV_OK;
 }
 
 int launch_pass(qsv_state *st, const Plan &P, int pass_idx, const DevPass *d_pass, const DevStage *d_st,
-                const DevOp *d_ops) {
+                const DevOp *d_ops, const double2 *ptab = nullptr) {
     const int m = P.m, r = P.r;
     const uint64_t n_tiles = 1ull << (st->n - m);
     const int threads = 1 << (m - r);
     const DevPass *pp = d_pass + pass_idx;
     int rc = QSV_OK;
     switch (r) {
-        case 1: rc = launch_pass_r<1>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
-        case 2: rc = launch_pass_r<2>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
-        case 3: rc = launch_pass_r<3>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
-        case 4: rc = launch_pass_r<4>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads); break;
+        case 1: rc = launch_pass_r<1>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads, ptab); break;
+        case 2: rc = launch_pass_r<2>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads, ptab); break;
+        case 3: rc = launch_pass_r<3>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads, ptab); break;
+        case 4: rc = launch_pass_r<4>(st, P, pass_idx, pp, d_st, d_ops, n_tiles, threads, ptab); break;
         default: return fail(QSV_E_UNSUPPORTED, "register qubits must be 1..4");
     }
     if (rc) return rc;
@@ -410,8 +415,9 @@ int upload_product_tables(qsv_state *st, const Plan &P, const std::vector<int> &
 // that leaves the state as compiled pass j+1 expects (stored = true / scale, as in
 // execute_with_paulis).  Before enqueueing a pass whose kernel is not ready the
 // host waits until it is, or until the GPU has finished pass j-1 (the GPU never
-// idles for it; a late pass gets the longest time to finish compiling).  A product-start plan's interpreted first pass
-// reads the product state written by product_state_kernel.
+// idles for it; a late pass gets the longest time to finish compiling).  A
+// product-start plan's interpreted first pass synthesises the product state as it
+// loads its tiles (pass_kernel with the factor tables).
 int execute_plan_mixed(qsv_state *st, Plan &P, const qsv_options *opt, qsv_run_stats *stats) {
     std::string err;
     const int np = (int)P.passes.size();
@@ -459,17 +465,14 @@ int execute_plan_mixed(qsv_state *st, Plan &P, const qsv_options *opt, qsv_run_s
             st->pending_basis = -1;
             ++compiled;
         } else {
+            const double2 *synth = nullptr;
             if (j == 0 && P.product) {
+                // the interpreted first pass synthesises the product state as it loads its tiles
                 rc = upload_product_tables(st, P, {});
                 if (rc) break;
-                tm.begin();
-                product_state_kernel<<<grid_for(st->size(), 256, st->sm_count), 256, 0, st->stream>>>(
-                    st->amps, st->size(), st->ptab, (P.n + 4) / 5);
-                tm.end(0.5 * full);
-                CUDA_TRY(cudaGetLastError());
+                synth = st->ptab;
                 st->pending_basis = -1;
-                alg_bytes += 0.5 * full;
-                ++launches;
+                b = 0.5 * full;
             } else {
                 rc = materialize(st);
                 if (rc) break;
@@ -496,8 +499,8 @@ int execute_plan_mixed(qsv_state *st, Plan &P, const qsv_options *opt, qsv_run_s
             if (!rc) rc = upload_plan(st, Q, st->plan_buf, &dp, &ds, &dop);
             if (rc) break;
             tm.begin();
-            rc = launch_pass(st, Q, 0, dp, ds, dop);
-            tm.end(full);
+            rc = launch_pass(st, Q, 0, dp, ds, dop, synth);
+            tm.end(b);
             if (rc) break;
         }
         cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming);

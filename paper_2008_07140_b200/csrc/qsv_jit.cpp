@@ -1754,6 +1754,13 @@ size_t spill_bytes(const std::string &log) {
     return total;
 }
 constexpr size_t kMaxSpillBytes = 128;
+// QSV_JIT_MAX_SPILL (diagnostic): spill bytes a three-CTA kernel may keep before it is
+// recompiled for two CTAs per SM
+size_t max_spill_bytes() {
+    static const size_t v = std::getenv("QSV_JIT_MAX_SPILL") ? (size_t)std::atol(std::getenv("QSV_JIT_MAX_SPILL"))
+                                                             : kMaxSpillBytes;
+    return v;
+}
 
 // QSV_NVRTC_FAST=min|mid (diagnostic): NVRTC --Ofast-compile level (cuts front-end time,
 // slightly different code); part of the disk-cache key
@@ -1926,7 +1933,7 @@ void compile_unit(Unit &u) {
     u.cubin = jit_compile_cubin(u.src, u.log);
     const std::string three = "__launch_bounds__(128, 3)";
     const size_t at = u.src.find(three);
-    if (!u.cubin.empty() && at != std::string::npos && spill_bytes(u.log) > kMaxSpillBytes) {
+    if (!u.cubin.empty() && at != std::string::npos && spill_bytes(u.log) > max_spill_bytes()) {
         std::string src2 = u.src;
         src2.replace(at, three.size(), "__launch_bounds__(128, 2)");
         std::string log2;
@@ -2056,12 +2063,33 @@ int load_unit(const Plan &P, Unit &u, int device, CacheEntry &out, std::string &
 
 }  // namespace
 
+// The pass kernels' sources, generated on up to 16 host threads (the uniform-scale
+// chain is filled first; jit_source is then read-only on the plan).
+std::vector<std::string> pass_sources(const Plan &P) {
+    const size_t np = P.passes.size();
+    std::vector<std::string> src(np);
+    pass_scales(P);
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t k; (k = next.fetch_add(1)) < np;) src[k] = jit_source(P, (int)k);
+    };
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 1; t < std::min<size_t>(hw, np); ++t) pool.emplace_back(work);
+    work();
+    for (auto &th : pool) th.join();
+    return src;
+}
+
 int jit_prepare(Plan &P, int device, std::string &err) {
     if (P.jit_device == device && P.jit_funcs.size() == P.passes.size()) return QSV_OK;
     if (!jit_available(err)) return QSV_E_DEVICE;
     std::vector<Unit> units;
-    for (size_t i = 0; i < P.passes.size(); ++i)
-        units.push_back(Unit{jit_source(P, (int)i), "qsv_pass", {}, {}, P.passes[i].m, false, (int)i});
+    {
+        std::vector<std::string> src = P.jit_part_src.size() == P.passes.size() ? P.jit_part_src : pass_sources(P);
+        for (size_t i = 0; i < P.passes.size(); ++i)
+            units.push_back(Unit{std::move(src[i]), "qsv_pass", {}, {}, P.passes[i].m, false, (int)i});
+    }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     jit_choose_supers(P, sms);
@@ -2133,8 +2161,7 @@ int jit_start_async(Plan &P, int device, std::string &err) {
     if (jit_ready(P, device)) return QSV_OK;
     if (!jit_available(err)) return QSV_E_DEVICE;
     if (P.jit_part_src.size() != P.passes.size()) {
-        P.jit_part_src.clear();
-        for (size_t i = 0; i < P.passes.size(); ++i) P.jit_part_src.push_back(jit_source(P, (int)i));
+        P.jit_part_src = pass_sources(P);
         P.jit_part_funcs.assign(P.passes.size(), nullptr);
         P.jit_part_grids.assign(P.passes.size(), 0);
     }

@@ -311,10 +311,23 @@ __device__ __forceinline__ void apply_op(const DevOp *op, double2 (&v)[1 << R], 
 // SMEM_OPS: the pass's op records are staged in shared memory once per
 // (persistent) CTA and read as uniform broadcasts (global L1 reads per op and
 // thread were the interpreter's main stall, long_scoreboard ~4 per issue)
+// product-state amplitude from the 5-bit group tables (product_state_kernel's rule)
+__device__ __forceinline__ double2 product_amp(const double2 *__restrict__ tab, int groups, uint64_t i) {
+    double2 a = tab[i & 31];
+    for (int g = 1; g < groups; ++g) {
+        const double2 b = tab[32 * g + ((i >> (5 * g)) & 31)];
+        a = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    }
+    return a;
+}
+
+// ptab != nullptr: the tile is synthesised as the product state of those tables
+// instead of read (the interpreted first pass of a product-start plan on a cold call)
 template <int R, bool SMEM_OPS>
 __global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, const DevPass *__restrict__ pass,
                                                    const DevStage *__restrict__ stages,
-                                                   const DevOp *__restrict__ ops_g, uint64_t n_tiles) {
+                                                   const DevOp *__restrict__ ops_g, uint64_t n_tiles,
+                                                   const double2 *__restrict__ ptab, int groups) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int m = pass->m;
     const uint32_t nloc = 1u << m;
@@ -341,8 +354,14 @@ __global__ void __launch_bounds__(512) pass_kernel(double2 *__restrict__ psi, co
         uint64_t base = tile_id;
         for (int j = 0; j < m; ++j) base = insert_zero(base, pass->tq[j]);
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nloc; i += T)
-            tile[swz(i)] = __ldcs(psi + base + (lo_tab[i & ((1u << kLoTabBits) - 1)] | hi_tab[i >> kLoTabBits]));
+        if (ptab) {
+            for (uint32_t i = threadIdx.x; i < nloc; i += T)
+                tile[swz(i)] = product_amp(ptab, groups,
+                                           base + (lo_tab[i & ((1u << kLoTabBits) - 1)] | hi_tab[i >> kLoTabBits]));
+        } else {
+            for (uint32_t i = threadIdx.x; i < nloc; i += T)
+                tile[swz(i)] = __ldcs(psi + base + (lo_tab[i & ((1u << kLoTabBits) - 1)] | hi_tab[i >> kLoTabBits]));
+        }
         __syncthreads();
 
         for (int s = sb; s < se; ++s) {
