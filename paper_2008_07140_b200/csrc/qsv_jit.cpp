@@ -1498,14 +1498,19 @@ constexpr double kPrefetchMinFp64 = 55.0;
 std::vector<double> pass_costs(const Plan &P) {
     const size_t np = P.passes.size();
     std::vector<double> sc(np + 1, 1.0), cost(np, 0.0);
+    std::ostringstream *saved = g_decls;
     for (size_t pi = 0; pi < np; ++pi) {
-        std::ostringstream dry;
+        // with a declaration sink, as jit_source emits: per-thread factor tables replace
+        // computed products (fewer FP64), the scale chain is unaffected
+        std::ostringstream dry, decls;
+        g_decls = &decls;
+        g_decl_id = 0;
         const double f = emit_tile_loop(
             dry, P, (int)pi, false, "n", [](const std::string &) { return std::string("0"); }, true, false, false,
             sc[pi], pi + 1 == np, &sc[pi + 1]);
         cost[pi] = f / (double)(1 << pass_r(P, (int)pi));
     }
-    P.jit_scale_in = sc;
+    g_decls = saved;
     return cost;
 }
 
@@ -1636,6 +1641,7 @@ std::string jit_source(const Plan &P, int pi, bool host, double *fp64_per_amp, u
 // stagings of the same passes are generated and each pass takes r = 4 when its
 // FP64 work per amplitude is within kR4CostRatio of the r = 5 staging.
 constexpr double kR4CostRatio = 1.10;
+constexpr double kR4LightFp64 = 65.0;
 
 Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s, bool auto_r) {
     Plan P5 = build_plan(recs, n, m, r, L, s);
@@ -1652,7 +1658,12 @@ Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int 
     const std::vector<double> c5 = pass_costs(P5);
     t4.join();
     for (int i = 0; i < np; ++i) {
-        if (c4[i] <= kR4CostRatio * c5[i]) {
+        // light passes (memory- or latency-bound) also take r = 4 when its FP64 work stays
+        // below the HBM floor: the 8-warp r = 5 CTAs hide less latency (QFT passes 1 and 3,
+        // 59 vs 48 FP64/amp: 42.3 -> 41.4 ms); the last pass keeps r = 5 (measured slower at
+        // r = 4: it flushes the deferred scale)
+        const bool light = c4[i] <= kR4LightFp64 && i + 1 < np;
+        if (c4[i] <= kR4CostRatio * c5[i] || light) {
             rs[i] = 4;
             ++n4;
         }

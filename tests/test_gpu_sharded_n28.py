@@ -62,7 +62,7 @@ def _worker(rank, world, port, out, transport):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,transport", [(2, "p2p"), (4, "p2p"), (2, "alltoall")])
+@pytest.mark.parametrize("world,transport", [(2, "p2p"), (4, "p2p"), (8, "p2p"), (2, "alltoall")])
 def test_sharded_n28_matches_unsharded(world, transport, tmp_path):
     import socket
 
