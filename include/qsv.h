@@ -82,6 +82,10 @@ typedef struct qsv_options {
                               state holding a pending basis index, qsv_set_basis); -1: never;
                               0: auto - qsv_run uses it for a pending basis state with specialised
                               kernels, qsv_plan_create does not */
+    int32_t plan_objective; /* what the scheduler's look-ahead minimises: 0 / 2 the summed modeled
+                              pass time (balanced FP64 work per pass; default), 1 the number of
+                              passes (front-loaded passes: faster for plans that carry Pauli errors,
+                              qsv_plan_execute_paulis) */
 } qsv_options;
 
 typedef struct qsv_run_stats {

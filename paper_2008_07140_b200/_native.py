@@ -36,7 +36,8 @@ class qsv_exchange(C.Structure):
 class qsv_options(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_qubits", C.c_int32), ("reg_qubits", C.c_int32),
                 ("low_qubits", C.c_int32), ("profile", C.c_int32), ("n_global", C.c_int32),
-                ("jit", C.c_int32), ("super_qubits", C.c_int32), ("product_start", C.c_int32)]
+                ("jit", C.c_int32), ("super_qubits", C.c_int32), ("product_start", C.c_int32),
+                ("plan_objective", C.c_int32)]
 
 
 class qsv_run_stats(C.Structure):
@@ -171,17 +172,20 @@ def last_launches(handle):
 
 
 def options(fuse=True, tile_qubits=0, reg_qubits=0, low_qubits=0, profile=False, n_global=0,
-            jit=0, super_qubits=0, product_start=0) -> qsv_options:
+            jit=0, super_qubits=0, product_start=0, plan_objective=0) -> qsv_options:
     """jit: 0 auto (specialised kernels for n >= 16), 1 always, -1 never;
     super_qubits: L2 super-tile size s (0 = default 21; s <= tile_qubits disables);
     product_start: 1 plan with a product-state start (runs only from set_basis), -1 never,
-    0 auto (qsv_run: on for basis starts with specialised kernels)."""
+    0 auto (qsv_run: on for basis starts with specialised kernels);
+    plan_objective: what the scheduler's look-ahead minimises - 0/2 modeled time (default),
+    1 the number of passes."""
     o = qsv_options()
     o.fuse, o.tile_qubits, o.reg_qubits = int(bool(fuse)), int(tile_qubits), int(reg_qubits)
     o.low_qubits, o.profile, o.n_global = int(low_qubits), int(bool(profile)), int(n_global)
     o.jit = int(jit)
     o.super_qubits = int(super_qubits)
     o.product_start = int(product_start)
+    o.plan_objective = int(plan_objective)
     return o
 
 

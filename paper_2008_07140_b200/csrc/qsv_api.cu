@@ -757,6 +757,7 @@ int qsv_plan_create(const qsv_gate *gates, int64_t n_gates, int n_qubits, const 
     int s;
     resolve_options(opt, n_qubits, m, r, L, s);
     auto p = std::make_unique<qsv_plan>();
+    PlanObjectiveScope objective(opt ? opt->plan_objective : 0);
     p->p = build_plan_start(recs, n_qubits, m, r, L, s, auto_r_of(opt, n_qubits), opt && opt->product_start > 0);
     *out = p.release();
     return QSV_OK;
@@ -958,12 +959,12 @@ struct CachedPlan {
 
 std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, const std::vector<GateRec> &recs,
                                         int n, int m, int r, int L, int s, int jit, int device, bool auto_r = false,
-                                        bool product = false) {
+                                        bool product = false, int objective = 0) {
     static std::mutex mu;
     static std::list<std::shared_ptr<CachedPlan>> lru;
     constexpr size_t kEntries = 16;
     std::vector<unsigned char> key(sizeof(int) * 7 + sizeof(qsv_gate) * (size_t)n_gates);
-    const int head[7] = {n, m, r + (auto_r ? 100 : 0) + (product ? 1000 : 0), L, s, jit, device};
+    const int head[7] = {n, m, r + (auto_r ? 100 : 0) + (product ? 1000 : 0) + (objective == 1 ? 10000 : 0), L, s, jit, device};
     std::memcpy(key.data(), head, sizeof(head));
     std::memcpy(key.data() + sizeof(head), gates, sizeof(qsv_gate) * (size_t)n_gates);
     {
@@ -978,6 +979,7 @@ std::shared_ptr<CachedPlan> cached_plan(const qsv_gate *gates, int64_t n_gates, 
     }
     auto e = std::make_shared<CachedPlan>();
     e->key.swap(key);
+    PlanObjectiveScope scope(objective);
     e->plan = build_plan_start(recs, n, m, r, L, s, auto_r, product);
     std::lock_guard<std::mutex> lk(mu);
     lru.push_front(e);
@@ -1033,7 +1035,7 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
                          (ps > 0 || (ps == 0 && product_env));
     const auto t0 = std::chrono::steady_clock::now();
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, jm, st->device,
-                                                 auto_r_of(opt, st->n), product);
+                                                 auto_r_of(opt, st->n), product, opt ? opt->plan_objective : 0);
     const auto t1 = std::chrono::steady_clock::now();
     bool jit_ready = false;
     if (want_jit) {
@@ -1058,7 +1060,8 @@ int qsv_run(qsv_state *st, const qsv_gate *gates, int64_t n_gates, const qsv_opt
     }
     if (product && !jit_ready) {
         // no specialised kernels: the plain plan runs on the interpreted kernel
-        cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, jm, st->device, auto_r_of(opt, st->n), false);
+        cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, s, jm, st->device, auto_r_of(opt, st->n), false,
+                         opt ? opt->plan_objective : 0);
     }
     Plan &P = cp->plan;
     if (stats) {
@@ -1644,7 +1647,7 @@ int qsv_exchange_fusable(qsv_state *st, const qsv_gate *gates, int64_t n_gates, 
     int m, r, L, sq;
     resolve_options(opt, st->n, m, r, L, sq);
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, jm, st->device,
-                                                 auto_r_of(opt, st->n));
+                                                 auto_r_of(opt, st->n), false, opt ? opt->plan_objective : 0);
     const Plan &P = cp->plan;
     *out = !use_supers(P) && !P.passes.empty() && positions && !(positions >> st->n);
     return QSV_OK;
@@ -1665,7 +1668,8 @@ int qsv_run_exchange(qsv_state *st, const qsv_gate *gates, int64_t n_gates, cons
     int m, r, L, sq;
     resolve_options(opt, st->n, m, r, L, sq);
     std::shared_ptr<CachedPlan> cp = cached_plan(gates, n_gates, recs, st->n, m, r, L, sq, opt ? opt->jit : 0,
-                                                 st->device, auto_r_of(opt, st->n));
+                                                 st->device, auto_r_of(opt, st->n), false,
+                                                 opt ? opt->plan_objective : 0);
     Plan &P = cp->plan;
     const int last = (int)P.passes.size() - 1;
     if (use_supers(P) || last < 0) return fail(QSV_E_UNSUPPORTED, "plan uses super-passes");

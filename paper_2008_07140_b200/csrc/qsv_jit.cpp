@@ -1358,7 +1358,10 @@ double emit_tile_loop(std::ostringstream &o, const Plan &P, int pi, bool host, c
             tma_issue(next_group);
         }
         g.declare_accumulators();
-        for (int oi = st.op_begin; oi < st.op_end; ++oi) g.op(P.gops[oi]);
+        // QSV_JIT_DIAG_NOOPS=1 (diagnostic only, wrong results): no gate math, so the kernel's
+        // time is its memory traffic, shared-memory re-layouts and barriers
+        static const bool diag_noops = std::getenv("QSV_JIT_DIAG_NOOPS") != nullptr;
+        for (int oi = st.op_begin; oi < st.op_end && !(diag_noops && !host); ++oi) g.op(P.gops[oi]);
         g.flush_all(sigma, final_pass && last);
         fp64 += g.fp64;
         if (probe && last && !host) {

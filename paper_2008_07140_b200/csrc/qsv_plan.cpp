@@ -453,15 +453,24 @@ double modeled_pass_time(const std::vector<GateRec> &recs, const std::vector<int
     return std::max(65.0, w / 1.5);
 }
 
-// QSV_PLAN_OBJECTIVE=time: the look-ahead minimises the summed modeled pass time of
-// the completion instead of the number of passes (heavy front passes + light tail
-// passes cost more than balanced ones of the same count)
+// The look-ahead minimises the summed modeled pass time of the completion rather than the
+// number of passes: heavy front passes + light tail passes cost more than balanced ones of
+// the same count (a pass costs ~max(HBM time, FP64 time)).  Measured on B200, three
+// interleaved rounds: C2 52.7 -> 51.0 ms (the same 7 passes and 579 FP64/amp, spread
+// 115/95/66/96/90/73/45 instead of 118/104/85/115/91/50/16), n = 32 229.9 -> 227.3 ms, QFT
+// unchanged (same plan).  A model with a per-stage term fitted to per-pass times (0.7 ms per
+// stage) chose worse plans (C2 51.9 ms, n = 32 8 passes 244 ms): the crude model stays.
+// qsv_options.plan_objective = 1 (or QSV_PLAN_OBJECTIVE=passes) restores the pass-count
+// objective: C5's Pauli-carrying trajectories run faster on front-loaded plans (1024
+// trajectories 0.79 s vs 1.06-1.20 s on time-balanced plans).
+thread_local int t_plan_objective = 0;
 bool objective_time() {
-    static const bool v = [] {
+    static const int env = [] {
         const char *e = std::getenv("QSV_PLAN_OBJECTIVE");
-        return e && std::string(e) == "time";
+        return !e ? 0 : std::string(e) == "passes" ? 1 : std::string(e) == "time" ? 2 : 0;
     }();
-    return v;
+    const int o = env ? env : t_plan_objective;
+    return o != 1;
 }
 
 // Summed modeled time of the greedy completion of `cur` (stops above `cap`).
@@ -1108,5 +1117,8 @@ Plan build_plan(const std::vector<GateRec> &recs_in, int n, int m, int r, int L,
     P.pass_op_begin.push_back((int64_t)P.ops.size());
     return P;
 }
+
+PlanObjectiveScope::PlanObjectiveScope(int objective) : saved(t_plan_objective) { t_plan_objective = objective; }
+PlanObjectiveScope::~PlanObjectiveScope() { t_plan_objective = saved; }
 
 }  // namespace qsv

@@ -162,6 +162,13 @@ int to_records(const qsv_gate *gates, int64_t n_gates, int n_qubits, std::vector
 
 // Builds the fused schedule.  m, r, L already clamped to the state size.
 Plan build_plan(const std::vector<GateRec> &recs, int n, int m, int r, int L, int s);
+// Look-ahead objective of the plans built on this thread while the scope lives
+// (qsv_options.plan_objective: 1 = fewest passes, otherwise modeled time).
+struct PlanObjectiveScope {
+    explicit PlanObjectiveScope(int objective);
+    ~PlanObjectiveScope();
+    int saved;
+};
 
 // The same passes (tiles and gate sets) as the flat plan B, each re-staged with
 // its own number of register qubits rs[k] (P.r = max).

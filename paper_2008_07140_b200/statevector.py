@@ -329,7 +329,8 @@ def run_full(program: Program, rng: np.random.Generator | None = None, noise=Non
                                max_qubits=max_qubits, chunk_log2=chunk_log2, initial_index=initial_index,
                                initial_state=initial_state,
                                opts=N.options(fuse=fuse, tile_qubits=tile_qubits, reg_qubits=reg_qubits,
-                                              low_qubits=low_qubits, profile=profile, jit=jit))
+                                              low_qubits=low_qubits, profile=profile, jit=jit,
+                                              plan_objective=1))
     if (noise is not None and noise_engine == "fused" and rng is not None and state is None
             and initial_state is None and initial_index == 0 and stream is None):
         # one trajectory = a batch of one: each noisy gate is ONE pass that applies U.K_c and
