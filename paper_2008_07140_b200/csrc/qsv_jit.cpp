@@ -453,8 +453,81 @@ struct StageGen {
         } else {
             thr.clear();
         }
+        // factors over tile-external bits only are uniform over the CTA: groups of up to six
+        // external qubits fold into one table indexed by those bits of the tile's base index,
+        // one load and one complex multiply per group instead of a select + multiply per
+        // control qubit (QFT: the CR phases of the 18 external controls of a register target
+        // were 216 of the middle pass's 468 complex multiplies per thread and every FSEL)
+        std::vector<const PendFactor *> ext;
+        for (const PendFactor &f : it->second) {
+            bool only = f.ccond.empty() && !f.sq.empty() && f.sq.size() <= 6;
+            for (int q : f.sq) only &= thread_bit.count(q) == 0;
+            if (only) ext.push_back(&f);
+        }
+        if (g_decls && ext.size() >= 2) {
+            std::vector<const PendFactor *> order = ext;
+            std::stable_sort(order.begin(), order.end(), [](const PendFactor *a, const PendFactor *b) {
+                return *std::min_element(a->sq.begin(), a->sq.end()) < *std::min_element(b->sq.begin(), b->sq.end());
+            });
+            std::vector<std::pair<std::vector<int>, std::vector<const PendFactor *>>> chunks;
+            for (const PendFactor *f : order) {
+                bool placed = false;
+                if (!chunks.empty()) {
+                    std::vector<int> u = chunks.back().first;
+                    for (int q : f->sq)
+                        if (std::find(u.begin(), u.end(), q) == u.end()) u.push_back(q);
+                    if (u.size() <= 6) {
+                        chunks.back().first = u;
+                        chunks.back().second.push_back(f);
+                        placed = true;
+                    }
+                }
+                if (!placed) chunks.push_back({f->sq, {f}});
+            }
+            for (auto &ch : chunks) {
+                std::vector<int> &cq = ch.first;
+                std::sort(cq.begin(), cq.end());
+                const int nq = (int)cq.size();
+                std::vector<cd> tab((size_t)1 << nq, cd(1, 0));
+                for (int x = 0; x < (1 << nq); ++x)
+                    for (const PendFactor *f : ch.second) {
+                        int combo = 0;
+                        for (size_t si = 0; si < f->sq.size(); ++si) {
+                            const int pos = (int)(std::find(cq.begin(), cq.end(), f->sq[si]) - cq.begin());
+                            combo |= ((x >> pos) & 1) << si;
+                        }
+                        tab[x] *= f->val[combo];
+                    }
+                bool trivial = true;
+                for (const cd &c : tab) trivial &= snap(c) == cd(1, 0);
+                if (trivial) continue;
+                const std::string tname = "qtab" + std::to_string(g_decl_id++);
+                *g_decls << (host_render ? "static const double2 " : "__device__ const double2 ") << tname << "["
+                         << (1 << nq) << "] = {";
+                for (int x = 0; x < (1 << nq); ++x) {
+                    const cd c = snap(tab[x]);
+                    *g_decls << (x ? ", " : "") << "{" << lit(c.real()) << ", " << lit(c.imag()) << "}";
+                }
+                *g_decls << "};\n";
+                // index: bit i <-> external qubit cq[i]; contiguous qubits are one shift + mask
+                std::string idx;
+                if (cq.back() - cq.front() == nq - 1) {
+                    idx = "((unsigned)(base >> " + std::to_string(cq.front()) + ") & " + std::to_string((1 << nq) - 1) + "u)";
+                } else {
+                    for (int i = 0; i < nq; ++i)
+                        idx += (i ? " | " : "") + std::string("(((unsigned)(base >> ") + std::to_string(cq[i]) +
+                               ") & 1u) << " + std::to_string(i) + ")";
+                    idx = "(" + idx + ")";
+                }
+                o << "    " << name << " = cmulc(" << name << ", " << tname << "[" << idx << "]);\n";
+                fp64 += 4;
+            }
+        } else {
+            ext.clear();
+        }
         for (const PendFactor &f : it->second) {
             if (std::find(thr.begin(), thr.end(), &f) != thr.end()) continue;
+            if (std::find(ext.begin(), ext.end(), &f) != ext.end()) continue;
             const std::string e = select_from(f.sq, f.val);
             if (e == c2(cd(1, 0))) continue;
             const std::string g = f.ccond.empty() ? e : "((" + f.ccond + ") ? " + e + " : " + one + ")";
@@ -1665,7 +1738,13 @@ Plan build_plan_auto(const std::vector<GateRec> &recs, int n, int m, int r, int 
         // below the HBM floor: the 8-warp r = 5 CTAs hide less latency (QFT passes 1 and 3,
         // 59 vs 48 FP64/amp: 42.3 -> 41.4 ms); the last pass keeps r = 5 (measured slower at
         // r = 4: it flushes the deferred scale)
-        const bool light = c4[i] <= kR4LightFp64 && i + 1 < np;
+        // ... unless its tile spreads over 2^8 or more 2 MB pages (8+ tile qubits at positions
+        // >= 17): such a pass is bound by the latency of its scattered lines, which 32 loads per
+        // thread in flight cover better than 16 (QFT's first pass, tile 0-2 + 21-29: 8.4 ms at
+        // r = 5, 9.9 ms at r = 4, though r = 4 needs no more FP64 there)
+        int high = 0;
+        for (int q = 17; q < n; ++q) high += (int)((P5.passes[i].tile_mask >> q) & 1);
+        const bool light = c4[i] <= kR4LightFp64 && i + 1 < np && high < 8;
         if (c4[i] <= kR4CostRatio * c5[i] || light) {
             rs[i] = 4;
             ++n4;

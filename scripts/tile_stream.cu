@@ -33,6 +33,33 @@ __global__ void __launch_bounds__(256, 2) k_tile(double2 *psi, u64 tmask, u64 em
         __stcs(gp + c_koff[k], v[k]);
     }
 }
+// the same with two shared-memory re-layouts (transposes of the 16 x 256 thread/register grid)
+// and CTA barriers between the loads and the stores, as a 3-stage pass without math
+__global__ void __launch_bounds__(256, 2) k_tile_x(double2 *psi, u64 tmask, u64 emask) {
+    extern __shared__ double2 tile[];
+    double2 *gp = psi + deposit(blockIdx.x, emask) + c_toff[threadIdx.x];
+    double2 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __ldcs(gp + c_koff[k]);
+    const unsigned t = threadIdx.x;
+    for (int round = 0; round < 2; ++round) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tile[(k * 256 + t) ^ (k & 7)] = v[k];
+        __syncthreads();
+        // thread t takes slots of 16 other threads: (t & 15) * 256 + (t >> 4) * 16 + k
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const unsigned kk = t & 15u, tt = (t >> 4) * 16u + k;
+            v[k] = tile[(kk * 256 + tt) ^ (kk & 7)];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        v[k].x += 1.0;
+        __stcs(gp + c_koff[k], v[k]);
+    }
+}
 static u64 hdeposit(u64 v, u64 mask) {
     u64 out = 0;
     for (int bit = 0; mask; ++bit) {
@@ -84,7 +111,16 @@ int main() {
         float ms;
         cudaEventElapsedTime(&ms, e0, e1);
         ms /= 3;
-        printf("%-40s %.3f ms  %.0f GB/s\n", c.name, ms, 2.0 * (16.0 * (1ull << n)) / ms * 1e-6);
+        printf("%-40s %.3f ms  %.0f GB/s", c.name, ms, 2.0 * (16.0 * (1ull << n)) / ms * 1e-6);
+        cudaFuncSetAttribute(k_tile_x, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        k_tile_x<<<1u << (n - 12), 256, 65536>>>(psi, tm, em);
+        cudaEventRecord(e0);
+        for (int r = 0; r < 3; ++r) k_tile_x<<<1u << (n - 12), 256, 65536>>>(psi, tm, em);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        ms /= 3;
+        printf("   | with 2 smem re-layouts %.3f ms  %.0f GB/s\n", ms, 2.0 * (16.0 * (1ull << n)) / ms * 1e-6);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;

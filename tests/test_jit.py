@@ -257,3 +257,40 @@ def test_product_start_split_rules():
     only2q = parse_program("QINIT 3\nCZ 0,1\nCNOT 1,2\n")
     assert run_product_plan_host(compile_gates(only2q.gate_instructions()), 3, 0, tile_qubits=3, reg_qubits=2,
                                  low_qubits=1) is None
+
+
+@pytest.mark.parametrize("cfg", [dict(tile_qubits=5, reg_qubits=3, low_qubits=2), dict(tile_qubits=6, reg_qubits=4, low_qubits=3)])
+def test_external_control_phase_tables(cfg):
+    """Controlled phases whose controls lie outside the tile are uniform over a CTA: groups of
+    up to six external qubits become one table lookup per accumulator (csrc/qsv_jit.cpp,
+    materialize).  Scattered and contiguous external controls, more than six per target (two
+    tables), 1- and 2-qubit diagonals, against the oracle; the tables must appear in the source."""
+    rng = np.random.default_rng(77)
+    n = 15
+    items = []
+    h = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    for t in (0, 1, 3):
+        items.append((h, (t,), ()))
+        for c in (5, 6, 7, 8, 9, 10, 11, 12, 13, 14):      # contiguous run: two tables
+            items.append((np.diag([1, np.exp(1j * rng.uniform(0, 6))]), (t,), (c,)))
+        items.append((h, (t,), ()))
+    for t in (2, 4):
+        items.append((h, (t,), ()))
+        for c in (6, 9, 11, 14):                            # scattered controls
+            items.append((np.diag([1, np.exp(1j * rng.uniform(0, 6))]), (t,), (c,)))
+        items.append((np.diag(np.exp(1j * rng.uniform(0, 6, 4))), (t, 13), ()))   # 2-qubit diagonal, one end external
+        items.append((np.diag([1, np.exp(1j * rng.uniform(0, 6))]), (t,), (8, 12)))  # two external controls
+        items.append((h, (t,), ()))
+    recs = N.gate_records(items)
+    psi = workloads.gaussian_state(n, 5)
+    ref = O.OracleState(n, psi.copy(), 0)
+    for u, t, c in items:
+        O.apply_gate(ref, u, t, c)
+    out = run_plan_host(recs, n, psi, **cfg)
+    assert np.abs(out - ref.amplitudes).max() <= 1e-12
+    hnd = plan_handle(recs, n, **cfg)
+    try:
+        src = kernel_source(hnd, 0, False)
+    finally:
+        N.lib().qsv_plan_destroy(hnd)
+    assert "(unsigned)(base >> " in src and "qtab" in src
