@@ -9,4 +9,4 @@ timeout 900 python bench.py --qubits 32 --steps 3 --warmup 3 --no-e2e --no-cpu-b
 timeout 900 python bench.py --workload traj > gpurun_out/bench_traj.json 2>> gpurun_out/bench_full.err; echo "traj rc=$?"
 timeout 900 python bench.py --workload partial > gpurun_out/bench_partial.json 2>> gpurun_out/bench_full.err; echo "partial rc=$?"
 timeout 900 python bench.py --workload noisy > gpurun_out/bench_noisy.json 2>> gpurun_out/bench_full.err; echo "noisy rc=$?"
-bash scripts/ncu_passes.sh "${NCU_PASSES:-0 3}"
+[ -n "$SKIP_NCU" ] || bash scripts/ncu_passes.sh "${NCU_PASSES:-0 3}"
