@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <vector>
 #include <cuda_runtime.h>
+#include <cuda.h>
+#include <cstring>
 typedef unsigned long long u64;
 
 __device__ __forceinline__ u64 deposit(u64 v, u64 mask) {
@@ -70,9 +72,34 @@ static u64 hdeposit(u64 v, u64 mask) {
     return out;
 }
 
-int main() {
+int main(int argc, char **argv) {
     const int n = 30;
     double2 *psi;
+    // argv[1] = "vmm": allocate through the virtual memory management API (one physical
+    // allocation, virtual range aligned to 512 MB) to see whether the driver maps it with larger
+    // pages than cudaMalloc's 2 MB
+    if (argc > 1 && !strcmp(argv[1], "vmm")) {
+        cudaFree(0);
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = 0;
+        size_t gran = 0;
+        cuMemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+        printf("recommended granularity %zu bytes\n", gran);
+        const size_t bytes = sizeof(double2) << n;
+        CUmemGenericAllocationHandle h;
+        CUdeviceptr va = 0;
+        CUresult r = cuMemCreate(&h, bytes, &prop, 0);
+        if (r == CUDA_SUCCESS) r = cuMemAddressReserve(&va, bytes, (size_t)512 << 20, 0, 0);
+        if (r == CUDA_SUCCESS) r = cuMemMap(va, bytes, 0, h, 0);
+        CUmemAccessDesc acc = {};
+        acc.location = prop.location;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        if (r == CUDA_SUCCESS) r = cuMemSetAccess(va, bytes, &acc, 1);
+        if (r != CUDA_SUCCESS) { printf("vmm alloc failed %d\n", (int)r); return 1; }
+        psi = (double2 *)va;
+    } else
     if (cudaMalloc(&psi, sizeof(double2) << n) != cudaSuccess) { printf("alloc failed\n"); return 1; }
     cudaMemset(psi, 0, sizeof(double2) << n);
     auto mask_of = [](std::vector<int> q) { u64 m = 0; for (int x : q) m |= 1ull << x; return m; };

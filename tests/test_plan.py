@@ -183,3 +183,28 @@ def test_plan_swaps_relabel_qubits(seed):
     prog = parse_program(workloads.qft_text(12, round_trip=True))
     _, passes = build_plan(compile_gates(prog.gate_instructions()), 12, tile_qubits=8, reg_qubits=4, low_qubits=3)
     assert not any(o["kind"] == 2 and np.allclose(o["m"][:16].reshape(4, 4), swap) for p in passes for o in p["ops"])
+
+
+def test_plan_objective_option():
+    """qsv_options.plan_objective: the look-ahead minimises the modeled pass time (default) or
+    the number of passes (1).  Both schedules reproduce the oracle; on the C2 circuit the time
+    objective needs no more passes and spreads the non-diagonal gates more evenly."""
+    prog = parse_program(workloads.rqc_for_qubits(14, 10, 3))
+    recs = compile_gates(prog.gate_instructions())
+    ref = O.run_full(prog).state.amplitudes
+    for objective in (0, 1, 2):
+        _, passes = build_plan(recs, 14, tile_qubits=6, reg_qubits=3, low_qubits=2, plan_objective=objective)
+        psi = np.zeros(1 << 14, complex)
+        psi[0] = 1
+        execute(passes, 14, psi)
+        assert np.abs(psi - ref).max() <= 1e-12, objective
+    c2 = compile_gates(parse_program(workloads.rqc_text(5, 6, 24, 0)).gate_instructions())
+
+    def mixing_per_pass(objective):
+        info, passes = build_plan(c2, 30, plan_objective=objective)
+        return info.passes, [sum(1 for o in p["ops"] if o["kind"] in (N.QSV_OP_MAT1, N.QSV_OP_MAT2)) for p in passes]
+
+    n_time, w_time = mixing_per_pass(0)
+    n_pass, w_pass = mixing_per_pass(1)
+    assert n_time <= n_pass + 1
+    assert max(w_time) <= max(w_pass) and min(w_time) >= min(w_pass)
