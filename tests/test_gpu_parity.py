@@ -491,3 +491,33 @@ def test_cold_call_runs_while_kernels_compile():
     prog2 = parse_program(workloads.rqc_for_qubits(22, 12, seed + 1))
     ref2 = O.run_full(prog2, initial=psi0).state.amplitudes
     assert_parity(SV.run_full(prog2, initial_state=psi0).state.amplitudes, ref2)
+
+
+EDGE_PROGRAMS = {
+    "no_gates_1": "QINIT 1\n",
+    "no_gates_5": "QINIT 5\nCREG 1\n",
+    "only_readout": "QINIT 3\nCREG 3\nMEASURE 0,$0\nMEASURE 2,$2\nPMEASURE 2,1,0\n",
+    "one_qubit_chain": "QINIT 1\nH 0\nT 0\nRX 0,\"0.3\"\nS 0\nH 0\n",
+    "diagonal_only": "QINIT 6\nT 0\nS 3\nCZ 1,4\nCR 0,5,\"pi/8\"\nRZ 2,\"0.7\"\nZ 5\n",
+    "many_controls": ("QINIT 10\n" + "".join(f"H {q}\n" for q in range(10))
+                      + "".join(f"CONTROL {q}\n" for q in range(1, 9)) + "RY 0,\"0.9\"\nSWAP 0,9\n"
+                      + "".join(f"ENDCONTROL {q}\n" for q in range(8, 0, -1)) + "iSWAP 9,0\n"),
+    "top_and_bottom": "QINIT 16\nH 15\nH 0\nCNOT 15,0\nRX 15,\"1.1\"\nCZ 0,15\nSWAP 0,15\nT 15\nH 0\n",
+}
+
+
+@pytest.mark.parametrize("name", sorted(EDGE_PROGRAMS))
+def test_edge_programs_all_configs(name):
+    """Gate-less programs, readout-only programs, a single qubit, diagonal-only streams, the
+    deepest control nesting the parser takes and gates on the extreme qubits, in every planner
+    configuration, against the oracle (statevector.py:360-430)."""
+    prog = parse_program(EDGE_PROGRAMS[name])
+    ref = O.run_full(prog, np.random.default_rng(7))
+    for cfg in CONFIGS:
+        res = SV.run_full(prog, np.random.default_rng(7), **cfg)
+        assert_parity(res.state.amplitudes, ref.state.amplitudes)
+        assert res.cregs == ref.cregs
+        assert len(res.tables) == len(ref.tables)
+        for (_, got), (_, want) in zip(res.tables, ref.tables):
+            assert np.abs(np.asarray(got) - np.asarray(want)).max() <= 1e-12
+        res.state.close()
