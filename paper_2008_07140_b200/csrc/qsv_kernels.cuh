@@ -288,7 +288,10 @@ __device__ __forceinline__ void apply_op(const DevOp *op, double2 (&v)[1 << R], 
     const uint4 h = *reinterpret_cast<const uint4 *>(op);
     const uint64_t ec = *(reinterpret_cast<const unsigned long long *>(op) + 2);
     const uint32_t code = h.x, rs = h.y, tc = h.z;
-    if ((tpart & tc) != tc || (base & ec) != ec) return;  // a scalar control is 0 for this thread
+    // most ops carry no scalar control: the test on the (CTA-uniform) record first keeps
+    // tpart / base, which the register allocator spills, out of the common path
+    if ((tc | (uint32_t)ec | (uint32_t)(ec >> 32)) != 0u)
+        if ((tpart & tc) != tc || (base & ec) != ec) return;  // a scalar control is 0 for this thread
     const uint32_t kind = code & 15, rc = rs & 0xff;
     const double *m = op->m;
     if (kind == K_MAT1) {
