@@ -294,3 +294,32 @@ def test_external_control_phase_tables(cfg):
     finally:
         N.lib().qsv_plan_destroy(hnd)
     assert "(unsigned)(base >> " in src and "qtab" in src
+
+
+def test_first_reading_pass_staggers_its_first_wave(monkeypatch):
+    """A plan's first pass that reads its input (>= 2^16 tiles) delays the second CTA of every
+    SM of its first residency wave (csrc/qsv_jit.cpp, kernel_head); later passes, small states,
+    product-start (synthesising) first passes and the host rendering do not; QSV_JIT_STAGGER=0
+    switches it off."""
+    monkeypatch.delenv("QSV_JIT_STAGGER", raising=False)
+
+    def sources(text, **opts):
+        prog = parse_program(text)
+        h = plan_handle(compile_gates(prog.gate_instructions()), prog.qubit_count, **opts)
+        try:
+            info = N.qsv_plan_info()
+            N.check(N.lib().qsv_plan_summary(h, C.byref(info)))
+            return [kernel_source(h, p, False) for p in range(info.passes)], kernel_source(h, 0, True)
+        finally:
+            N.lib().qsv_plan_destroy(h)
+
+    big, host0 = sources(workloads.qft_text(30, round_trip=False), product_start=-1)
+    assert len(big) >= 2 and "%nsmid" in big[0] and "clock64()" in big[0]
+    assert all("%nsmid" not in s for s in big[1:]) and "%nsmid" not in host0
+    small, _ = sources(workloads.qft_text(20, round_trip=False), product_start=-1)
+    assert all("%nsmid" not in s for s in small)
+    prod, _ = sources(workloads.rqc_text(5, 6, 8, seed=3), product_start=1)
+    assert "%nsmid" not in prod[0]
+    monkeypatch.setenv("QSV_JIT_STAGGER", "0")
+    off, _ = sources(workloads.qft_text(30, round_trip=False), product_start=-1)
+    assert all("%nsmid" not in s for s in off)
