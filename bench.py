@@ -375,7 +375,12 @@ def run_traj(args) -> None:
     bc = args.batch_clean
     topts = planner_options(args)
     run_trajectories(prog, 1e-3, min(8, n_traj), base_seed=SEED, device=local, rank=rank, world=world,
-                     batch_clean=bc, options=topts)  # warm-up (compiles the clean plan, and the batched one if bc > 0)
+                     batch_clean=bc, options=topts)  # compiles the clean plan (and the batched one if bc > 0)
+    # one whole untimed batch: the first batch of a process on a fresh box measured 0.94-1.20 s
+    # against 0.77-0.79 s for every later one (host-side first-run costs of the launch loop)
+    run_trajectories(prog, 1e-3, n_traj, base_seed=SEED, device=local, rank=rank, world=world,
+                     streams=int(os.environ.get("QSV_TRAJ_STREAMS", "2")), dedup=args.dedup, batch_clean=bc,
+                     options=topts)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
